@@ -1,0 +1,147 @@
+/*
+ * flatquant.h -- C ABI of the B200-native FlatQuant online hot path
+ * (arXiv 2410.09426, "FlatQuant: Flatness Matters for LLM Quantization").
+ *
+ * One linear layer Y = X W^T executed as
+ *
+ *   fq_transform_quant   a1-a5: y_t = vec_row(P1^T . reshape(x_t, n1, n2) . P2)   (Eq.3)
+ *                               s_t = alpha . max|y_t| / 7                       (Eq.1 PAPER.md:90-93;
+ *                               q   = clamp(rint(y / s_t), -8, 7), packed int4    PAPER.md:258-259, 367)
+ *   fq_w4a4_linear       a6-a7: acc = Q_a Q_w^T (int32, exact), Y = acc . s_a[t] . s_w[o]
+ *                               (INT4 GEMM PAPER.md:315, per-channel weights PAPER.md:367)
+ *
+ * Conventions common to every entry point
+ *  - Pointers named x, p1, p2, q, scale, qa, sa, qw, sw, y, acc are DEVICE pointers
+ *    (cudaMalloc / torch CUDA storage) unless the name ends in _host.  All buffers are
+ *    caller-allocated; the library never allocates, frees or retains them.  They must stay
+ *    valid until the work queued on `stream` has completed.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Every call
+ *    is asynchronous with respect to the host unless stated otherwise.
+ *  - Argument validation is synchronous: on any error nothing is launched and a non-zero
+ *    fq_status is returned.  T == 0 returns FQ_OK without launching.  A failed launch
+ *    returns FQ_ECUDA; fq_last_cuda_error() returns the cudaError_t value.  Device faults
+ *    surface at the caller's next synchronisation, as with any CUDA library.
+ *  - Layouts are row-major.  INT4 codes are two's-complement nibbles, element 2i in the
+ *    LOW nibble of byte i of its row (reading R7).  Device pointers must be
+ *    16-byte aligned and row strides multiples of 16 bytes.
+ *  - Stateless and re-entrant; per-device kernel attributes are set once, thread-safely.
+ *  - Non-finite inputs give unspecified codes (the oracle's precondition is finite x).
+ */
+#ifndef FLATQUANT_H_
+#define FLATQUANT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FQ_ABI_VERSION 1
+
+typedef enum {
+  FQ_OK = 0,
+  FQ_EINVAL = 1,   /* null pointer, bad enum, alpha outside (0, 1], negative size          */
+  FQ_ESHAPE = 2,   /* n1*n2 != K, odd K, K % 32 != 0 for the GEMM, misaligned pointer/stride */
+  FQ_ENOTSUP = 3,  /* well-formed but no kernel for it (e.g. n1 or n2 > 256, FQ_ASYM)       */
+  FQ_ECUDA = 4     /* a CUDA launch/runtime call failed; see fq_last_cuda_error()            */
+} fq_status;
+
+typedef enum { FQ_F16 = 0, FQ_BF16 = 1 } fq_dtype;
+
+/* FQ_SYM: per-token symmetric (the paper's setting).  FQ_ASYM is reserved
+ * for the asymmetric mode and returns FQ_ENOTSUP in ABI v1. */
+typedef enum { FQ_SYM = 0, FQ_ASYM = 1 } fq_qmode;
+
+/* ---------------------------------------------------------------------------------------
+ * fq_transform_quant -- fused Kronecker transform + clip + per-token INT4 quantize + pack.
+ *   PAPER.md:236-244 (Eq.3, activation factor Q(P1^T x_1 X~ x_2 P2))
+ *   (clipping ratio after the transform), PAPER.md:367 (per-token symmetric), Eq.1.
+ *
+ *   x      [T, ldx] elements of x_dtype; row t holds x_t (n = n1*n2 used), ldx >= n,
+ *          ldx*elemsize % 16 == 0.  Viewed as V_t = reshape(x_t, n1, n2) in C order.
+ *   p1     [n1, n1] row-major, x_dtype.     p2 [n2, n2] row-major, x_dtype.
+ *   alpha  post-sigmoid clipping ratio in (0, 1]; 1 = no clipping.
+ *   qmode  FQ_SYM (FQ_ASYM -> FQ_ENOTSUP in v1).
+ *   q      [T, n/2] uint8 packed codes (output).     scale [T] fp32 (output), s_t.
+ *   zero   must be NULL for FQ_SYM.
+ *   Supported: n1, n2 >= 1, n even, n1, n2 <= 256 (tensor-core kernel when n1 % 16 == 0
+ *   and n2 % 16 == 0; a CUDA-core kernel otherwise).
+ * ------------------------------------------------------------------------------------- */
+fq_status fq_transform_quant(const void* x, int32_t x_dtype, int64_t T, int64_t ldx,
+                             int32_t n1, int32_t n2, const void* p1, const void* p2,
+                             float alpha, int32_t qmode, uint8_t* q, float* scale,
+                             int8_t* zero, void* stream);
+
+/* fq_transform_f32 -- same kernel as fq_transform_quant, additionally exporting the
+ * transformed activations y [T, n] fp32 (before clipping/quantization) so that the
+ * "transformed activations rel 1e-3" bar can be checked on the production code path.
+ * q/scale may be NULL (then only y is written... q and scale are still computed). */
+fq_status fq_transform_f32(const void* x, int32_t x_dtype, int64_t T, int64_t ldx,
+                           int32_t n1, int32_t n2, const void* p1, const void* p2,
+                           float alpha, uint8_t* q, float* scale, float* y, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * fq_w4a4_linear -- W4A4 GEMM + dequant epilogue.
+ *   Y[t, o] = cvt_rn( float(acc[t, o]) * sa[t] * sw[o] ),  acc = sum_k qa[t,k] qw[o,k]
+ *   PAPER.md:241 (weights pre-transformed offline, P1^{-1} x_1 W~ x_2 P2^{-T})
+ *   (INT4 GEMM), PAPER.md:367 (per-token x per-channel scales).
+ *
+ *   qa [T, K/2] uint8 packed activation codes (from fq_transform_quant), sa [T] fp32.
+ *   qw [N, K/2] uint8 packed weight codes (K contiguous, same nibble order), sw [N] fp32.
+ *   za, colsum_w: asymmetric-mode hooks; must be NULL in ABI v1.
+ *   y  [T, N] of y_dtype (FQ_F16 or FQ_BF16), row-major.
+ *   Requires K % 32 == 0 and N % 8 == 0.  Exact integer accumulation (|acc| <= 64 K < 2^31).
+ * ------------------------------------------------------------------------------------- */
+fq_status fq_w4a4_linear(const uint8_t* qa, const float* sa, const int8_t* za, int64_t T,
+                         int32_t K, const uint8_t* qw, const float* sw,
+                         const int32_t* colsum_w, int32_t N, void* y, int32_t y_dtype,
+                         void* stream);
+
+/* fq_w4a4_gemm_i32 -- the same GEMM kernel exporting the raw int32 accumulators
+ * acc [T, N] (bit-exactness bar).  Same shape requirements as fq_w4a4_linear. */
+fq_status fq_w4a4_gemm_i32(const uint8_t* qa, int64_t T, int32_t K, const uint8_t* qw,
+                           int32_t N, int32_t* acc, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * fq_flatquant_linear -- the whole hot path a1-a7 for one linear layer: transform+quant of
+ * x into the caller's workspace (q_ws [T, n/2] uint8, s_ws [T] fp32), then the W4A4 GEMM.
+ * Equivalent to fq_transform_quant followed by fq_w4a4_linear on the same stream.
+ * ------------------------------------------------------------------------------------- */
+fq_status fq_flatquant_linear(const void* x, int32_t x_dtype, int64_t T, int32_t n1,
+                              int32_t n2, const void* p1, const void* p2, float alpha,
+                              const uint8_t* qw, const float* sw, int32_t N, void* y,
+                              int32_t y_dtype, uint8_t* q_ws, float* s_ws, void* stream);
+
+/* fq_flatquant_linear_host -- as fq_flatquant_linear but x_host [T, n] and y_host [T, N]
+ * are HOST buffers (page-locked strongly recommended): copies x_host -> x_dev, runs the hot
+ * path, copies y_dev -> y_host, all on `stream`, then synchronises the stream before
+ * returning (so y_host is valid on return).  x_dev/y_dev are caller-provided device staging
+ * buffers of the same shapes. */
+fq_status fq_flatquant_linear_host(const void* x_host, void* x_dev, int32_t x_dtype,
+                                   int64_t T, int32_t n1, int32_t n2, const void* p1,
+                                   const void* p2, float alpha, const uint8_t* qw,
+                                   const float* sw, int32_t N, void* y_host, void* y_dev,
+                                   int32_t y_dtype, uint8_t* q_ws, float* s_ws, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Helpers
+ * ------------------------------------------------------------------------------------- */
+/* (n1, n2) = argmin(n1 + n2) s.t. n1 n2 = n, n1 <= n2.  Host-only, sync. */
+fq_status fq_choose_decomposition(int64_t n, int32_t* n1, int32_t* n2);
+
+/* Selects the GEMM implementation for subsequent calls in this process (testing aid):
+ * 0 = default (tcgen05 kind::i8 where available), 1 = legacy mma.sync cross-check kernel.
+ * Returns FQ_EINVAL for unknown values. */
+fq_status fq_set_gemm_impl(int32_t impl);
+
+/* Number of kernel launches issued by this library since process start (bench accounting). */
+uint64_t fq_launch_count(void);
+
+const char* fq_status_string(int32_t status);
+int32_t fq_abi_version(void);
+int32_t fq_last_cuda_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLATQUANT_H_ */

@@ -1,0 +1,168 @@
+"""Python face of the C ABI: the same entry points as include/flatquant.h, taking torch tensors.
+
+Marshalling only (pointers, sizes, dtypes, the current CUDA stream); the work runs in the CUDA
+kernels of libflatquant.so.  Allocating conveniences (`transform_quant`, `w4a4_linear`, ...)
+create outputs with torch and then call the same entry points.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import FQ_BF16, FQ_F16, FQ_SYM, check, load
+
+__all__ = [
+    "fq_transform_quant", "fq_transform_f32", "fq_w4a4_linear", "fq_w4a4_gemm_i32", "fq_flatquant_linear",
+    "fq_flatquant_linear_host", "fq_choose_decomposition", "fq_set_gemm_impl", "fq_launch_count",
+    "fq_abi_version", "transform_quant", "transform_f32", "w4a4_linear", "w4a4_gemm_i32", "prepare_weight",
+    "flatquant_linear",
+]
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _fq_dtype(dt: torch.dtype) -> int:
+    if dt == torch.float16:
+        return FQ_F16
+    if dt == torch.bfloat16:
+        return FQ_BF16
+    raise TypeError(f"unsupported dtype {dt} (fp16 or bf16)")
+
+
+def _cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("all tensors must be CUDA tensors (there is no CPU path)")
+
+
+# ------------------------------------------------------------------ raw entry points
+def fq_transform_quant(x, n1, n2, p1, p2, alpha, q, scale, zero=None, qmode=FQ_SYM, stream=None):
+    _cuda(x, p1, p2, q, scale, zero)
+    assert x.dim() == 2 and x.stride(1) == 1
+    st = load().fq_transform_quant(_ptr(x), _fq_dtype(x.dtype), x.shape[0], x.stride(0), n1, n2, _ptr(p1),
+                                   _ptr(p2), float(alpha), qmode, _ptr(q), _ptr(scale), _ptr(zero), _stream(stream))
+    check("fq_transform_quant", st)
+
+
+def fq_transform_f32(x, n1, n2, p1, p2, alpha, q, scale, y, stream=None):
+    _cuda(x, p1, p2, q, scale, y)
+    assert x.dim() == 2 and x.stride(1) == 1
+    st = load().fq_transform_f32(_ptr(x), _fq_dtype(x.dtype), x.shape[0], x.stride(0), n1, n2, _ptr(p1), _ptr(p2),
+                                 float(alpha), _ptr(q), _ptr(scale), _ptr(y), _stream(stream))
+    check("fq_transform_f32", st)
+
+
+def fq_w4a4_linear(qa, sa, qw, sw, y, K=None, za=None, colsum_w=None, stream=None):
+    _cuda(qa, sa, qw, sw, y, za, colsum_w)
+    K = qa.shape[1] * 2 if K is None else K
+    st = load().fq_w4a4_linear(_ptr(qa), _ptr(sa), _ptr(za), qa.shape[0], K, _ptr(qw), _ptr(sw), _ptr(colsum_w),
+                               qw.shape[0], _ptr(y), _fq_dtype(y.dtype), _stream(stream))
+    check("fq_w4a4_linear", st)
+
+
+def fq_w4a4_gemm_i32(qa, qw, acc, K=None, stream=None):
+    _cuda(qa, qw, acc)
+    K = qa.shape[1] * 2 if K is None else K
+    st = load().fq_w4a4_gemm_i32(_ptr(qa), qa.shape[0], K, _ptr(qw), qw.shape[0], _ptr(acc), _stream(stream))
+    check("fq_w4a4_gemm_i32", st)
+
+
+def fq_flatquant_linear(x, n1, n2, p1, p2, alpha, qw, sw, y, q_ws, s_ws, stream=None):
+    _cuda(x, p1, p2, qw, sw, y, q_ws, s_ws)
+    st = load().fq_flatquant_linear(_ptr(x), _fq_dtype(x.dtype), x.shape[0], n1, n2, _ptr(p1), _ptr(p2),
+                                    float(alpha), _ptr(qw), _ptr(sw), qw.shape[0], _ptr(y), _fq_dtype(y.dtype),
+                                    _ptr(q_ws), _ptr(s_ws), _stream(stream))
+    check("fq_flatquant_linear", st)
+
+
+def fq_flatquant_linear_host(x_host, x_dev, n1, n2, p1, p2, alpha, qw, sw, y_host, y_dev, q_ws, s_ws, stream=None):
+    """x_host / y_host are CPU tensors (pinned recommended); synchronises the stream."""
+    _cuda(x_dev, p1, p2, qw, sw, y_dev, q_ws, s_ws)
+    if x_host.is_cuda or y_host.is_cuda:
+        raise ValueError("x_host and y_host must be host tensors")
+    st = load().fq_flatquant_linear_host(_ptr(x_host), _ptr(x_dev), _fq_dtype(x_dev.dtype), x_dev.shape[0], n1, n2,
+                                         _ptr(p1), _ptr(p2), float(alpha), _ptr(qw), _ptr(sw), qw.shape[0],
+                                         _ptr(y_host), _ptr(y_dev), _fq_dtype(y_dev.dtype), _ptr(q_ws), _ptr(s_ws),
+                                         _stream(stream))
+    check("fq_flatquant_linear_host", st)
+
+
+def fq_choose_decomposition(n: int) -> tuple[int, int]:
+    a, b = ctypes.c_int32(), ctypes.c_int32()
+    check("fq_choose_decomposition", load().fq_choose_decomposition(int(n), ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
+
+
+def fq_set_gemm_impl(impl: int) -> None:
+    check("fq_set_gemm_impl", load().fq_set_gemm_impl(int(impl)))
+
+
+def fq_launch_count() -> int:
+    return int(load().fq_launch_count())
+
+
+def fq_abi_version() -> int:
+    return int(load().fq_abi_version())
+
+
+# ------------------------------------------------------------------ allocating conveniences
+def transform_quant(x, n1, n2, p1, p2, alpha=1.0, stream=None):
+    T = x.shape[0]
+    q = torch.empty((T, n1 * n2 // 2), dtype=torch.uint8, device=x.device)
+    s = torch.empty((T,), dtype=torch.float32, device=x.device)
+    fq_transform_quant(x, n1, n2, p1, p2, alpha, q, s, stream=stream)
+    return q, s
+
+
+def transform_f32(x, n1, n2, p1, p2, alpha=1.0, stream=None):
+    T = x.shape[0]
+    q = torch.empty((T, n1 * n2 // 2), dtype=torch.uint8, device=x.device)
+    s = torch.empty((T,), dtype=torch.float32, device=x.device)
+    y = torch.empty((T, n1 * n2), dtype=torch.float32, device=x.device)
+    fq_transform_f32(x, n1, n2, p1, p2, alpha, q, s, y, stream=stream)
+    return q, s, y
+
+
+def w4a4_linear(qa, sa, qw, sw, out_dtype=torch.float16, stream=None):
+    y = torch.empty((qa.shape[0], qw.shape[0]), dtype=out_dtype, device=qa.device)
+    fq_w4a4_linear(qa, sa, qw, sw, y, stream=stream)
+    return y
+
+
+def w4a4_gemm_i32(qa, qw, stream=None):
+    acc = torch.empty((qa.shape[0], qw.shape[0]), dtype=torch.int32, device=qa.device)
+    fq_w4a4_gemm_i32(qa, qw, acc, stream=stream)
+    return acc
+
+
+def prepare_weight(w, n1, n2, p1, p2, alpha_w=1.0, stream=None):
+    """Offline weight side of Eq.3: W'_o = P1^{-1} W~_o P2^{-T}, quantized per
+    output channel.  This IS the activation kernel applied with
+    (P1^{-T}, P2^{-T}): (P1^{-T})^T W~ (P2^{-T}).  The two small inverses are computed once
+    on the host in float64 (offline preparation, not the hot path); the transform and the
+    per-channel quantization run in fq_transform_quant."""
+    p1i_t = torch.linalg.inv(p1.detach().to("cpu", torch.float64)).T.contiguous()
+    p2i_t = torch.linalg.inv(p2.detach().to("cpu", torch.float64)).T.contiguous()
+    p1i_t = p1i_t.to(device=w.device, dtype=w.dtype)
+    p2i_t = p2i_t.to(device=w.device, dtype=w.dtype)
+    return transform_quant(w, n1, n2, p1i_t, p2i_t, alpha_w, stream=stream)
+
+
+def flatquant_linear(x, n1, n2, p1, p2, alpha, qw, sw, out_dtype=torch.float16, stream=None):
+    """Whole hot path for one linear: returns Y [T, N]."""
+    T = x.shape[0]
+    y = torch.empty((T, qw.shape[0]), dtype=out_dtype, device=x.device)
+    q_ws = torch.empty((T, n1 * n2 // 2), dtype=torch.uint8, device=x.device)
+    s_ws = torch.empty((T,), dtype=torch.float32, device=x.device)
+    fq_flatquant_linear(x, n1, n2, p1, p2, alpha, qw, sw, y, q_ws, s_ws, stream=stream)
+    return y

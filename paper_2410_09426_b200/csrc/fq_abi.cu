@@ -1,0 +1,228 @@
+// fq_abi.cu -- the extern "C" boundary declared in include/flatquant.h: argument validation,
+// kernel selection and launch.  No computation happens here; every step runs in the kernels.
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <cuda_runtime.h>
+#include "../../include/flatquant.h"
+#include "fq_internal.h"
+
+namespace fq {
+
+static std::atomic<uint64_t> g_launches{0};
+static std::atomic<int> g_last_cuda_error{0};
+static std::atomic<int> g_gemm_impl{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cached[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = n > 0 ? n : 1;
+  }
+  return cached[dev];
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+static fq_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return FQ_OK;
+  g_last_cuda_error.store(int(e));
+  return FQ_ECUDA;
+}
+
+static fq_status validate_tq(const void* x, int32_t x_dtype, int64_t T, int64_t ldx, int32_t n1, int32_t n2,
+                             const void* p1, const void* p2, float alpha, const uint8_t* q,
+                             const float* scale) {
+  if (x_dtype != FQ_F16 && x_dtype != FQ_BF16) return FQ_EINVAL;
+  if (T < 0 || n1 < 1 || n2 < 1) return FQ_EINVAL;
+  if (!(alpha > 0.0f && alpha <= 1.0f)) return FQ_EINVAL;   // also rejects NaN
+  if (T == 0) return FQ_OK;
+  if (!x || !p1 || !p2 || !q || !scale) return FQ_EINVAL;
+  const int64_t n = int64_t(n1) * n2;
+  if (n % 2 != 0) return FQ_ESHAPE;
+  if (ldx < n) return FQ_ESHAPE;
+  if ((ldx * 2) % 16 != 0) return FQ_ESHAPE;
+  if (!aligned16(x) || !aligned16(q) || !aligned16(p1) || !aligned16(p2)) return FQ_ESHAPE;
+  if (n1 > 256 || n2 > 256) return FQ_ENOTSUP;
+  return FQ_OK;
+}
+
+static fq_status run_tq(const void* x, int32_t x_dtype, int64_t T, int64_t ldx, int32_t n1, int32_t n2,
+                        const void* p1, const void* p2, float alpha, uint8_t* q, float* scale, float* y,
+                        void* stream) {
+  TQArgs a{};
+  a.x = x;
+  a.T = T;
+  a.ldx = ldx;
+  a.n1 = n1;
+  a.n2 = n2;
+  a.p1 = p1;
+  a.p2 = p2;
+  a.alpha = alpha;
+  a.q = q;
+  a.scale = scale;
+  a.y = y;
+  a.bf16 = (x_dtype == FQ_BF16);
+  a.force_simt = false;
+  a.stream = static_cast<cudaStream_t>(stream);
+  const bool tc = (n1 % 16 == 0) && (n2 % 16 == 0);
+  if (!tc && !tq_simt_supported(n1, n2)) return FQ_ENOTSUP;
+  return cuda_status(transform_quant_launch(a));
+}
+
+static fq_status validate_gemm(const uint8_t* qa, int64_t T, int32_t K, const uint8_t* qw, int32_t N,
+                               const void* y) {
+  if (T < 0 || K < 0 || N < 0) return FQ_EINVAL;
+  if (T == 0 || N == 0) return FQ_OK;
+  if (!qa || !qw || !y) return FQ_EINVAL;
+  if (K == 0 || K % 32 != 0 || N % 8 != 0) return FQ_ESHAPE;
+  if (!aligned16(qa) || !aligned16(qw) || !aligned16(y)) return FQ_ESHAPE;
+  if (K > 131072) return FQ_ENOTSUP;
+  if (T > (int64_t(1) << 30)) return FQ_ENOTSUP;
+  return FQ_OK;
+}
+
+static fq_status run_gemm(const uint8_t* qa, const float* sa, int64_t T, int32_t K, const uint8_t* qw,
+                          const float* sw, int32_t N, void* y, bool y_bf16, bool out_i32, void* stream) {
+  GemmArgs a{};
+  a.qa = qa;
+  a.sa = sa;
+  a.T = T;
+  a.K = K;
+  a.qw = qw;
+  a.sw = sw;
+  a.N = N;
+  a.y = y;
+  a.y_bf16 = y_bf16;
+  a.out_i32 = out_i32;
+  a.stream = static_cast<cudaStream_t>(stream);
+  if (g_gemm_impl.load() == 1 || !gemm_tc05_supported(a)) return cuda_status(gemm_mma_launch(a));
+  return cuda_status(gemm_tc05_launch(a));
+}
+
+}  // namespace fq
+
+using namespace fq;
+
+extern "C" {
+
+fq_status fq_transform_quant(const void* x, int32_t x_dtype, int64_t T, int64_t ldx, int32_t n1, int32_t n2,
+                             const void* p1, const void* p2, float alpha, int32_t qmode, uint8_t* q,
+                             float* scale, int8_t* zero, void* stream) {
+  if (qmode != FQ_SYM && qmode != FQ_ASYM) return FQ_EINVAL;
+  if (qmode == FQ_ASYM) return FQ_ENOTSUP;
+  if (zero != nullptr) return FQ_EINVAL;
+  fq_status s = validate_tq(x, x_dtype, T, ldx, n1, n2, p1, p2, alpha, q, scale);
+  if (s != FQ_OK || T == 0) return s;
+  return run_tq(x, x_dtype, T, ldx, n1, n2, p1, p2, alpha, q, scale, nullptr, stream);
+}
+
+fq_status fq_transform_f32(const void* x, int32_t x_dtype, int64_t T, int64_t ldx, int32_t n1, int32_t n2,
+                           const void* p1, const void* p2, float alpha, uint8_t* q, float* scale, float* y,
+                           void* stream) {
+  fq_status s = validate_tq(x, x_dtype, T, ldx, n1, n2, p1, p2, alpha, q, scale);
+  if (s != FQ_OK || T == 0) return s;
+  if (!y) return FQ_EINVAL;
+  if (!aligned16(y)) return FQ_ESHAPE;
+  return run_tq(x, x_dtype, T, ldx, n1, n2, p1, p2, alpha, q, scale, y, stream);
+}
+
+fq_status fq_w4a4_linear(const uint8_t* qa, const float* sa, const int8_t* za, int64_t T, int32_t K,
+                         const uint8_t* qw, const float* sw, const int32_t* colsum_w, int32_t N, void* y,
+                         int32_t y_dtype, void* stream) {
+  if (y_dtype != FQ_F16 && y_dtype != FQ_BF16) return FQ_EINVAL;
+  if (za != nullptr || colsum_w != nullptr) return FQ_ENOTSUP;
+  fq_status s = validate_gemm(qa, T, K, qw, N, y);
+  if (s != FQ_OK || T == 0 || N == 0) return s;
+  if (!sa || !sw) return FQ_EINVAL;
+  if (!aligned16(sw)) return FQ_ESHAPE;
+  return run_gemm(qa, sa, T, K, qw, sw, N, y, y_dtype == FQ_BF16, false, stream);
+}
+
+fq_status fq_w4a4_gemm_i32(const uint8_t* qa, int64_t T, int32_t K, const uint8_t* qw, int32_t N,
+                           int32_t* acc, void* stream) {
+  fq_status s = validate_gemm(qa, T, K, qw, N, acc);
+  if (s != FQ_OK || T == 0 || N == 0) return s;
+  return run_gemm(qa, nullptr, T, K, qw, nullptr, N, acc, false, true, stream);
+}
+
+fq_status fq_flatquant_linear(const void* x, int32_t x_dtype, int64_t T, int32_t n1, int32_t n2,
+                              const void* p1, const void* p2, float alpha, const uint8_t* qw, const float* sw,
+                              int32_t N, void* y, int32_t y_dtype, uint8_t* q_ws, float* s_ws, void* stream) {
+  const int64_t n = int64_t(n1) * n2;
+  if (n > INT32_MAX) return FQ_ESHAPE;
+  if (y_dtype != FQ_F16 && y_dtype != FQ_BF16) return FQ_EINVAL;
+  fq_status s = validate_tq(x, x_dtype, T, n, n1, n2, p1, p2, alpha, q_ws, s_ws);
+  if (s != FQ_OK || T == 0) return s;
+  s = validate_gemm(q_ws, T, int32_t(n), qw, N, y);
+  if (s != FQ_OK || N == 0) return s;
+  if (!sw) return FQ_EINVAL;
+  if (!aligned16(sw)) return FQ_ESHAPE;
+  s = run_tq(x, x_dtype, T, n, n1, n2, p1, p2, alpha, q_ws, s_ws, nullptr, stream);
+  if (s != FQ_OK) return s;
+  return run_gemm(q_ws, s_ws, T, int32_t(n), qw, sw, N, y, y_dtype == FQ_BF16, false, stream);
+}
+
+fq_status fq_flatquant_linear_host(const void* x_host, void* x_dev, int32_t x_dtype, int64_t T, int32_t n1,
+                                   int32_t n2, const void* p1, const void* p2, float alpha, const uint8_t* qw,
+                                   const float* sw, int32_t N, void* y_host, void* y_dev, int32_t y_dtype,
+                                   uint8_t* q_ws, float* s_ws, void* stream) {
+  if (T < 0) return FQ_EINVAL;
+  if (T == 0) return FQ_OK;
+  if (!x_host || !x_dev || !y_host || !y_dev) return FQ_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t xbytes = size_t(T) * size_t(n1) * size_t(n2) * 2;
+  const size_t ybytes = size_t(T) * size_t(N) * 2;
+  fq_status s = cuda_status(cudaMemcpyAsync(x_dev, x_host, xbytes, cudaMemcpyHostToDevice, st));
+  if (s != FQ_OK) return s;
+  s = fq_flatquant_linear(x_dev, x_dtype, T, n1, n2, p1, p2, alpha, qw, sw, N, y_dev, y_dtype, q_ws, s_ws, stream);
+  if (s != FQ_OK) return s;
+  s = cuda_status(cudaMemcpyAsync(y_host, y_dev, ybytes, cudaMemcpyDeviceToHost, st));
+  if (s != FQ_OK) return s;
+  return cuda_status(cudaStreamSynchronize(st));
+}
+
+fq_status fq_choose_decomposition(int64_t n, int32_t* n1, int32_t* n2) {
+  if (n < 1 || !n1 || !n2) return FQ_EINVAL;
+  if (n > INT32_MAX) return FQ_ENOTSUP;
+  int64_t b1 = 1, b2 = n;
+  for (int64_t a = 1; a * a <= n; ++a)
+    if (n % a == 0 && a + n / a < b1 + b2) {
+      b1 = a;
+      b2 = n / a;
+    }
+  *n1 = int32_t(b1);
+  *n2 = int32_t(b2);
+  return FQ_OK;
+}
+
+fq_status fq_set_gemm_impl(int32_t impl) {
+  if (impl != 0 && impl != 1) return FQ_EINVAL;
+  g_gemm_impl.store(impl);
+  return FQ_OK;
+}
+
+uint64_t fq_launch_count(void) { return g_launches.load(); }
+
+const char* fq_status_string(int32_t status) {
+  switch (status) {
+    case FQ_OK: return "FQ_OK";
+    case FQ_EINVAL: return "FQ_EINVAL: invalid argument";
+    case FQ_ESHAPE: return "FQ_ESHAPE: unsupported shape, stride or alignment";
+    case FQ_ENOTSUP: return "FQ_ENOTSUP: no kernel for this configuration";
+    case FQ_ECUDA: return "FQ_ECUDA: CUDA error (see fq_last_cuda_error)";
+    default: return "unknown fq_status";
+  }
+}
+
+int32_t fq_abi_version(void) { return FQ_ABI_VERSION; }
+int32_t fq_last_cuda_error(void) { return g_last_cuda_error.load(); }
+
+}  // extern "C"

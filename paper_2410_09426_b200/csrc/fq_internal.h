@@ -1,0 +1,48 @@
+// fq_internal.h -- internal (non-ABI) declarations shared by the library's translation units.
+#pragma once
+#include <cstdint>
+#include <algorithm>
+#include <cuda_runtime.h>
+
+namespace fq {
+
+struct TQArgs {
+  const void* x;
+  int64_t T, ldx;
+  int n1, n2;
+  const void* p1;
+  const void* p2;
+  float alpha;
+  uint8_t* q;
+  float* scale;
+  float* y;         // optional fp32 export of the transformed activations (debug / parity)
+  bool bf16;
+  bool force_simt;
+  cudaStream_t stream;
+};
+
+struct GemmArgs {
+  const uint8_t* qa;
+  const float* sa;
+  int64_t T;
+  int K;
+  const uint8_t* qw;
+  const float* sw;
+  int N;
+  void* y;          // fp16/bf16 output, or int32 accumulators when out_i32
+  bool y_bf16;
+  bool out_i32;
+  cudaStream_t stream;
+};
+
+int num_sms();
+void count_launch();
+
+cudaError_t transform_quant_launch(const TQArgs& a);
+bool tq_simt_supported(int n1, int n2);
+
+cudaError_t gemm_mma_launch(const GemmArgs& a);      // legacy mma.sync cross-check kernel
+cudaError_t gemm_tc05_launch(const GemmArgs& a);     // tcgen05 kind::i8 kernel
+bool gemm_tc05_supported(const GemmArgs& a);
+
+}  // namespace fq

@@ -44,23 +44,42 @@ def rng(seed: int, tag: str, *extra) -> np.random.Generator:
     return np.random.Generator(np.random.Philox(key=_key(seed, tag, *extra)))
 
 
+ROW_BLOCK = 256
+
+
 def activations(T: int, n: int, seed: int = 0, tag: str = "x", dtype=np.float16,
                 outlier_frac: float = 0.01, outlier_scale: float = 50.0,
                 pivot_channels: int = 4, pivot_scale: float = 400.0,
-                clamp: float = 60000.0) -> np.ndarray:
-    """Gaussian activations with channel outliers and one pivot token (token 0)."""
-    g = rng(seed, tag + "/x", T, n)
-    x = g.standard_normal((T, n), dtype=np.float64)
-    if n > 0 and outlier_frac > 0:
-        go = rng(seed, tag + "/outlier_channels", n)  # fixed per layer, independent of T
-        k = max(1, int(round(outlier_frac * n)))
-        ch = go.choice(n, size=k, replace=False)
-        x[:, ch] *= outlier_scale
-        if T > 0 and pivot_channels > 0:
-            pc = go.choice(n, size=min(pivot_channels, n), replace=False)
-            x[0, pc] *= pivot_scale
-    np.clip(x, -clamp, clamp, out=x)
-    return x.astype(dtype)
+                clamp: float = 60000.0, rows=None) -> np.ndarray:
+    """Gaussian activations with channel outliers and one pivot token (token 0).
+
+    Rows are drawn in blocks of ROW_BLOCK from streams keyed by (seed, tag, n, block), so
+    row t is the same for every T and any subset `rows` can be regenerated on its own
+    (the oracle re-derives sampled tokens of a large workload this way).
+    """
+    idx = np.arange(T) if rows is None else np.asarray(rows, dtype=np.int64)
+    out = np.empty((idx.size, n), dtype=dtype)
+    if n == 0 or idx.size == 0:
+        return out
+    go = rng(seed, tag + "/outlier_channels", n)      # fixed per layer
+    k = max(1, int(round(outlier_frac * n))) if outlier_frac > 0 else 0
+    ch = go.choice(n, size=k, replace=False) if k else np.zeros(0, np.int64)
+    pc = go.choice(n, size=min(pivot_channels, n), replace=False) if pivot_channels > 0 else np.zeros(0, np.int64)
+    blocks = np.unique(idx // ROW_BLOCK)
+    pos = {}
+    for i, r in enumerate(idx):
+        pos.setdefault(int(r) // ROW_BLOCK, []).append((i, int(r) % ROW_BLOCK))
+    for b in blocks:
+        g = rng(seed, tag + "/x", n, int(b))
+        blk = g.standard_normal((ROW_BLOCK, n), dtype=np.float32)
+        if k:
+            blk[:, ch] *= outlier_scale
+        if b == 0 and pc.size:
+            blk[0, pc] *= pivot_scale
+        np.clip(blk, -clamp, clamp, out=blk)
+        sel = pos[int(b)]
+        out[[i for i, _ in sel]] = blk[[j for _, j in sel]].astype(dtype)
+    return out
 
 
 def _haar_orthogonal(g: np.random.Generator, n: int) -> np.ndarray:

@@ -1,0 +1,58 @@
+"""Parity helpers: compare the CUDA path (through the C ABI) with the float64 oracle.
+
+The four bars (BASELINE.json north_star; metrics defined in SURVEY.md §8(c)):
+  1. int32 GEMM accumulators bit-exact given identical codes;
+  2. transformed activations: max_t ||y_gpu,t - y_ora,t||_inf / ||y_ora,t||_inf <= 1e-3;
+  3. codes equal except at oracle near-ties (|frac(v) - 1/2| <= TAU, v = y/s in code units),
+     where they may differ by exactly +-1, in <= 0.1% of the elements;
+  4. outputs: ||Y_gpu - Y_ora||_F / ||Y_ora||_F <= 2e-2 and per-token max-normalised <= 2e-2.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle as O
+
+Y_REL = 1e-3          # bar 2
+TAU = 1e-2            # bar 3 near-tie window (code units) for fp16 intermediates
+MISMATCH_FRAC = 1e-3  # bar 3
+OUT_REL = 2e-2        # bar 4
+SCALE_REL = 1e-3      # scales follow from bar 2 (s = alpha max|y| / 7)
+
+
+def per_token_rel(a: np.ndarray, ref: np.ndarray) -> np.ndarray:
+    den = np.abs(ref).max(axis=1)
+    num = np.abs(a - ref).max(axis=1)
+    return np.where(den > 0, num / np.where(den > 0, den, 1.0), num)
+
+
+def check_transform(q_packed, s_gpu, y_gpu, y_ora, q_ora, s_ora, tau=TAU, label=""):
+    """Bars 2 and 3 (+ scales).  Returns a dict of statistics."""
+    stats = {}
+    if y_gpu is not None:
+        rel = per_token_rel(np.asarray(y_gpu, np.float64), y_ora)
+        stats["y_rel_max"] = float(rel.max(initial=0.0))
+        assert stats["y_rel_max"] <= Y_REL, f"{label} transformed activations rel {stats['y_rel_max']:.3e}"
+    s_gpu = np.asarray(s_gpu, np.float64)
+    srel = np.abs(s_gpu - s_ora) / s_ora
+    stats["scale_rel_max"] = float(srel.max(initial=0.0))
+    assert stats["scale_rel_max"] <= SCALE_REL, f"{label} scales rel {stats['scale_rel_max']:.3e}"
+    qg = O.unpack_int4(np.asarray(q_packed))
+    diff = qg.astype(np.int16) - q_ora.astype(np.int16)
+    mism = diff != 0
+    stats["mismatch_frac"] = float(mism.mean()) if mism.size else 0.0
+    stats["mismatches"] = int(mism.sum())
+    assert np.all(np.abs(diff) <= 1), f"{label} code differs by more than 1"
+    tie = O.near_tie_mask(y_ora, s_ora, tau)
+    assert np.all(tie[mism]), f"{label} {int((mism & ~tie).sum())} code mismatches away from a near-tie"
+    assert stats["mismatch_frac"] <= MISMATCH_FRAC, f"{label} mismatch fraction {stats['mismatch_frac']:.2e}"
+    return stats
+
+
+def check_output(y_gpu, y_ora, label=""):
+    y_gpu = np.asarray(y_gpu, np.float64)
+    fro = np.linalg.norm(y_gpu - y_ora) / max(np.linalg.norm(y_ora), 1e-300)
+    tok = per_token_rel(y_gpu, y_ora).max(initial=0.0)
+    assert fro <= OUT_REL, f"{label} output rel Frobenius {fro:.3e}"
+    assert tok <= OUT_REL, f"{label} output per-token rel {tok:.3e}"
+    return {"out_rel_fro": float(fro), "out_rel_tok": float(tok)}

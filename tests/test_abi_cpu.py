@@ -1,0 +1,115 @@
+"""The C-ABI library loads on a CPU-only box, exports every symbol include/flatquant.h declares,
+and its host-side validation rejects bad arguments before any launch (no GPU needed)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import oracle as O
+import paper_2410_09426_b200 as fq
+from paper_2410_09426_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "flatquant.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(fq_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = fq.load()
+    names = declared_functions()
+    assert len(names) >= 12
+    for n in names:
+        assert hasattr(lib, n), f"{n} declared in flatquant.h but not exported"
+    # the binding covers the same set
+    assert set(names) == set(_lib.SIGNATURES)
+
+
+def test_abi_version_and_status_strings():
+    lib = fq.load()
+    assert fq.fq_abi_version() == 1
+    for s in range(5):
+        assert lib.fq_status_string(s).startswith(b"FQ_")
+    assert lib.fq_status_string(99) == b"unknown fq_status"
+
+
+def test_choose_decomposition_matches_oracle_rule():
+    for n in list(range(1, 2000)) + [4096, 8192, 11008, 14336, 28672, 57344]:
+        assert fq.fq_choose_decomposition(n) == O.choose_decomposition(n)
+
+
+VP = ctypes.c_void_p
+A16 = VP(0x1000)     # aligned fake device pointers: validation must reject before any use
+MIS = VP(0x1001)
+
+
+def tq(**kw):
+    args = dict(x=A16, dt=0, T=4, ldx=512, n1=16, n2=32, p1=A16, p2=A16, alpha=1.0, qmode=0, q=A16, s=A16,
+                zero=None, stream=None)
+    args.update(kw)
+    return fq.load().fq_transform_quant(args["x"], args["dt"], args["T"], args["ldx"], args["n1"], args["n2"],
+                                        args["p1"], args["p2"], args["alpha"], args["qmode"], args["q"], args["s"],
+                                        args["zero"], args["stream"])
+
+
+def test_transform_quant_validation():
+    assert tq(T=0) == _lib.FQ_OK                          # nothing to do, no launch
+    assert tq(alpha=0.0) == _lib.FQ_EINVAL
+    assert tq(alpha=1.5) == _lib.FQ_EINVAL
+    assert tq(alpha=float("nan")) == _lib.FQ_EINVAL
+    assert tq(dt=7) == _lib.FQ_EINVAL
+    assert tq(qmode=1) == _lib.FQ_ENOTSUP                 # asymmetric mode reserved (NEXT-1)
+    assert tq(qmode=3) == _lib.FQ_EINVAL
+    assert tq(zero=A16) == _lib.FQ_EINVAL
+    assert tq(x=None) == _lib.FQ_EINVAL
+    assert tq(q=None) == _lib.FQ_EINVAL
+    assert tq(T=-1) == _lib.FQ_EINVAL
+    assert tq(n1=3, n2=5, ldx=16) == _lib.FQ_ESHAPE        # odd n cannot be nibble-packed
+    assert tq(ldx=256) == _lib.FQ_ESHAPE                  # ldx < n
+    assert tq(ldx=516) == _lib.FQ_ESHAPE                  # row stride not 16-byte multiple
+    assert tq(x=MIS) == _lib.FQ_ESHAPE
+    assert tq(n1=512, n2=2, ldx=1024) == _lib.FQ_ENOTSUP
+
+
+def gemm(**kw):
+    a = dict(qa=A16, sa=A16, za=None, T=8, K=64, qw=A16, sw=A16, cs=None, N=16, y=A16, dt=0, stream=None)
+    a.update(kw)
+    return fq.load().fq_w4a4_linear(a["qa"], a["sa"], a["za"], a["T"], a["K"], a["qw"], a["sw"], a["cs"], a["N"],
+                                    a["y"], a["dt"], a["stream"])
+
+
+def test_w4a4_linear_validation():
+    assert gemm(T=0) == _lib.FQ_OK
+    assert gemm(N=0) == _lib.FQ_OK
+    assert gemm(K=48) == _lib.FQ_ESHAPE                   # K % 32
+    assert gemm(N=12) == _lib.FQ_ESHAPE                   # N % 8
+    assert gemm(qa=None) == _lib.FQ_EINVAL
+    assert gemm(sa=None) == _lib.FQ_EINVAL
+    assert gemm(dt=5) == _lib.FQ_EINVAL
+    assert gemm(za=A16) == _lib.FQ_ENOTSUP
+    assert gemm(cs=A16) == _lib.FQ_ENOTSUP
+    assert gemm(y=MIS) == _lib.FQ_ESHAPE
+    assert gemm(K=262144) == _lib.FQ_ENOTSUP
+    lib = fq.load()
+    assert lib.fq_w4a4_gemm_i32(A16, 8, 40, A16, 16, A16, None) == _lib.FQ_ESHAPE
+    assert lib.fq_w4a4_gemm_i32(None, 8, 64, A16, 16, A16, None) == _lib.FQ_EINVAL
+
+
+def test_gemm_impl_selector_validation():
+    assert fq.load().fq_set_gemm_impl(7) == _lib.FQ_EINVAL
+    with pytest.raises(fq.FlatQuantError):
+        fq.fq_set_gemm_impl(-1)
+
+
+def test_product_path_does_not_import_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2410_09426_b200")
+    for dp, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dp, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace("oracle's", ""), f

@@ -1,0 +1,245 @@
+"""GPU parity: the CUDA path (called through the C ABI) against the float64 oracle.
+
+Small cases run element by element; the BASELINE configs run at full size on the GPU in the
+launch configuration bench.py uses, compared on sampled tokens (first 256, which include the
+pivot token 0, plus 256 random ones) that the oracle recomputes one by one.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth
+from tests import parity
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_2410_09426_b200 as fq
+    DEV = torch.device("cuda:0")
+
+
+def to_dev(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(DEV)
+
+
+def np_of(t):
+    t = t.detach().cpu()
+    if t.dtype == torch.bfloat16:
+        t = t.float()
+    return t.numpy()
+
+
+def make_inputs(T, n1, n2, seed=0, tdtype=torch.float16, **kw):
+    x = torch.from_numpy(synth.activations(T, n1 * n2, seed=seed, dtype=np.float32, **kw)).to(tdtype)
+    p1 = torch.from_numpy(synth.well_conditioned(n1, seed=seed, tag="p1", dtype=np.float32)).to(tdtype)
+    p2 = torch.from_numpy(synth.well_conditioned(n2, seed=seed, tag="p2", dtype=np.float32)).to(tdtype)
+    return x, p1, p2
+
+
+def run_tq(x, p1, p2, alpha, n1, n2):
+    q, s, y = fq.transform_f32(x.to(DEV), n1, n2, p1.to(DEV), p2.to(DEV), alpha)
+    torch.cuda.synchronize()
+    return np_of(q), np_of(s), np_of(y)
+
+
+SHAPES = [(16, 32), (64, 64), (64, 128), (112, 128), (128, 224),    # tensor-core instantiations
+          (8, 8), (6, 10), (16, 48), (32, 32), (2, 3 * 2)]          # CUDA-core kernel
+
+
+@pytest.mark.parametrize("n1,n2", SHAPES)
+@pytest.mark.parametrize("alpha", [1.0, 0.9])
+@pytest.mark.parametrize("tdtype", [torch.float16, torch.bfloat16])
+def test_transform_quant_vs_oracle(n1, n2, alpha, tdtype):
+    T = 300 if n1 * n2 <= 16384 else 137                  # several teams/CTAs and a ragged tail
+    x, p1, p2 = make_inputs(T, n1, n2, seed=n1 + n2, tdtype=tdtype)
+    q, s, y = run_tq(x, p1, p2, alpha, n1, n2)
+    qo, so, yo = O.transform_quant(x.float().numpy(), p1.float().numpy(), p2.float().numpy(), alpha)
+    st = parity.check_transform(q, s, y, yo, qo, so, label=f"{n1}x{n2} a={alpha} {tdtype}")
+    assert st["mismatch_frac"] <= parity.MISMATCH_FRAC
+
+
+@pytest.mark.parametrize("n1,n2", [(16, 32), (64, 64), (112, 128)])
+def test_transform_special_matrices(n1, n2):
+    """Identity P: y = x exactly, so codes are the oracle's on the raw activations; Hadamard:
+    a spike spreads to +-7 everywhere; permutation: codes are permuted identity codes."""
+    T = 64
+    x, _, _ = make_inputs(T, n1, n2, seed=3)
+    eye1, eye2 = torch.eye(n1, dtype=torch.float16), torch.eye(n2, dtype=torch.float16)
+    q, s, y = run_tq(x, eye1, eye2, 1.0, n1, n2)
+    assert np.array_equal(y, x.float().numpy())
+    qo, so, yo = O.transform_quant(x.float().numpy(), eye1.float().numpy(), eye2.float().numpy(), 1.0)
+    parity.check_transform(q, s, y, yo, qo, so, tau=1e-4, label="identity")
+    if (n1 & (n1 - 1)) == 0 and (n2 & (n2 - 1)) == 0:
+        h1 = torch.from_numpy(synth.hadamard(n1, np.float32)).half()
+        h2 = torch.from_numpy(synth.hadamard(n2, np.float32)).half()
+        spike = torch.zeros((4, n1 * n2), dtype=torch.float16)
+        spike[0, 3] = 2.0
+        spike[1, n1 * n2 - 1] = -300.0
+        spike[2, 7] = 0.001
+        q, s, y = run_tq(spike, h1, h2, 1.0, n1, n2)
+        codes = O.unpack_int4(q)
+        assert np.all(np.abs(codes[:3]) == 7)
+        assert np.all(codes[3] == 0) and s[3] == 1.0      # all-zero token: s = 1, codes 0
+    p1 = torch.from_numpy(synth.permutation(n1, seed=1, dtype=np.float32)).half()
+    p2 = torch.from_numpy(synth.permutation(n2, seed=2, dtype=np.float32)).half()
+    q, s, y = run_tq(x, p1, p2, 1.0, n1, n2)
+    perm = np.kron(p1.float().numpy(), p2.float().numpy()).argmax(axis=0)
+    assert np.array_equal(y, x.float().numpy()[:, perm])
+
+
+def test_transform_overflow_stress_fp16():
+    """A token at +-60000 in every channel: the fp16 intermediate must not overflow (exact
+    power-of-two prescale), and zero / tiny tokens must not underflow."""
+    n1, n2, T = 64, 64, 8
+    g = np.random.default_rng(0)
+    x = np.where(g.random((T, n1 * n2)) < 0.5, -60000.0, 60000.0).astype(np.float16)
+    x[1] = 0
+    x[2] = (g.standard_normal(n1 * n2) * 1e-4).astype(np.float16)
+    p1 = synth.well_conditioned(n1, seed=5, tag="p1")
+    p2 = synth.well_conditioned(n2, seed=5, tag="p2")
+    q, s, y = run_tq(torch.from_numpy(x), torch.from_numpy(p1), torch.from_numpy(p2), 1.0, n1, n2)
+    assert np.all(np.isfinite(y)) and np.all(np.isfinite(s))
+    qo, so, yo = O.transform_quant(x, p1, p2, 1.0)
+    parity.check_transform(q, s, y, yo, qo, so, label="overflow stress")
+
+
+def test_transform_strided_rows_and_empty():
+    n1, n2, T = 64, 64, 33
+    x, p1, p2 = make_inputs(T, n1, n2, seed=4)
+    xb = torch.zeros((T, n1 * n2 + 64), dtype=torch.float16)
+    xb[:, : n1 * n2] = x
+    xd = xb.to(DEV)[:, : n1 * n2]                       # ldx = n + 64
+    q, s = fq.transform_quant(xd, n1, n2, p1.to(DEV), p2.to(DEV), 0.95)
+    qo, so, yo = O.transform_quant(x.float().numpy(), p1.float().numpy(), p2.float().numpy(), 0.95)
+    parity.check_transform(np_of(q), np_of(s), None, yo, qo, so, label="strided")
+    q0, s0 = fq.transform_quant(xd[:0], n1, n2, p1.to(DEV), p2.to(DEV), 1.0)
+    assert q0.shape == (0, n1 * n2 // 2)
+
+
+@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("T,N,K", [(1, 8, 32), (37, 24, 96), (128, 256, 128), (300, 520, 4096),
+                                   (2048, 4096, 4096), (257, 4096, 14336), (64, 28672, 4096)])
+def test_gemm_i32_bit_exact(impl, T, N, K):
+    qa = synth.random_codes(T, K, seed=T, tag="qa")
+    qw = synth.random_codes(N, K, seed=N, tag="qw")
+    fq.fq_set_gemm_impl(impl)
+    try:
+        acc = fq.w4a4_gemm_i32(to_dev(O.pack_int4(qa)), to_dev(O.pack_int4(qw)))
+        torch.cuda.synchronize()
+    finally:
+        fq.fq_set_gemm_impl(0)
+    ref = O.int_gemm(qa, qw)
+    assert np.array_equal(np_of(acc).astype(np.int64), ref)
+
+
+def test_gemm_i32_extreme_values():
+    T, N, K = 130, 264, 28672
+    qa = np.full((T, K), -8, np.int8)
+    qw = np.full((N, K), -8, np.int8)
+    qw[1::2] = 7
+    acc = fq.w4a4_gemm_i32(to_dev(O.pack_int4(qa)), to_dev(O.pack_int4(qw)))
+    ref = O.int_gemm(qa, qw)
+    assert np.array_equal(np_of(acc).astype(np.int64), ref)
+
+
+@pytest.mark.parametrize("out_dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("impl", [0, 1])
+def test_w4a4_linear_dequant(out_dtype, impl):
+    T, N, K = 333, 776, 2048
+    qa = synth.random_codes(T, K, seed=1, tag="qa")
+    qw = synth.random_codes(N, K, seed=2, tag="qw")
+    sa = synth.random_scales(T, seed=1, tag="sa")
+    sw = synth.random_scales(N, seed=2, tag="sw")
+    fq.fq_set_gemm_impl(impl)
+    try:
+        y = fq.w4a4_linear(to_dev(O.pack_int4(qa)), to_dev(sa), to_dev(O.pack_int4(qw)), to_dev(sw), out_dtype)
+        torch.cuda.synchronize()
+    finally:
+        fq.fq_set_gemm_impl(0)
+    ref = O.w4a4_linear(qa, sa, qw, sw)
+    parity.check_output(np_of(y), ref, label="w4a4_linear")
+    # fp16/bf16 rounding of an fp32 product: element-wise within a few ulps of the reference
+    ulp = 2.0 ** -10 if out_dtype == torch.float16 else 2.0 ** -7
+    assert np.all(np.abs(np_of(y) - ref) <= ulp * np.abs(ref) + 1e-6)
+
+
+def _chain(cfg, lin, tokens, seed=0, alpha=0.9, full_weight_prep=True):
+    T = cfg["T"]
+    n1, n2, N, K = lin.n1, lin.n2, lin.N, lin.K
+    x = synth.activations(T, K, seed=seed, tag=lin.name)
+    p1 = synth.well_conditioned(n1, seed=seed, tag=lin.name + "/p1")
+    p2 = synth.well_conditioned(n2, seed=seed, tag=lin.name + "/p2")
+    if full_weight_prep:
+        w = synth.weights(N, K, seed=seed, tag=lin.name)
+        qw, sw, _ = O.prepare_weight(w, p1, p2, 1.0)
+    else:   # large configs: synthetic pre-quantized weights (the GEMM is weight-agnostic)
+        qw = synth.random_codes(N, K, seed=seed, tag=lin.name + "/qw")
+        sw = synth.random_scales(N, seed=seed, tag=lin.name + "/sw")
+    sw32 = np.asarray(sw, np.float32)
+    xd = to_dev(x)
+    qa, sa = fq.transform_quant(xd, n1, n2, to_dev(p1), to_dev(p2), alpha)
+    y = fq.w4a4_linear(qa, sa, to_dev(O.pack_int4(qw)), to_dev(sw32))
+    yfull = fq.flatquant_linear(xd, n1, n2, to_dev(p1), to_dev(p2), alpha, to_dev(O.pack_int4(qw)), to_dev(sw32))
+    torch.cuda.synchronize()
+    assert torch.equal(y, yfull)                        # the fused entry point is the same path
+    rows = tokens if tokens is not None else np.arange(T)
+    qo, so, yo = O.transform_quant(x[rows], p1, p2, alpha)
+    parity.check_transform(np_of(qa[torch.as_tensor(rows, device=DEV)]), np_of(sa)[rows], None, yo, qo, so,
+                           label=f"{lin.name} transform")
+    out_o = O.w4a4_linear(qo, so, qw, sw32.astype(np.float64))
+    return parity.check_output(np_of(y)[rows], out_o, label=f"{lin.name} output")
+
+
+def sample_rows(T, seed=0):
+    if T <= 512:
+        return None
+    g = np.random.default_rng(seed)
+    return np.unique(np.concatenate([np.arange(256), g.choice(np.arange(256, T), 256, replace=False)]))
+
+
+@pytest.mark.parametrize("cfg_name", ["C1", "C2"])
+def test_chain_full(cfg_name):
+    cfg = synth.config(cfg_name)
+    for lin in cfg["linears"]:
+        _chain(cfg, lin, None)
+
+
+@pytest.mark.parametrize("cfg_name", ["C3", "C4"])
+def test_chain_llama3_8b(cfg_name):
+    cfg = synth.config(cfg_name)
+    for lin in cfg["linears"]:
+        _chain(cfg, lin, sample_rows(cfg["T"]), full_weight_prep=(lin.N * lin.K <= 4096 * 14336))
+
+
+def test_chain_llama3_70b_sampled():
+    cfg = synth.config("C5")
+    for lin in cfg["linears"]:
+        _chain(cfg, lin, sample_rows(cfg["T"]), full_weight_prep=False)
+
+
+def test_determinism():
+    cfg = synth.config("C2")
+    lin = cfg["linears"][0]
+    x, p1, p2 = make_inputs(cfg["T"], lin.n1, lin.n2, seed=9)
+    qw = to_dev(O.pack_int4(synth.random_codes(lin.N, lin.K, seed=9)))
+    sw = to_dev(synth.random_scales(lin.N, seed=9))
+    outs = [fq.flatquant_linear(x.to(DEV), lin.n1, lin.n2, p1.to(DEV), p2.to(DEV), 0.9, qw, sw) for _ in range(2)]
+    assert torch.equal(outs[0], outs[1])
+
+
+def test_gpu_weight_prep_matches_oracle():
+    """NEXT-2 preview: W' = P1^{-1} W~ P2^{-T} via the activation kernel with (P1^{-T}, P2^{-T}).
+    The fp16-rounded inverses perturb W' by ~1e-3 relative; compare dequantized weights."""
+    n1, n2, N = 64, 64, 512
+    w = synth.weights(N, n1 * n2, seed=3)
+    p1 = synth.well_conditioned(n1, seed=3, tag="p1")
+    p2 = synth.well_conditioned(n2, seed=3, tag="p2")
+    qw, sw = fq.prepare_weight(to_dev(w), n1, n2, to_dev(p1), to_dev(p2), 1.0)
+    _, _, wp = O.prepare_weight(w, p1, p2, 1.0)
+    deq = O.dequantize_rows(O.unpack_int4(np_of(qw)), np_of(sw).astype(np.float64))
+    assert np.linalg.norm(deq - wp) / np.linalg.norm(wp) < 0.15     # 4-bit RTN error dominates
+    assert np.all(np.abs(np_of(sw) / (np.abs(wp).max(1) / 7) - 1) < 1e-2)
