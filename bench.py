@@ -1,0 +1,450 @@
+#!/usr/bin/env python
+"""bench.py -- FlatQuant online hot path on B200: prefill tokens/s of all layer linears.
+
+One step = the whole hot path over one batch of synthetic tokens:
+for every linear of the configuration, fq_transform_quant (Kronecker transform + clip + INT4
+quantize/pack) followed by fq_w4a4_linear (tcgen05 W4A4 GEMM + dequant epilogue).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one process per GPU, NCCL); every rank processes its own T
+tokens (weak scaling, no collective in the timed path), the time is the max over ranks.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+INT8_PER_BF16 = 2.0          # nominal dense ratio (4.5 / 2.25 POPS), B200_PROFILING.md
+
+
+def peaks():
+    if os.path.exists(PEAKS_PATH):
+        p = json.load(open(PEAKS_PATH))
+        return p, "measured (MEASURED_PEAKS.json)"
+    return dict(FALLBACK), "fallback (B200_PROFILING.md)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C3", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--alpha", type=float, default=0.9)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fp16", action="store_true")
+    ap.add_argument("--verify", action="store_true", help="all-gather outputs (untimed) and check shards")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------ clocks sampler
+class Clocks:
+    """nvidia-smi sampler (100 ms) started before the warm-up; the summary keeps the samples
+    taken inside the timed window (padded by 0.3 s, since one window can be shorter than a
+    sampling period)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.t0 = self.t1 = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append((time.time(), parts))
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
+    def stop(self):
+        time.sleep(0.35)
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = [r for t, r in self.rows if self.t0 is not None and self.t0 - 0.3 <= t <= self.t1 + 0.3]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        sm = [v for v in (num(r[0]) for r in rows) if v is not None]
+        mx = [v for v in (num(r[1]) for r in rows) if v is not None]
+        pw = [v for v in (num(r[6]) for r in rows) if v is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows), "power_w_max": max(pw) if pw else None}
+
+
+# ------------------------------------------------------------------------ workload
+def build_workload(cfg_name, rank, dev, torch, fq):
+    cfg = synth.config(cfg_name)
+    T = cfg["T"]
+    layers = []
+    for lin in cfg["linears"]:
+        n1, n2, N, K = lin.n1, lin.n2, lin.N, lin.K
+        x = torch.from_numpy(synth.activations(T, K, seed=1000 + rank, tag=lin.name)).to(dev)
+        p1 = torch.from_numpy(synth.well_conditioned(n1, seed=0, tag=lin.name + "/p1")).to(dev)
+        p2 = torch.from_numpy(synth.well_conditioned(n2, seed=0, tag=lin.name + "/p2")).to(dev)
+        w = torch.from_numpy(synth.weights(N, K, seed=0, tag=lin.name)).to(dev)
+        qw, sw = fq.prepare_weight(w, n1, n2, p1, p2, 1.0)          # offline weight side on the GPU
+        layers.append(dict(lin=lin, x=x, p1=p1, p2=p2, w=w, qw=qw, sw=sw,
+                           q=torch.empty((T, K // 2), dtype=torch.uint8, device=dev),
+                           s=torch.empty((T,), dtype=torch.float32, device=dev),
+                           y=torch.empty((T, N), dtype=torch.float16, device=dev)))
+    return cfg, layers
+
+
+def tq_bytes(T, lin):
+    return T * (2 * lin.K + lin.K // 2 + 4) + 2 * (lin.n1 ** 2 + lin.n2 ** 2)
+
+
+def tq_flops(T, lin):
+    return 2 * T * lin.K * (lin.n1 + lin.n2)
+
+
+def gemm_ops(T, lin):
+    return 2 * T * lin.N * lin.K
+
+
+# ------------------------------------------------------------------------ oracle (CPU) timing
+def cpu_oracle_rate(cfg_name, sample_tokens, alpha, budget_s=20.0):
+    """The float64 oracle as it stands, on a bounded token sample of the same workload."""
+    import oracle as O
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    cfg = synth.config(cfg_name)
+    prepared = []
+    for lin in cfg["linears"]:
+        x = synth.activations(sample_tokens, lin.K, seed=1000, tag=lin.name)
+        p1 = synth.well_conditioned(lin.n1, seed=0, tag=lin.name + "/p1")
+        p2 = synth.well_conditioned(lin.n2, seed=0, tag=lin.name + "/p2")
+        w = synth.weights(lin.N, lin.K, seed=0, tag=lin.name)
+        qw, sw, _ = O.prepare_weight(w, p1, p2, 1.0)                 # offline, untimed
+        prepared.append((x, p1, p2, qw, sw))
+    done, t0 = 0, time.perf_counter()
+    while True:
+        for x, p1, p2, qw, sw in prepared:
+            qa, sa, _ = O.transform_quant(x, p1, p2, alpha)
+            O.dequant(O.int_gemm(qa, qw), sa, sw)
+        done += sample_tokens
+        el = time.perf_counter() - t0
+        if el >= budget_s or done >= 4 * sample_tokens:
+            break
+    return done / el, cores, f"{sample_tokens} tokens x {done // sample_tokens} passes of all {cfg_name} linears " \
+                             f"(transform+quant, int GEMM, dequant; weight prep untimed), {el:.1f} s"
+
+
+# ------------------------------------------------------------------------ our implementation
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2410_09426_b200 as fq
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    fq.load()
+    if os.environ.get("FQ_GEMM_IMPL"):                     # testing aid: 0 pair (default), 1 mma.sync, 2 1-CTA
+        fq.fq_set_gemm_impl(int(os.environ["FQ_GEMM_IMPL"]))
+
+    cfg, layers = build_workload(args.config, rank, dev, torch, fq)
+    T = cfg["T"]
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > L2 (126 MB)
+
+    def step(evs=None):
+        for i, L in enumerate(layers):
+            lin = L["lin"]
+            if evs is not None:
+                evs[2 * i][0].record(stream)
+            fq.fq_transform_quant(L["x"], lin.n1, lin.n2, L["p1"], L["p2"], args.alpha, L["q"], L["s"])
+            if evs is not None:
+                evs[2 * i][1].record(stream)
+                evs[2 * i + 1][0].record(stream)
+            fq.fq_w4a4_linear(L["q"], L["s"], L["qw"], L["sw"], L["y"])
+            if evs is not None:
+                evs[2 * i + 1][1].record(stream)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    clk = Clocks(local).start()
+    t_w = time.time()
+    w = 0
+    while w < max(args.warmup, 3) or time.time() - t_w < 1.0:      # >= 1 s soak so clocks settle
+        flush.zero_()
+        step()
+        w += 1
+        if w % 50 == 0:
+            torch.cuda.synchronize()
+    barrier()
+
+    # ---- timed region: K steps, L2 flushed before each step (flush itself untimed) ----
+    per_kernel = [[0.0, 0.0] for _ in range(2 * len(layers))]
+    step_ms = []
+    launches0 = fq.fq_launch_count()
+    clk.mark_start()
+    if True:
+        for _ in range(args.steps):
+            flush.zero_()
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(2 * len(layers))]
+            step(evs)
+            torch.cuda.synchronize()
+            ms = 0.0
+            for k, (a, b) in enumerate(evs):
+                d = a.elapsed_time(b)
+                per_kernel[k][0] += d
+                per_kernel[k][1] += 1
+                ms += d
+            step_ms.append(ms)
+        barrier()
+    clk.mark_end()
+    clk.stop()
+    launches = fq.fq_launch_count() - launches0
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * T / (ms_per_step * 1e-3)
+
+    # ---- kernel-level rooflines ----
+    pk, peak_src = peaks()
+    gemm_ms = sum(per_kernel[2 * i + 1][0] for i in range(len(layers))) / args.steps
+    tq_ms = sum(per_kernel[2 * i][0] for i in range(len(layers))) / args.steps
+    g_ops = sum(gemm_ops(T, L["lin"]) for L in layers)
+    t_bytes = sum(tq_bytes(T, L["lin"]) for L in layers)
+    t_flops = sum(tq_flops(T, L["lin"]) for L in layers)
+    int8_peak = pk["bf16_tflops"] * INT8_PER_BF16
+    gemm_tops = g_ops / (gemm_ms * 1e-3) / 1e12
+    tq_gbs = t_bytes / (tq_ms * 1e-3) / 1e9
+    kernels = {}
+    for i, L in enumerate(layers):
+        lin = L["lin"]
+        tq_i = per_kernel[2 * i][0] / args.steps
+        gm_i = per_kernel[2 * i + 1][0] / args.steps
+        kernels[lin.name] = {
+            "n1xn2": f"{lin.n1}x{lin.n2}", "N": lin.N,
+            "tq_us": round(tq_i * 1e3, 2), "tq_gbs": round(tq_bytes(T, lin) / (tq_i * 1e-3) / 1e9, 1),
+            "tq_tflops": round(tq_flops(T, lin) / (tq_i * 1e-3) / 1e12, 1),
+            "gemm_us": round(gm_i * 1e3, 2), "gemm_tops": round(gemm_ops(T, lin) / (gm_i * 1e-3) / 1e12, 1),
+        }
+
+    # ---- FP16 baseline (torch.matmul / cuBLAS on the same shapes), context for "vs FP16" ----
+    fp16 = None
+    if not args.no_fp16:
+        xs = [L["x"] for L in layers]
+        ws = [L["w"] for L in layers]
+        for _ in range(3):
+            for x, w in zip(xs, ws):
+                torch.matmul(x, w.t())
+        f_ms = []
+        for _ in range(max(5, args.steps // 2)):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for x, w in zip(xs, ws):
+                torch.matmul(x, w.t())
+            b.record(stream)
+            torch.cuda.synchronize()
+            f_ms.append(a.elapsed_time(b))
+        fp16_ms = sum(f_ms) / len(f_ms)
+        fp16 = {"ms_per_step": round(fp16_ms, 4), "tokens_per_s": round(world * T / (fp16_ms * 1e-3), 1),
+                "speedup_ours_vs_fp16": round(fp16_ms / ms_per_step, 3)}
+
+    # ---- e2e: through the public C ABI with HOST buffers (H2D + hot path + D2H per step) ----
+    e2e = None
+    if not args.no_e2e:
+        hx = [L["x"].cpu().pin_memory() for L in layers]
+        hy = [torch.empty(L["y"].shape, dtype=L["y"].dtype).pin_memory() for L in layers]
+        dx = [torch.empty_like(L["x"]) for L in layers]
+
+        def e2e_step():
+            for L, x_h, y_h, x_d in zip(layers, hx, hy, dx):
+                lin = L["lin"]
+                fq.fq_flatquant_linear_host(x_h, x_d, lin.n1, lin.n2, L["p1"], L["p2"], args.alpha, L["qw"], L["sw"],
+                                            y_h, L["y"], L["q"], L["s"])
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        e_ms = []
+        for _ in range(max(3, args.steps // 2)):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            e2e_step()
+            b.record(stream)
+            torch.cuda.synchronize()
+            e_ms.append(a.elapsed_time(b))
+        e_tot = sum(e_ms)
+        if world > 1:
+            t = torch.tensor([e_tot], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_tot = float(t.item())
+        e2e_step_ms = e_tot / len(e_ms)
+        e2e = {"value": round(world * T / (e2e_step_ms * 1e-3), 1), "unit": "tokens/s",
+               "ms_per_step": round(e2e_step_ms, 4),
+               "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in hx)),
+               "d2h_bytes_per_step": int(sum(y.numel() * y.element_size() for y in hy))}
+
+    # ---- verification (untimed): shards are independent, gather and compare with local ----
+    verify = None
+    if args.verify and world > 1:
+        from paper_2410_09426_b200.sharding import gather_rows
+        y0 = layers[0]["y"]
+        full = gather_rows(y0, world * T)
+        verify = bool(torch.equal(full[rank * T:(rank + 1) * T], y0))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, cores, sample = cpu_oracle_rate(args.config, 128, args.alpha)
+        cpu = {"value": round(rate, 2), "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        frac = gemm_tops / int8_peak
+        out = {
+            "metric": "prefill tokens/s, FlatQuant W4A4 layer linears (transform+quant -> W4A4 GEMM)",
+            "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp16 in / int4 x int4 -> int32 / fp16 out",
+            "data": "synthetic (seeded Gaussian + channel outliers + pivot token; random-init weights)",
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "tokens_per_gpu": T,
+                       "linears": [f"{L['lin'].name} {L['lin'].K}({L['lin'].n1}x{L['lin'].n2})->{L['lin'].N}"
+                                   for L in layers],
+                       "alpha": args.alpha, "parallelism": f"token-shard x{world}",
+                       "l2": "flushed (256 MiB write) before every timed step; flush untimed"},
+            "roofline": {"bound": "tensor", "kernel": "fq_w4a4_linear (tcgen05 kind::i8)",
+                         "achieved": round(gemm_tops, 1), "peak": round(int8_peak, 1), "unit": "TOPS",
+                         "frac": round(frac, 4), "traffic": None,
+                         "peak_source": f"{peak_src}: bf16 {pk['bf16_tflops']} TF/s x nominal int8/bf16 ratio 2"},
+            "tq_roofline": {"bound": "hbm", "kernel": "fq_transform_quant", "achieved": round(tq_gbs, 1),
+                            "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(tq_gbs / pk["hbm_gbs"], 4),
+                            "tflops": round(t_flops / (tq_ms * 1e-3) / 1e12, 1)},
+            "time_share": {"transform_quant": round(tq_ms / ms_per_step, 4), "gemm": round(gemm_ms / ms_per_step, 4)},
+            "kernels": kernels,
+            "fp16_baseline": fp16,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        if verify is not None:
+            out["verify_allgather"] = verify
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------ reference arm
+def run_reference(args):
+    """Reference arm for this tier: the float64 oracle, timed as it stands on the host cores, on a
+    bounded token sample per step (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle as O
+    cfg = synth.config(args.config)
+    sample = 32
+    prepared = []
+    for lin in cfg["linears"]:
+        x = synth.activations(sample, lin.K, seed=1000, tag=lin.name)
+        p1 = synth.well_conditioned(lin.n1, seed=0, tag=lin.name + "/p1")
+        p2 = synth.well_conditioned(lin.n2, seed=0, tag=lin.name + "/p2")
+        w = synth.weights(lin.N, lin.K, seed=0, tag=lin.name)
+        qw, sw, _ = O.prepare_weight(w, p1, p2, 1.0)
+        prepared.append((x, p1, p2, qw, sw))
+
+    def step():
+        for x, p1, p2, qw, sw in prepared:
+            qa, sa, _ = O.transform_quant(x, p1, p2, args.alpha)
+            O.dequant(O.int_gemm(qa, qw), sa, sw)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    value = sample * args.steps / el
+    desc = f"{sample} tokens per step through all {args.config} linears (float64 oracle)"
+    print(json.dumps({
+        "impl": "reference", "metric": "prefill tokens/s, FlatQuant W4A4 layer linears (transform+quant -> W4A4 GEMM)",
+        "value": round(value, 2), "unit": "tokens/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"{args.config}: {cfg['desc']}", "sample_tokens_per_step": sample},
+        "cpu_baseline": {"value": round(value, 2), "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": desc},
+        "e2e": {"value": round(value, 2), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

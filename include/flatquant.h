@@ -22,8 +22,10 @@
  *    returns FQ_ECUDA; fq_last_cuda_error() returns the cudaError_t value.  Device faults
  *    surface at the caller's next synchronisation, as with any CUDA library.
  *  - Layouts are row-major.  INT4 codes are two's-complement nibbles, element 2i in the
- *    LOW nibble of byte i of its row (reading R7).  Device pointers must be
- *    16-byte aligned and row strides multiples of 16 bytes.
+ *    LOW nibble of byte i of its row (reading R7).  Alignment: every pointer
+ *    is aligned to its element size; in addition the tensor-core paths (the GEMM, and the
+ *    transform when n1 % 16 == 0 and n2 % 16 == 0) need x, q, qa, qw, y and sw 16-byte
+ *    aligned and row strides that are multiples of 16 bytes (FQ_ESHAPE otherwise).
  *  - Stateless and re-entrant; per-device kernel attributes are set once, thread-safely.
  *  - Non-finite inputs give unspecified codes (the oracle's precondition is finite x).
  */
@@ -57,8 +59,8 @@ typedef enum { FQ_SYM = 0, FQ_ASYM = 1 } fq_qmode;
  *   PAPER.md:236-244 (Eq.3, activation factor Q(P1^T x_1 X~ x_2 P2))
  *   (clipping ratio after the transform), PAPER.md:367 (per-token symmetric), Eq.1.
  *
- *   x      [T, ldx] elements of x_dtype; row t holds x_t (n = n1*n2 used), ldx >= n,
- *          ldx*elemsize % 16 == 0.  Viewed as V_t = reshape(x_t, n1, n2) in C order.
+ *   x      [T, ldx] elements of x_dtype; row t holds x_t (n = n1*n2 used), ldx >= n.
+ *          Viewed as V_t = reshape(x_t, n1, n2) in C order.
  *   p1     [n1, n1] row-major, x_dtype.     p2 [n2, n2] row-major, x_dtype.
  *   alpha  post-sigmoid clipping ratio in (0, 1]; 1 = no clipping.
  *   qmode  FQ_SYM (FQ_ASYM -> FQ_ENOTSUP in v1).
@@ -73,9 +75,9 @@ fq_status fq_transform_quant(const void* x, int32_t x_dtype, int64_t T, int64_t 
                              int8_t* zero, void* stream);
 
 /* fq_transform_f32 -- same kernel as fq_transform_quant, additionally exporting the
- * transformed activations y [T, n] fp32 (before clipping/quantization) so that the
- * "transformed activations rel 1e-3" bar can be checked on the production code path.
- * q/scale may be NULL (then only y is written... q and scale are still computed). */
+ * transformed activations y [T, n] fp32 (before clipping/quantization; 8-byte aligned) so
+ * that the "transformed activations rel 1e-3" bar can be checked on the production code
+ * path.  q and scale are written exactly as by fq_transform_quant (both required). */
 fq_status fq_transform_f32(const void* x, int32_t x_dtype, int64_t T, int64_t ldx,
                            int32_t n1, int32_t n2, const void* p1, const void* p2,
                            float alpha, uint8_t* q, float* scale, float* y, void* stream);
@@ -130,8 +132,8 @@ fq_status fq_flatquant_linear_host(const void* x_host, void* x_dev, int32_t x_dt
 fq_status fq_choose_decomposition(int64_t n, int32_t* n1, int32_t* n2);
 
 /* Selects the GEMM implementation for subsequent calls in this process (testing aid):
- * 0 = default (tcgen05 kind::i8 where available), 1 = legacy mma.sync cross-check kernel.
- * Returns FQ_EINVAL for unknown values. */
+ * 0 = default (tcgen05 kind::i8 on a CTA pair, cta_group::2), 1 = legacy mma.sync
+ * cross-check kernel, 2 = tcgen05 kind::i8 on a single CTA.  Returns FQ_EINVAL otherwise. */
 fq_status fq_set_gemm_impl(int32_t impl);
 
 /* Number of kernel launches issued by this library since process start (bench accounting). */

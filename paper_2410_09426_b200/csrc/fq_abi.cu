@@ -48,8 +48,14 @@ static fq_status validate_tq(const void* x, int32_t x_dtype, int64_t T, int64_t 
   const int64_t n = int64_t(n1) * n2;
   if (n % 2 != 0) return FQ_ESHAPE;
   if (ldx < n) return FQ_ESHAPE;
-  if ((ldx * 2) % 16 != 0) return FQ_ESHAPE;
-  if (!aligned16(x) || !aligned16(q) || !aligned16(p1) || !aligned16(p2)) return FQ_ESHAPE;
+  const bool tc = (n1 % 16 == 0) && (n2 % 16 == 0);
+  if (tc) {
+    // tensor-core kernel: 16-byte cp.async of x rows and 16-byte stores of packed rows
+    if ((ldx * 2) % 16 != 0 || !aligned16(x) || !aligned16(q)) return FQ_ESHAPE;
+  }
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(p1) | reinterpret_cast<uintptr_t>(p2)) & 1u)
+    return FQ_ESHAPE;
+  if ((reinterpret_cast<uintptr_t>(scale) & 3u) != 0) return FQ_ESHAPE;
   if (n1 > 256 || n2 > 256) return FQ_ENOTSUP;
   return FQ_OK;
 }
@@ -103,8 +109,10 @@ static fq_status run_gemm(const uint8_t* qa, const float* sa, int64_t T, int32_t
   a.y_bf16 = y_bf16;
   a.out_i32 = out_i32;
   a.stream = static_cast<cudaStream_t>(stream);
-  if (g_gemm_impl.load() == 1 || !gemm_tc05_supported(a)) return cuda_status(gemm_mma_launch(a));
-  return cuda_status(gemm_tc05_launch(a));
+  const int impl = g_gemm_impl.load();
+  if (impl == 0 && gemm_pair_supported(a)) return cuda_status(gemm_pair_launch(a));
+  if (impl == 2 && gemm_tc05_supported(a)) return cuda_status(gemm_tc05_launch(a));
+  return cuda_status(gemm_mma_launch(a));
 }
 
 }  // namespace fq
@@ -130,7 +138,7 @@ fq_status fq_transform_f32(const void* x, int32_t x_dtype, int64_t T, int64_t ld
   fq_status s = validate_tq(x, x_dtype, T, ldx, n1, n2, p1, p2, alpha, q, scale);
   if (s != FQ_OK || T == 0) return s;
   if (!y) return FQ_EINVAL;
-  if (!aligned16(y)) return FQ_ESHAPE;
+  if ((reinterpret_cast<uintptr_t>(y) & 7u) != 0) return FQ_ESHAPE;
   return run_tq(x, x_dtype, T, ldx, n1, n2, p1, p2, alpha, q, scale, y, stream);
 }
 
@@ -204,7 +212,7 @@ fq_status fq_choose_decomposition(int64_t n, int32_t* n1, int32_t* n2) {
 }
 
 fq_status fq_set_gemm_impl(int32_t impl) {
-  if (impl != 0 && impl != 1) return FQ_EINVAL;
+  if (impl < 0 || impl > 2) return FQ_EINVAL;
   g_gemm_impl.store(impl);
   return FQ_OK;
 }

@@ -1,0 +1,379 @@
+// fq_gemm_tc05_pair.cu -- W4A4 GEMM + dequant on a CTA PAIR (tcgen05.mma.cta_group::2 kind::i8).
+//
+//   acc[t,o] = sum_k qa[t,k] qw[o,k]               (Eq.3; PAPER.md:315 INT4 GEMM)
+//   y[t,o]   = cvt_rn(float(acc) * sa[t] * sw[o])  (per-token x per-channel)
+//
+// Same int4 -> int8 widening contract as fq_gemm_tc05.cu (x16 per operand, acc/256 exact).
+// Two SMs of a TPC cooperate on a 256 (tokens) x 192 (features) tile: each CTA holds its own
+// 128 activation rows as the A operand in TMEM (widened by converter warps straight from
+// registers with tcgen05.st) and HALF of the 192 weight rows (96) as the B operand in shared
+// memory; the leader CTA issues one M=256 N=192 K=32 MMA for both.  Per SM this halves the
+// shared-memory and L1 traffic per MAC relative to a single-CTA tile.
+//   warps 0-3 : epilogue (own TMEM lanes -> dequant -> global)
+//   warp  4   : TMEM allocator (both CTAs) + MMA issuer (leader CTA only)
+//   warps 5-8 : A converters, one activation row per thread (256-bit loads)
+//   warps 9-12: B converters, 4 threads per weight row (coalesced), SWIZZLE_128B K-major
+// Synchronisation: converters of both CTAs arrive (release.cluster) on the leader's `full`
+// barrier; the leader's tcgen05.commit multicasts to both CTAs' `empty` / `tfull` barriers;
+// both CTAs' epilogues arrive on the leader's `tempty` barrier.
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "fq_device.cuh"
+#include "fq_internal.h"
+#include "fq_tc05.cuh"
+
+namespace fq {
+namespace g3 {
+
+constexpr int BM = 256, BM_CTA = 128;     // tokens per pair tile / per CTA
+constexpr int BN = 192, BN_CTA = 96;      // features per pair tile / B rows per CTA
+constexpr int BK = 128;                   // int8 K per stage
+constexpr int UK = 32;
+constexpr int STAGES = 4;
+constexpr int B_BYTES = BN_CTA * BK;      // 12 KB per stage per CTA
+constexpr int A_COLS = BK / 4;            // TMEM columns per A stage
+constexpr int TMEM_ACC0 = 0;              // two accumulators [0, 2*BN)
+constexpr int TMEM_A0 = 2 * BN;           // A stages [2*BN, 2*BN + STAGES*A_COLS) = [384, 512)
+constexpr int TMEM_COLS = 512;
+constexpr int NUM_EPI_WARPS = 4, MMA_WARP = 4;
+constexpr int A_WARP0 = 5, NUM_A_WARPS = 8;     // 2 warps per TMEM lane quarter (each half of K)
+constexpr int B_WARP0 = 13, NUM_B_WARPS = 6;
+constexpr int NUM_CONV_WARPS = NUM_A_WARPS + NUM_B_WARPS;
+constexpr int THREADS = (B_WARP0 + NUM_B_WARPS) * 32;
+constexpr int B_TASKS = BN_CTA * 4 / (NUM_B_WARPS * 32);    // 16-byte packed chunks per B thread
+constexpr int PF = 4;                                       // K-blocks of register prefetch
+constexpr size_t SMEM_BYTES = size_t(STAGES) * B_BYTES + 1024 + 256;
+constexpr uint32_t IDESC = tc::idesc_i8(BM, BN);
+static_assert(TMEM_A0 + STAGES * A_COLS <= TMEM_COLS, "TMEM budget");
+static_assert(B_TASKS * NUM_B_WARPS * 32 == BN_CTA * 4, "B task split");
+
+FQ_DEVICE void widen8(uint32_t p, uint32_t& lo, uint32_t& hi) {   // 8 nibbles -> 8 x (16 q) int8
+  lo = (p << 4) & 0xF0F0F0F0u;
+  hi = p & 0xF0F0F0F0u;
+}
+
+FQ_DEVICE void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+struct Sched {
+  int num_m, num_n, num_tiles, num_kb, cluster, num_clusters;
+  FQ_DEVICE void tile(int id, int& mb, int& nb) const {
+    mb = id % num_m;
+    nb = id / num_m;
+  }
+};
+
+// Walks this cluster's (tile, k-block) job sequence without per-step divisions.
+struct Cursor {
+  int tile, kb, mb, nb;
+  bool valid;
+  FQ_DEVICE void init(const Sched& s) {
+    tile = s.cluster;
+    kb = 0;
+    valid = tile < s.num_tiles;
+    if (valid) s.tile(tile, mb, nb);
+  }
+  FQ_DEVICE void next(const Sched& s) {
+    if (++kb == s.num_kb) {
+      kb = 0;
+      tile += s.num_clusters;
+      valid = tile < s.num_tiles;
+      if (valid) s.tile(tile, mb, nb);
+    }
+  }
+};
+
+template <bool OUT_I32, bool BF16>
+__global__ void __launch_bounds__(THREADS, 1)
+gemm_pair_kernel(const uint8_t* __restrict__ qa, const float* __restrict__ sa, int T, int K,
+                 const uint8_t* __restrict__ qw, const float* __restrict__ sw, int N,
+                 void* __restrict__ yv) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(STAGES) * B_BYTES);
+  uint64_t* full = bars;                 // [STAGES] leader: converters of both CTAs -> MMA
+  uint64_t* empty = bars + STAGES;       // [STAGES] each CTA: MMA commit -> converters
+  uint64_t* tfull = bars + 2 * STAGES;   // [2]      each CTA: MMA commit -> epilogue
+  uint64_t* tempty = tfull + 2;          // [2]      leader: epilogues of both CTAs -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc::cluster_ctarank();
+  Sched sc;
+  sc.num_m = (T + BM - 1) / BM;
+  sc.num_n = (N + BN - 1) / BN;
+  sc.num_tiles = sc.num_m * sc.num_n;
+  sc.num_kb = (K + BK - 1) / BK;
+  sc.cluster = blockIdx.x >> 1;
+  sc.num_clusters = gridDim.x >> 1;
+  const int KB = K / 2;
+
+  if (warp == MMA_WARP) {
+    if (lane == 0) {
+      for (int s = 0; s < STAGES; ++s) {
+        tc::mbar_init(&full[s], 2);                 // one arrival per CTA of the pair
+        tc::mbar_init(&empty[s], 1);
+      }
+      for (int b = 0; b < 2; ++b) {
+        tc::mbar_init(&tfull[b], 1);
+        tc::mbar_init(&tempty[b], 2);
+      }
+      tc::fence_barrier_init();
+    }
+    __syncwarp();
+    tc::tmem_alloc2(tmem_slot, TMEM_COLS);
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();            // peer barriers initialised before any remote arrive
+  tc::fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // All converter warps of this CTA finish a stage, then ONE thread signals the leader's
+  // `full` barrier: a CTA-scope arrive in the leader, a single release.cluster remote arrive in
+  // the peer (one cluster-scope fence per stage instead of one per warp).
+  auto signal_full = [&](uint64_t* bar) {
+    named_bar_sync(1, NUM_CONV_WARPS * 32);
+    if (threadIdx.x == A_WARP0 * 32) {
+      if (rank == 0) tc::mbar_arrive(bar);
+      else tc::mbar_arrive_cluster(bar, 0);
+    }
+  };
+
+  if (warp >= A_WARP0) {
+    // ================================ converters ================================
+    // Each thread keeps PF K-blocks of its packed data in flight in a statically indexed
+    // register ring (the loop below is unrolled PF times, so slot indices are constants).
+    const bool is_a = warp < B_WARP0;
+    int stage = 0;
+    uint32_t phase = 0;
+    Cursor ld, cv;          // load cursor runs PF jobs ahead of the convert cursor
+    ld.init(sc);
+    cv.init(sc);
+    if (is_a) {
+      const int aw = warp - A_WARP0;
+      const int quarter = warp & 3, khalf = aw >> 2;
+      const int r_local = quarter * 32 + lane;                   // == TMEM lane of this row
+      const bool wide = (KB % 32) == 0;
+      const uint32_t tl = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(TMEM_A0 + khalf * (A_COLS / 2));
+      uint32_t ring[PF][8];
+      auto load = [&](uint32_t (&r)[8]) {
+        const int row = ld.mb * BM + int(rank) * BM_CTA + r_local;
+        const int kbyte = ld.kb * (BK / 2) + khalf * 32;
+        const bool ok = ld.valid && row < T && kbyte < KB;
+        const uint8_t* p = qa + size_t(ok ? row : 0) * KB + (ok ? kbyte : 0);
+        if (!ok) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) r[i] = 0;
+        } else if (wide) {
+          tc::ldg256(p, r);
+        } else {
+          const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(p));
+          const uint4 v1 = (kbyte + 16 < KB) ? __ldg(reinterpret_cast<const uint4*>(p + 16)) : make_uint4(0, 0, 0, 0);
+          r[0] = v0.x; r[1] = v0.y; r[2] = v0.z; r[3] = v0.w;
+          r[4] = v1.x; r[5] = v1.y; r[6] = v1.z; r[7] = v1.w;
+        }
+        ld.next(sc);
+      };
+#pragma unroll
+      for (int u = 0; u < PF; ++u) load(ring[u]);
+      while (cv.valid) {
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+          if (!cv.valid) break;
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          uint32_t w[16];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) widen8(ring[u][i], w[2 * i], w[2 * i + 1]);
+          load(ring[u]);                                          // refill this slot PF jobs ahead
+          tmem_st16(tl + uint32_t(stage * A_COLS), w);
+          tc::tmem_st_wait();
+          tc::fence_before();
+          signal_full(&full[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          cv.next(sc);
+        }
+      }
+    } else {
+      const int ct = threadIdx.x - B_WARP0 * 32;
+      uint4 ring[PF][B_TASKS];
+      auto load = [&](uint4 (&r)[B_TASKS]) {
+#pragma unroll
+        for (int i = 0; i < B_TASKS; ++i) {
+          const int task = ct + i * NUM_B_WARPS * 32, rl = task >> 2, c = task & 3;
+          const int row = ld.nb * BN + int(rank) * BN_CTA + rl, kbyte = ld.kb * (BK / 2) + c * 16;
+          r[i] = (ld.valid && row < N && kbyte < KB)
+                     ? __ldg(reinterpret_cast<const uint4*>(qw + size_t(row) * KB + kbyte))
+                     : make_uint4(0, 0, 0, 0);
+        }
+        ld.next(sc);
+      };
+#pragma unroll
+      for (int u = 0; u < PF; ++u) load(ring[u]);
+      while (cv.valid) {
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+          if (!cv.valid) break;
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sB = smem + size_t(stage) * B_BYTES;
+#pragma unroll
+          for (int i = 0; i < B_TASKS; ++i) {
+            const int task = ct + i * NUM_B_WARPS * 32, rl = task >> 2, c = task & 3;
+            uint4 o0, o1;
+            widen8(ring[u][i].x, o0.x, o0.y);
+            widen8(ring[u][i].y, o0.z, o0.w);
+            widen8(ring[u][i].z, o1.x, o1.y);
+            widen8(ring[u][i].w, o1.z, o1.w);
+            uint8_t* rowp = sB + rl * 128;
+            *reinterpret_cast<uint4*>(rowp + (((2 * c) ^ (rl & 7)) << 4)) = o0;
+            *reinterpret_cast<uint4*>(rowp + (((2 * c + 1) ^ (rl & 7)) << 4)) = o1;
+          }
+          load(ring[u]);
+          tc::fence_proxy_async_smem();
+          signal_full(&full[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          cv.next(sc);
+        }
+      }
+    }
+  } else if (warp == MMA_WARP) {
+    // ================================ MMA issuer (leader CTA) ================================
+    if (rank == 0 && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = sc.cluster; tile < sc.num_tiles; tile += sc.num_clusters, ++it) {
+        const int buf = it & 1;
+        tc::mbar_wait_cluster(&tempty[buf], ((it >> 1) & 1) ^ 1);
+        tc::fence_after();
+        const uint32_t tmem_d = tmem_base + uint32_t(TMEM_ACC0 + buf * BN);
+        for (int kb = 0; kb < sc.num_kb; ++kb) {
+          tc::mbar_wait_cluster(&full[stage], phase);
+          tc::fence_after();
+          const uint32_t a_t = tmem_base + uint32_t(TMEM_A0 + stage * A_COLS);
+          const uint32_t b0 = smem_u32(smem + size_t(stage) * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)
+            tc::mma_ts_i8_pair(tmem_d, a_t + k * (UK / 4), tc::sdesc_sw128(b0 + k * UK, 16, 1024), IDESC,
+                               (kb | k) != 0);
+          tc::mma_commit_pair(&empty[stage], 0x3);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc::mma_commit_pair(&tfull[buf], 0x3);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ================================ epilogue ================================
+    const int r_local = warp * 32 + lane;
+    int it = 0;
+    for (int tile = sc.cluster; tile < sc.num_tiles; tile += sc.num_clusters, ++it) {
+      int mb, nb;
+      sc.tile(tile, mb, nb);
+      const int buf = it & 1;
+      tc::mbar_wait(&tfull[buf], (it >> 1) & 1);
+      tc::fence_after();
+      const int row = mb * BM + int(rank) * BM_CTA + r_local;
+      const bool row_ok = row < T;
+      const float s_a = (!OUT_I32 && row_ok) ? sa[row] * (1.0f / 256.0f) : 0.f;
+#pragma unroll 1
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        uint32_t v[32];
+        tc::tmem_ld32(tmem_base + (uint32_t(warp * 32) << 16) + uint32_t(TMEM_ACC0 + buf * BN + cc * 32), v);
+        tc::tmem_ld_wait();
+        const int col0 = nb * BN + cc * 32;
+        if (row_ok) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            const int col = col0 + j;
+            if (col >= N) break;
+            if constexpr (OUT_I32) {
+              int32_t* dst = static_cast<int32_t*>(yv) + size_t(row) * N + col;
+              reinterpret_cast<int4*>(dst)[0] =
+                  make_int4(int(v[j]) >> 8, int(v[j + 1]) >> 8, int(v[j + 2]) >> 8, int(v[j + 3]) >> 8);
+              reinterpret_cast<int4*>(dst)[1] =
+                  make_int4(int(v[j + 4]) >> 8, int(v[j + 5]) >> 8, int(v[j + 6]) >> 8, int(v[j + 7]) >> 8);
+            } else {
+              const float4 w0 = __ldg(reinterpret_cast<const float4*>(sw + col));
+              const float4 w1 = __ldg(reinterpret_cast<const float4*>(sw + col + 4));
+              const float f0 = float(int(v[j + 0])) * s_a * w0.x, f1 = float(int(v[j + 1])) * s_a * w0.y;
+              const float f2 = float(int(v[j + 2])) * s_a * w0.z, f3 = float(int(v[j + 3])) * s_a * w0.w;
+              const float f4 = float(int(v[j + 4])) * s_a * w1.x, f5 = float(int(v[j + 5])) * s_a * w1.y;
+              const float f6 = float(int(v[j + 6])) * s_a * w1.z, f7 = float(int(v[j + 7])) * s_a * w1.w;
+              uint4 o;
+              if constexpr (BF16) {
+                __nv_bfloat162 h0 = __floats2bfloat162_rn(f0, f1), h1 = __floats2bfloat162_rn(f2, f3);
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(f4, f5), h3 = __floats2bfloat162_rn(f6, f7);
+                o = make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                               *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
+                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(yv) + size_t(row) * N + col) = o;
+              } else {
+                o = make_uint4(pack_half2(f0, f1), pack_half2(f2, f3), pack_half2(f4, f5), pack_half2(f6, f7));
+                *reinterpret_cast<uint4*>(static_cast<__half*>(yv) + size_t(row) * N + col) = o;
+              }
+            }
+          }
+        }
+      }
+      tc::fence_before();
+      named_bar_sync(2, NUM_EPI_WARPS * 32);
+      if (threadIdx.x == 0) {
+        if (rank == 0) tc::mbar_arrive(&tempty[buf]);
+        else tc::mbar_arrive_cluster(&tempty[buf], 0);
+      }
+    }
+  }
+
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();
+  if (warp == MMA_WARP) {
+    tc::fence_after();
+    tc::tmem_dealloc2(tmem_base, TMEM_COLS);
+  }
+}
+
+}  // namespace g3
+
+bool gemm_pair_supported(const GemmArgs& a) {
+  return a.K % 32 == 0 && a.K <= 131072 && a.N % 8 == 0 && a.T <= int64_t(1) << 30;
+}
+
+cudaError_t gemm_pair_launch(const GemmArgs& a) {
+  using namespace g3;
+  auto kern = a.out_i32 ? gemm_pair_kernel<true, false>
+                        : (a.y_bf16 ? gemm_pair_kernel<false, true> : gemm_pair_kernel<false, false>);
+  static bool attr_done[3] = {false, false, false};
+  const int which = a.out_i32 ? 0 : (a.y_bf16 ? 1 : 2);
+  if (!attr_done[which]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    if (e != cudaSuccess) return e;
+    attr_done[which] = true;
+  }
+  const int num_tiles = int((a.T + BM - 1) / BM) * ((a.N + BN - 1) / BN);
+  const int clusters = std::max(1, std::min(num_tiles, num_sms() / 2));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(2 * clusters));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = a.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a.qa, a.sa, int(a.T), a.K, a.qw, a.sw, a.N, a.y);
+  count_launch();
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+}  // namespace fq

@@ -42,7 +42,9 @@ cudaError_t transform_quant_launch(const TQArgs& a);
 bool tq_simt_supported(int n1, int n2);
 
 cudaError_t gemm_mma_launch(const GemmArgs& a);      // legacy mma.sync cross-check kernel
-cudaError_t gemm_tc05_launch(const GemmArgs& a);     // tcgen05 kind::i8 kernel
+cudaError_t gemm_tc05_launch(const GemmArgs& a);     // tcgen05 kind::i8, single CTA
 bool gemm_tc05_supported(const GemmArgs& a);
+cudaError_t gemm_pair_launch(const GemmArgs& a);     // tcgen05 kind::i8, CTA pair (cta_group::2)
+bool gemm_pair_supported(const GemmArgs& a);
 
 }  // namespace fq

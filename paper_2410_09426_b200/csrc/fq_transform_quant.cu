@@ -34,9 +34,12 @@ struct TQCfg {
   static constexpr int X_ELEMS = N1 * XPITCH;    // one token tile
   static constexpr int P2_ELEMS = N2 * XPITCH;
   static constexpr int QBYTES = N1 * N2 / 2;     // packed codes per token
-  // smem: P2 | per team: X[2] | staging codes | strip maxima
-  static constexpr size_t SMEM = size_t(P2_ELEMS) * 2 +
-                                 size_t(TEAMS) * (size_t(NBUF * X_ELEMS) * 2 + QBYTES + WARPS * 4 + 16);
+  // smem: P2 | per team: X[NBUF] | staging codes | strip maxima (each team 128-B aligned)
+  static constexpr size_t P2_BYTES = (size_t(P2_ELEMS) * 2 + 127) / 128 * 128;
+  static constexpr size_t QOFF = size_t(NBUF * X_ELEMS) * 2;
+  static constexpr size_t MAXOFF = QOFF + (QBYTES + 15) / 16 * 16;
+  static constexpr size_t TEAM_BYTES = (MAXOFF + WARPS * 4 + 127) / 128 * 128;
+  static constexpr size_t SMEM = P2_BYTES + size_t(TEAMS) * TEAM_BYTES;
 };
 
 template <int N1, int N2, bool BF16, bool WRITE_Y, int TEAMS, int NBUF>
@@ -58,11 +61,10 @@ tq_mma_kernel(const uint16_t* __restrict__ x, int64_t T, int64_t ldx,
   const int warp = tt / 32;
   const int lane = threadIdx.x % 32;
   const int g = lane >> 2, qd = lane & 3;
-  uint8_t* team_base = smem + size_t(C::P2_ELEMS) * 2 +
-                       size_t(team) * (size_t(NBUF * C::X_ELEMS) * 2 + C::QBYTES + WARPS * 4 + 16);
+  uint8_t* team_base = smem + C::P2_BYTES + size_t(team) * C::TEAM_BYTES;
   uint16_t* sX = reinterpret_cast<uint16_t*>(team_base);
-  uint8_t* sQ = team_base + size_t(NBUF * C::X_ELEMS) * 2;
-  float* sMax = reinterpret_cast<float*>(sQ + ((C::QBYTES + 15) / 16) * 16);
+  uint8_t* sQ = team_base + C::QOFF;
+  float* sMax = reinterpret_cast<float*>(team_base + C::MAXOFF);
 
   // ---- P2 -> smem (whole CTA), padded rows, always as fp16: stage 2 runs in fp16 so the
   //      re-fed intermediate keeps an 11-bit mantissa (a bf16 intermediate fails the code

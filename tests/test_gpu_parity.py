@@ -120,7 +120,7 @@ def test_transform_strided_rows_and_empty():
     assert q0.shape == (0, n1 * n2 // 2)
 
 
-@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("impl", [0, 1, 2])
 @pytest.mark.parametrize("T,N,K", [(1, 8, 32), (37, 24, 96), (128, 256, 128), (300, 520, 4096),
                                    (2048, 4096, 4096), (257, 4096, 14336), (64, 28672, 4096)])
 def test_gemm_i32_bit_exact(impl, T, N, K):
@@ -147,7 +147,7 @@ def test_gemm_i32_extreme_values():
 
 
 @pytest.mark.parametrize("out_dtype", [torch.float16, torch.bfloat16])
-@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("impl", [0, 1, 2])
 def test_w4a4_linear_dequant(out_dtype, impl):
     T, N, K = 333, 776, 2048
     qa = synth.random_codes(T, K, seed=1, tag="qa")
