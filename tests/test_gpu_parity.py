@@ -187,11 +187,14 @@ def _chain(cfg, lin, tokens, seed=0, alpha=0.9, full_weight_prep=True):
     torch.cuda.synchronize()
     assert torch.equal(y, yfull)                        # the fused entry point is the same path
     rows = tokens if tokens is not None else np.arange(T)
+    rows = np.asarray(rows)
     qo, so, yo = O.transform_quant(x[rows], p1, p2, alpha)
     parity.check_transform(np_of(qa[torch.as_tensor(rows, device=DEV)]), np_of(sa)[rows], None, yo, qo, so,
                            label=f"{lin.name} transform")
     out_o = O.w4a4_linear(qo, so, qw, sw32.astype(np.float64))
-    return parity.check_output(np_of(y)[rows], out_o, label=f"{lin.name} output")
+    qa_rows = O.unpack_int4(np_of(qa[torch.as_tensor(rows, device=DEV)]))
+    out_same = O.w4a4_linear(qa_rows, np_of(sa)[rows].astype(np.float64), qw, sw32.astype(np.float64))
+    return parity.check_output(np_of(y)[rows], out_o, out_same, label=f"{lin.name} output")
 
 
 def sample_rows(T, seed=0):
@@ -232,14 +235,21 @@ def test_determinism():
 
 
 def test_gpu_weight_prep_matches_oracle():
-    """NEXT-2 preview: W' = P1^{-1} W~ P2^{-T} via the activation kernel with (P1^{-T}, P2^{-T}).
-    The fp16-rounded inverses perturb W' by ~1e-3 relative; compare dequantized weights."""
+    """NEXT-2 preview: W' = P1^{-1} W~ P2^{-T} via the activation kernel with
+    (P1^{-T}, P2^{-T}) rounded to fp16 on the host.  Parity: the oracle's transform+quant of W
+    with those same fp16 matrices (bars 2-3, per output channel); plus the dequantized weights
+    against the exact float64 W' within the 4-bit RTN step (half a step + the fp16 rounding of
+    the inverses)."""
     n1, n2, N = 64, 64, 512
     w = synth.weights(N, n1 * n2, seed=3)
     p1 = synth.well_conditioned(n1, seed=3, tag="p1")
     p2 = synth.well_conditioned(n2, seed=3, tag="p2")
     qw, sw = fq.prepare_weight(to_dev(w), n1, n2, to_dev(p1), to_dev(p2), 1.0)
+    p1i_t = np.linalg.inv(p1.astype(np.float64)).T.astype(np.float16)
+    p2i_t = np.linalg.inv(p2.astype(np.float64)).T.astype(np.float16)
+    qo, so, yo = O.transform_quant(w, p1i_t, p2i_t, 1.0)
+    parity.check_transform(np_of(qw), np_of(sw), None, yo, qo, so, label="weight prep")
     _, _, wp = O.prepare_weight(w, p1, p2, 1.0)
     deq = O.dequantize_rows(O.unpack_int4(np_of(qw)), np_of(sw).astype(np.float64))
-    assert np.linalg.norm(deq - wp) / np.linalg.norm(wp) < 0.15     # 4-bit RTN error dominates
-    assert np.all(np.abs(np_of(sw) / (np.abs(wp).max(1) / 7) - 1) < 1e-2)
+    step = np_of(sw).astype(np.float64)[:, None]
+    assert np.all(np.abs(deq - wp) <= 0.5 * step + 2e-2 * np.abs(wp).max(1, keepdims=True))
