@@ -136,6 +136,13 @@ fq_status fq_choose_decomposition(int64_t n, int32_t* n1, int32_t* n2);
  * cross-check kernel, 2 = tcgen05 kind::i8 on a single CTA.  Returns FQ_EINVAL otherwise. */
 fq_status fq_set_gemm_impl(int32_t impl);
 
+/* Selects the transform+quant implementation for subsequent calls in this process (testing
+ * aid): 0 = default (tcgen05/TMEM/TMA kernel for n2 in {64,128} with n1 = 64, or n2 = 128 with
+ * n1 in {80,96,112,128}; otherwise the legacy mma.sync kernel where instantiated, else the
+ * CUDA-core kernel), 1 = legacy mma.sync kernel (else CUDA cores), 2 = CUDA-core kernel.
+ * Returns FQ_EINVAL otherwise.  All implementations compute the same function. */
+fq_status fq_set_tq_impl(int32_t impl);
+
 /* Number of kernel launches issued by this library since process start (bench accounting). */
 uint64_t fq_launch_count(void);
 

@@ -12,6 +12,9 @@ import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libflatquant.so")
+# FQ_TRACE_LIB=1 loads the instrumented build (device timelines; profiling scripts only)
+if os.environ.get("FQ_TRACE_LIB") == "1":
+    LIB_PATH = os.path.join(HERE, "libflatquant_trace.so")
 
 FQ_OK, FQ_EINVAL, FQ_ESHAPE, FQ_ENOTSUP, FQ_ECUDA = 0, 1, 2, 3, 4
 FQ_F16, FQ_BF16 = 0, 1
@@ -32,6 +35,7 @@ SIGNATURES = {
                                         _vp, _i32, _vp, _vp, _vp]),
     "fq_choose_decomposition": (_i32, [_i64, _c.POINTER(_i32), _c.POINTER(_i32)]),
     "fq_set_gemm_impl": (_i32, [_i32]),
+    "fq_set_tq_impl": (_i32, [_i32]),
     "fq_launch_count": (_u64, []),
     "fq_status_string": (_c.c_char_p, [_i32]),
     "fq_abi_version": (_i32, []),

@@ -15,7 +15,7 @@ from ._lib import FQ_BF16, FQ_F16, FQ_SYM, check, load
 
 __all__ = [
     "fq_transform_quant", "fq_transform_f32", "fq_w4a4_linear", "fq_w4a4_gemm_i32", "fq_flatquant_linear",
-    "fq_flatquant_linear_host", "fq_choose_decomposition", "fq_set_gemm_impl", "fq_launch_count",
+    "fq_flatquant_linear_host", "fq_choose_decomposition", "fq_set_gemm_impl", "fq_set_tq_impl", "fq_launch_count",
     "fq_abi_version", "transform_quant", "transform_f32", "w4a4_linear", "w4a4_gemm_i32", "prepare_weight",
     "flatquant_linear",
 ]
@@ -105,6 +105,10 @@ def fq_choose_decomposition(n: int) -> tuple[int, int]:
 
 def fq_set_gemm_impl(impl: int) -> None:
     check("fq_set_gemm_impl", load().fq_set_gemm_impl(int(impl)))
+
+
+def fq_set_tq_impl(impl: int) -> None:
+    check("fq_set_tq_impl", load().fq_set_tq_impl(int(impl)))
 
 
 def fq_launch_count() -> int:

@@ -37,25 +37,31 @@ def _digest() -> str:
     return h.hexdigest()
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    stamp = LIB + ".sha256"
-    dig = _digest()
-    if not force and os.path.exists(LIB) and os.path.exists(stamp) and open(stamp).read() == dig:
-        return LIB
-    cmd = [NVCC] + NVCC_FLAGS + ["-o", LIB] + sources()
+TRACE_LIB = os.path.join(HERE, "libflatquant_trace.so")
+
+
+def build(verbose: bool = False, force: bool = False, trace: bool = False) -> str:
+    """Build libflatquant.so; trace=True builds the instrumented libflatquant_trace.so instead
+    (-DFQ_TRACE: device timelines for scripts/trace_tq.py; never loaded by the product)."""
+    lib = TRACE_LIB if trace else LIB
+    stamp = lib + ".sha256"
+    dig = _digest() + ("-trace" if trace else "")
+    if not force and os.path.exists(lib) and os.path.exists(stamp) and open(stamp).read() == dig:
+        return lib
+    cmd = [NVCC] + NVCC_FLAGS + (["-DFQ_TRACE"] if trace else []) + ["-o", lib] + sources()
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = r.stdout + r.stderr
-    with open(os.path.join(HERE, "build.log"), "w") as f:
+    with open(os.path.join(HERE, "build_trace.log" if trace else "build.log"), "w") as f:
         f.write(" ".join(cmd) + "\n" + log)
     if r.returncode != 0:
         sys.stderr.write(log)
-        raise RuntimeError("nvcc failed building libflatquant.so (see paper_2410_09426_b200/build.log)")
+        raise RuntimeError(f"nvcc failed building {os.path.basename(lib)} (see paper_2410_09426_b200/build*.log)")
     if verbose:
         sys.stderr.write(log)
     with open(stamp, "w") as f:
         f.write(dig)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, trace="--trace" in sys.argv))

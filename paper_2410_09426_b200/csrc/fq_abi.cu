@@ -13,6 +13,9 @@ namespace fq {
 static std::atomic<uint64_t> g_launches{0};
 static std::atomic<int> g_last_cuda_error{0};
 static std::atomic<int> g_gemm_impl{0};
+static std::atomic<int> g_tq_impl{0};
+
+int tq_impl() { return g_tq_impl.load(); }
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
@@ -76,7 +79,6 @@ static fq_status run_tq(const void* x, int32_t x_dtype, int64_t T, int64_t ldx, 
   a.scale = scale;
   a.y = y;
   a.bf16 = (x_dtype == FQ_BF16);
-  a.force_simt = false;
   a.stream = static_cast<cudaStream_t>(stream);
   const bool tc = (n1 % 16 == 0) && (n2 % 16 == 0);
   if (!tc && !tq_simt_supported(n1, n2)) return FQ_ENOTSUP;
@@ -208,6 +210,12 @@ fq_status fq_choose_decomposition(int64_t n, int32_t* n1, int32_t* n2) {
     }
   *n1 = int32_t(b1);
   *n2 = int32_t(b2);
+  return FQ_OK;
+}
+
+fq_status fq_set_tq_impl(int32_t impl) {
+  if (impl < 0 || impl > 2) return FQ_EINVAL;
+  g_tq_impl.store(impl);
   return FQ_OK;
 }
 

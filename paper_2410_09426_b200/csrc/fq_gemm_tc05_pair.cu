@@ -25,6 +25,20 @@
 namespace fq {
 namespace g3 {
 
+// Optional device timeline of the first CTA pair (build with -DFQ_TRACE; scripts/trace_gemm.py).
+#ifdef FQ_TRACE
+__device__ unsigned long long g_trace[2 * 256];
+FQ_DEVICE void trace(int ev) {
+  if (blockIdx.x < 2 && ev < 256) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+    g_trace[blockIdx.x * 256 + ev] = t;
+  }
+}
+#else
+FQ_DEVICE void trace(int) {}
+#endif
+
 constexpr int BM = 256, BM_CTA = 128;     // tokens per pair tile / per CTA
 constexpr int BN = 192, BN_CTA = 96;      // features per pair tile / B rows per CTA
 constexpr int BK = 128;                   // int8 K per stage
@@ -41,7 +55,10 @@ constexpr int B_WARP0 = 13, NUM_B_WARPS = 6;
 constexpr int NUM_CONV_WARPS = NUM_A_WARPS + NUM_B_WARPS;
 constexpr int THREADS = (B_WARP0 + NUM_B_WARPS) * 32;
 constexpr int B_TASKS = BN_CTA * 4 / (NUM_B_WARPS * 32);    // 16-byte packed chunks per B thread
-constexpr int PF = 4;                                       // K-blocks of register prefetch
+#ifndef FQ_GEMM_PF
+#define FQ_GEMM_PF 6
+#endif
+constexpr int PF = FQ_GEMM_PF;                              // K-blocks of register prefetch
 constexpr size_t SMEM_BYTES = size_t(STAGES) * B_BYTES + 1024 + 256;
 constexpr uint32_t IDESC = tc::idesc_i8(BM, BN);
 static_assert(TMEM_A0 + STAGES * A_COLS <= TMEM_COLS, "TMEM budget");
@@ -104,6 +121,7 @@ gemm_pair_kernel(const uint8_t* __restrict__ qa, const float* __restrict__ sa, i
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) trace(250);
   const uint32_t rank = tc::cluster_ctarank();
   Sched sc;
   sc.num_m = (T + BM - 1) / BM;
@@ -138,11 +156,14 @@ gemm_pair_kernel(const uint8_t* __restrict__ qa, const float* __restrict__ sa, i
   // All converter warps of this CTA finish a stage, then ONE thread signals the leader's
   // `full` barrier: a CTA-scope arrive in the leader, a single release.cluster remote arrive in
   // the peer (one cluster-scope fence per stage instead of one per warp).
+  int jtrace = 0;
   auto signal_full = [&](uint64_t* bar) {
     named_bar_sync(1, NUM_CONV_WARPS * 32);
     if (threadIdx.x == A_WARP0 * 32) {
       if (rank == 0) tc::mbar_arrive(bar);
       else tc::mbar_arrive_cluster(bar, 0);
+      if (jtrace < 64) trace(jtrace);
+      ++jtrace;
     }
   };
 
@@ -188,20 +209,27 @@ gemm_pair_kernel(const uint8_t* __restrict__ qa, const float* __restrict__ sa, i
         for (int u = 0; u < PF; ++u) {
           if (!cv.valid) break;
           tc::mbar_wait(&empty[stage], phase ^ 1);
+          const int jt = jtrace;
+          const bool trA = threadIdx.x == A_WARP0 * 32 && jt >= 16 && jt < 28;
+          if (trA) trace(160 + (jt - 16) * 4 + 0);
           uint32_t w[16];
 #pragma unroll
           for (int i = 0; i < 8; ++i) widen8(ring[u][i], w[2 * i], w[2 * i + 1]);
-          load(ring[u]);                                          // refill this slot PF jobs ahead
           tmem_st16(tl + uint32_t(stage * A_COLS), w);
+          if (trA) trace(160 + (jt - 16) * 4 + 1);
           tc::tmem_st_wait();
           tc::fence_before();
+          if (trA) trace(160 + (jt - 16) * 4 + 2);
           signal_full(&full[stage]);
+          if (trA) trace(160 + (jt - 16) * 4 + 3);
+          load(ring[u]);            // refill this slot PF jobs ahead (after the barrier: nothing waits on it)
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           cv.next(sc);
         }
       }
     } else {
       const int ct = threadIdx.x - B_WARP0 * 32;
+      int bjob = 0;
       uint4 ring[PF][B_TASKS];
       auto load = [&](uint4 (&r)[B_TASKS]) {
 #pragma unroll
@@ -221,22 +249,29 @@ gemm_pair_kernel(const uint8_t* __restrict__ qa, const float* __restrict__ sa, i
         for (int u = 0; u < PF; ++u) {
           if (!cv.valid) break;
           tc::mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sB = smem + size_t(stage) * B_BYTES;
+          const bool trB = threadIdx.x == B_WARP0 * 32 && bjob >= 16 && bjob < 28;
+          if (trB) trace(208 + (bjob - 16) * 3 + 0);
+          const uint32_t sB = smem_u32(smem + size_t(stage) * B_BYTES);
 #pragma unroll
           for (int i = 0; i < B_TASKS; ++i) {
             const int task = ct + i * NUM_B_WARPS * 32, rl = task >> 2, c = task & 3;
-            uint4 o0, o1;
-            widen8(ring[u][i].x, o0.x, o0.y);
-            widen8(ring[u][i].y, o0.z, o0.w);
-            widen8(ring[u][i].z, o1.x, o1.y);
-            widen8(ring[u][i].w, o1.z, o1.w);
-            uint8_t* rowp = sB + rl * 128;
-            *reinterpret_cast<uint4*>(rowp + (((2 * c) ^ (rl & 7)) << 4)) = o0;
-            *reinterpret_cast<uint4*>(rowp + (((2 * c + 1) ^ (rl & 7)) << 4)) = o1;
+            uint32_t o[8];
+            widen8(ring[u][i].x, o[0], o[1]);
+            widen8(ring[u][i].y, o[2], o[3]);
+            widen8(ring[u][i].z, o[4], o[5]);
+            widen8(ring[u][i].w, o[6], o[7]);
+            const uint32_t rowp = sB + uint32_t(rl * 128);
+            tc::sts128(rowp + uint32_t(((2 * c) ^ (rl & 7)) << 4), o[0], o[1], o[2], o[3]);
+            tc::sts128(rowp + uint32_t(((2 * c + 1) ^ (rl & 7)) << 4), o[4], o[5], o[6], o[7]);
           }
-          load(ring[u]);
+          // fence.proxy.async is a CTA membar: it would wait for every load in flight, so the
+          // prefetch for this ring slot is issued only after the stage is signalled
+          if (trB) trace(208 + (bjob - 16) * 3 + 1);
           tc::fence_proxy_async_smem();
+          if (trB) trace(208 + (bjob - 16) * 3 + 2);
           signal_full(&full[stage]);
+          ++bjob;
+          load(ring[u]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           cv.next(sc);
         }
@@ -256,6 +291,7 @@ gemm_pair_kernel(const uint8_t* __restrict__ qa, const float* __restrict__ sa, i
         for (int kb = 0; kb < sc.num_kb; ++kb) {
           tc::mbar_wait_cluster(&full[stage], phase);
           tc::fence_after();
+          if (it * sc.num_kb + kb < 64) trace(64 + it * sc.num_kb + kb);
           const uint32_t a_t = tmem_base + uint32_t(TMEM_A0 + stage * A_COLS);
           const uint32_t b0 = smem_u32(smem + size_t(stage) * B_BYTES);
 #pragma unroll
@@ -266,6 +302,7 @@ gemm_pair_kernel(const uint8_t* __restrict__ qa, const float* __restrict__ sa, i
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         tc::mma_commit_pair(&tfull[buf], 0x3);
+        if (it < 8) trace(128 + it);
       }
     }
     __syncwarp();
@@ -279,6 +316,7 @@ gemm_pair_kernel(const uint8_t* __restrict__ qa, const float* __restrict__ sa, i
       const int buf = it & 1;
       tc::mbar_wait(&tfull[buf], (it >> 1) & 1);
       tc::fence_after();
+      if (threadIdx.x == 0 && it < 8) trace(136 + it);
       const int row = mb * BM + int(rank) * BM_CTA + r_local;
       const bool row_ok = row < T;
       const float s_a = (!OUT_I32 && row_ok) ? sa[row] * (1.0f / 256.0f) : 0.f;
@@ -326,6 +364,7 @@ gemm_pair_kernel(const uint8_t* __restrict__ qa, const float* __restrict__ sa, i
       if (threadIdx.x == 0) {
         if (rank == 0) tc::mbar_arrive(&tempty[buf]);
         else tc::mbar_arrive_cluster(&tempty[buf], 0);
+        if (it < 8) trace(144 + it);
       }
     }
   }
@@ -336,10 +375,17 @@ gemm_pair_kernel(const uint8_t* __restrict__ qa, const float* __restrict__ sa, i
   if (warp == MMA_WARP) {
     tc::fence_after();
     tc::tmem_dealloc2(tmem_base, TMEM_COLS);
+    if (lane == 0) trace(251);
   }
 }
 
 }  // namespace g3
+
+#ifdef FQ_TRACE
+extern "C" int fq_debug_trace_gemm(unsigned long long* out) {
+  return int(cudaMemcpyFromSymbol(out, g3::g_trace, sizeof(unsigned long long) * 512));
+}
+#endif
 
 bool gemm_pair_supported(const GemmArgs& a) {
   return a.K % 32 == 0 && a.K <= 131072 && a.N % 8 == 0 && a.T <= int64_t(1) << 30;

@@ -17,7 +17,6 @@ struct TQArgs {
   float* scale;
   float* y;         // optional fp32 export of the transformed activations (debug / parity)
   bool bf16;
-  bool force_simt;
   cudaStream_t stream;
 };
 
@@ -38,8 +37,14 @@ struct GemmArgs {
 int num_sms();
 void count_launch();
 
-cudaError_t transform_quant_launch(const TQArgs& a);
+cudaError_t transform_quant_launch(const TQArgs& a);   // impl selection (fq_set_tq_impl)
 bool tq_simt_supported(int n1, int n2);
+bool tq_mma_supported(int n1, int n2);                 // legacy mma.sync kernel instantiations
+cudaError_t tq_mma_launch(const TQArgs& a);
+cudaError_t tq_simt_launch(const TQArgs& a);
+bool tq_tc05_supported(const TQArgs& a);               // tcgen05 / TMA kernel
+cudaError_t tq_tc05_launch(const TQArgs& a);
+int tq_impl();
 
 cudaError_t gemm_mma_launch(const GemmArgs& a);      // legacy mma.sync cross-check kernel
 cudaError_t gemm_tc05_launch(const GemmArgs& a);     // tcgen05 kind::i8, single CTA

@@ -1,0 +1,535 @@
+// fq_tq_tc05.cu -- fused Kronecker transform + clip + per-token INT4 quantize + pack on the
+// 5th-generation tensor cores (tcgen05, TMEM, TMA).
+//
+// Per token t (Eq.3 activation factor; clip PAPER.md:258-259; per-token
+// symmetric INT4 PAPER.md:367, Eq.1):
+//   V_t = reshape(x_t, n1, n2) (row-major)   W_t = P1^T V_t   Y_t = W_t P2
+//   s_t = alpha max|Y_t| / 7 (1 if Y_t == 0)  q = clamp(rint(Y_t / s_t), -8, 7), packed
+//
+// P1^T is applied first, as in the paper's kernel (App. B.3).  Both small
+// matmuls run as tcgen05.mma kind::f16 with M = 128 and every operand in the MN-major
+// SWIZZLE_128B shared-memory layout, so the token tiles, P1 and P2 are TMA-loaded exactly as they
+// sit in HBM (no transposes):
+//   stage 1  D1[(t,j)][i] = sum_i' X_t[i'][j] P1[i'][i]   (= W_t^T)  A = X tile  [K=i'][M=(t,j)]
+//                                                                  B = P1      [K=i'][N=i]
+//   stage 2  D2[(t,i)][j] = sum_j' W_t[i][j'] P2[j'][j]   (= Y_t)    A = W (smem) [K=j'][M=(t,i)]
+//                                                                  B = P2      [K=j'][N=j]
+// Between the stages an epilogue moves W from TMEM (fp32) to shared memory as fp16 after an
+// exact per-token power-of-two prescale (reading R9: an fp16 intermediate, never bf16;
+// the prescale makes it overflow/underflow-safe and is divided out of Y exactly).  D2 lane (t,i)
+// holds row i of Y_t, so the quantized row is packed in registers and stored contiguously.
+//
+// Tile = TOK tokens (2 for n1 = 64, else 1), so that both MMAs have M = 128.  Warp roles
+// (persistent, one CTA per SM, tiles strided by gridDim):
+//   warp 0      TMA producer: P1, P2 once, then X tiles into a STAGES-deep ring
+//   warp 1      MMA issuer (one thread): stage 1 of tile k+1 is issued before stage 2 of tile k
+//   warp 2      TMEM allocator
+//   warps 4-7   epilogue group 0 (even tiles), warps 8-11 group 1 (odd tiles): each group does
+//               stage-1 epilogue (prescale, fp16, smem) and stage-2 epilogue (absmax, quantize,
+//               pack, store) of its own tiles; TMEM/smem buffers are indexed by the group.
+#include <cstdint>
+#include <mutex>
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include "fq_device.cuh"
+#include "fq_internal.h"
+#include "fq_tc05.cuh"
+
+namespace fq {
+namespace tq5 {
+
+// Optional device-side timeline (build with -DFQ_TRACE, scripts/trace_tq.py): globaltimer stamps
+// of the pipeline events of the first TRACE_CTAS CTAs.  Compiled out of the production library.
+constexpr int TRACE_CTAS = 4, TRACE_EV = 256;
+#ifdef FQ_TRACE
+__device__ unsigned long long g_trace[TRACE_CTAS * TRACE_EV];
+__device__ unsigned long long g_cta[1024 * 2];     // every CTA: start, end
+__device__ unsigned long long g_stamp[8];
+FQ_DEVICE unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+  return t;
+}
+__global__ void stamp_kernel(int slot) { g_stamp[slot] = gtimer(); }
+FQ_DEVICE void cta_stamp(int which) {
+  if (blockIdx.x < 1024) g_cta[blockIdx.x * 2 + which] = gtimer();
+}
+FQ_DEVICE void trace(int ev) {
+  if (blockIdx.x < TRACE_CTAS && ev < TRACE_EV) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+    g_trace[blockIdx.x * TRACE_EV + ev] = t;
+  }
+}
+#else
+FQ_DEVICE void trace(int) {}
+FQ_DEVICE void cta_stamp(int) {}
+#endif
+
+constexpr int THREADS = 12 * 32;
+constexpr int SMEM_LIMIT = 232448;       // max dynamic smem per block on sm_100
+constexpr int SMEM_OVERHEAD = 1024 + 512;  // 1024-B alignment slack + barriers/scratch
+
+template <int N1, int N2>
+struct Cfg {
+  static_assert(N2 == 64 || N2 == 128, "n2 in {64, 128}");
+  static_assert(N1 % 16 == 0 && N1 >= 16 && N1 <= 128, "n1 multiple of 16, <= 128");
+  static_assert(N1 == 64 || N2 == 128, "n1 != 64 needs n2 == 128 (stage-1 M = n2)");
+  static constexpr int TOK = (N1 == 64) ? 2 : 1;       // tokens per tile
+  static constexpr int JB = N2 / 64;                   // 64-element j blocks of a token row
+  static constexpr int G1 = TOK * N2 / 128;            // stage-1 MMA groups (M = 128) per tile
+  static constexpr int P1_ATOMS = (N1 + 63) / 64;
+  static constexpr int P1_BYTES = P1_ATOMS * N1 * 128;
+  static constexpr int P2_BYTES = JB * N2 * 128;
+  static constexpr int X_BYTES = TOK * JB * N1 * 128;  // TOK * n * 2
+  static constexpr int A2_BYTES = 2 * N2 * 128;        // 2 M-atoms x N2 K-rows x 128 B
+  static constexpr int D1C = G1 * N1;                  // TMEM columns of one stage-1 result
+  static constexpr int TMEM_COLS = (2 * D1C + 2 * N2) <= 256 ? 256 : 512;
+  static constexpr int FIXED = P1_BYTES + P2_BYTES + 2 * A2_BYTES;
+  static constexpr int STAGES_FIT = (SMEM_LIMIT - SMEM_OVERHEAD - FIXED) / X_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static constexpr size_t SMEM = size_t(FIXED) + size_t(STAGES) * X_BYTES + SMEM_OVERHEAD;
+  static_assert(2 * D1C + 2 * N2 <= 512, "TMEM budget");
+  static_assert(STAGES >= 2, "shared-memory budget");
+};
+
+constexpr float MAGIC = 12582912.0f;   // 1.5 * 2^23: fma(y, c, MAGIC) rounds y*c half-to-even
+
+// per-token exact power-of-two exponent e with m * 2^e in [2^14, 2^15) (fp16-safe); m >= 0 and
+// finite.  A subnormal (or zero) m gets the largest scale 2^126.
+FQ_DEVICE int prescale_exp(float m) {
+  const int be = int(__float_as_uint(m) >> 23);       // biased exponent (sign bit is 0)
+  if (be == 0) return 126;
+  const int e = 14 - (be - 127);
+  return e < -126 ? -126 : (e > 126 ? 126 : e);
+}
+
+FQ_DEVICE float exp2i(int e) { return __int_as_float((127 + e) << 23); }
+
+FQ_DEVICE float max3f(float a, float b, float c) {   // FMNMX3 (sm_100); |.| folds into operand modifiers
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+FQ_DEVICE float fma_sat(float a, float b, float c) {  // FFMA.SAT: clamp to [0, 1]
+  float r;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// max |v[i]| over N values: 8 independent accumulators fed two values per 3-input max
+// (a running max would be a dependent chain of N operations)
+template <int N>
+FQ_DEVICE float absmax(const uint32_t* v) {
+  static_assert(N % 16 == 0, "");
+  float a[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) a[e] = fmaxf(fabsf(__uint_as_float(v[e])), fabsf(__uint_as_float(v[8 + e])));
+#pragma unroll
+  for (int i = 16; i < N; i += 16)
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      a[e] = max3f(a[e], fabsf(__uint_as_float(v[i + e])), fabsf(__uint_as_float(v[i + 8 + e])));
+  return max3f(max3f(a[0], a[1], a[2]), max3f(a[3], a[4], a[5]), fmaxf(a[6], a[7]));
+}
+
+// 8 quantized values in MAGIC form (low nibble of the bit pattern = two's-complement code)
+// -> one 32-bit word, element 2m in the low nibble of byte m.
+FQ_DEVICE uint32_t pack8(const float (&v)[8]) {
+  const uint32_t e = __byte_perm(__byte_perm(__float_as_uint(v[0]), __float_as_uint(v[2]), 0x0040),
+                                 __byte_perm(__float_as_uint(v[4]), __float_as_uint(v[6]), 0x0040), 0x5410);
+  const uint32_t o = __byte_perm(__byte_perm(__float_as_uint(v[1]), __float_as_uint(v[3]), 0x0040),
+                                 __byte_perm(__float_as_uint(v[5]), __float_as_uint(v[7]), 0x0040), 0x5410);
+  return (e & 0x0F0F0F0Fu) | ((o << 4) & 0xF0F0F0F0u);
+}
+
+template <int N1, int N2, bool BF16, bool WRITE_Y>
+__global__ void __launch_bounds__(THREADS, 1)
+tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmP1,
+               const __grid_constant__ CUtensorMap tmP2, int64_t T, float alpha, uint8_t* __restrict__ q,
+               float* __restrict__ scale, float* __restrict__ y_out) {
+  using C = Cfg<N1, N2>;
+  constexpr int S = C::STAGES, TOK = C::TOK;
+  constexpr uint32_t IDESC1 = tc::idesc_f16(128, N1, BF16 ? 1 : 0, 1, 1);
+  constexpr uint32_t IDESC2 = tc::idesc_f16(128, N2, 0, 1, 1);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sP1 = smem;
+  uint8_t* sP2 = sP1 + C::P1_BYTES;
+  uint8_t* sA2 = sP2 + C::P2_BYTES;
+  uint8_t* sX = sA2 + 2 * C::A2_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sX + size_t(S) * C::X_BYTES);
+  uint64_t* xfull = bars;            // [S]  TMA -> MMA
+  uint64_t* xempty = bars + S;       // [S]  MMA commit -> TMA
+  uint64_t* pfull = bars + 2 * S;    // P1, P2 landed
+  uint64_t* d1full = pfull + 1;      // [2]  MMA commit -> epilogue group
+  uint64_t* a2full = d1full + 2;     // [2]  epilogue group (4 warps) -> MMA
+  uint64_t* d2full = a2full + 2;     // [2]  MMA commit -> epilogue group
+  __shared__ float red[16];                                    // [2 groups][2 parities][4 warps]
+  __shared__ uint32_t tmem_slot[1];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    trace(0);
+    cta_stamp(0);
+  }
+  const int num_tiles = int((T + TOK - 1) / TOK);                 // T < 2^31 (host check)
+  const int my_tiles = num_tiles > int(blockIdx.x) ? (num_tiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
+
+  // X tiles stream into the ring as early as possible (before the TMEM allocation completes)
+  auto issue_x = [&](int k) {
+    const int s = k % S;
+    tc::mbar_wait(&xempty[s], ((k / S) & 1) ^ 1);
+    tc::mbar_expect_tx(&xfull[s], C::X_BYTES);
+    const int t0 = (int(blockIdx.x) + k * int(gridDim.x)) * TOK;
+    uint8_t* dst = sX + size_t(s) * C::X_BYTES;
+#pragma unroll
+    for (int b = 0; b < C::JB; ++b) tc::tma_load_3d(dst + b * TOK * N1 * 128, &tmX, &xfull[s], b * 64, 0, t0);
+    if (k < 16) trace(8 + k);
+  };
+  const int prefill = my_tiles < S ? my_tiles : S;
+  if (threadIdx.x == 0) {
+    tc::tma_prefetch_desc(&tmX);
+    tc::tma_prefetch_desc(&tmP1);
+    tc::tma_prefetch_desc(&tmP2);
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(&xfull[s], 1);
+      tc::mbar_init(&xempty[s], 1);
+    }
+    tc::mbar_init(pfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&d1full[b], 1);
+      tc::mbar_init(&a2full[b], 4);
+      tc::mbar_init(&d2full[b], 1);
+    }
+    tc::fence_barrier_init();
+    tc::mbar_expect_tx(pfull, C::P1_BYTES + C::P2_BYTES);
+    for (int a = 0; a < C::P1_ATOMS; ++a) tc::tma_load_2d(sP1 + a * N1 * 128, &tmP1, pfull, a * 64, 0);
+    for (int b = 0; b < C::JB; ++b) tc::tma_load_2d(sP2 + b * N2 * 128, &tmP2, pfull, b * 64, 0);
+    for (int k = 0; k < prefill; ++k) issue_x(k);
+    trace(1);
+  }
+  if (warp == 2) tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  tc::mbar_wait(pfull, 0);
+  if (threadIdx.x == 0) trace(2);
+  if constexpr (BF16) {
+    // stage 2 runs in fp16 (R9): convert P2 in place (bf16 -> fp16 is exact in normal range)
+    for (int i = threadIdx.x; i < C::P2_BYTES / 16; i += THREADS) {
+      uint4* p = reinterpret_cast<uint4*>(sP2) + i;
+      uint4 v = *p;
+      uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+        w[h] = pack_half2(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xFFFF0000u));
+      *p = v;
+    }
+    tc::fence_proxy_async_smem();
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ================================ TMA producer ================================
+    if (lane == 0)
+      for (int k = prefill; k < my_tiles; ++k) issue_x(k);
+    __syncwarp();
+  } else if (warp == 1) {
+    // ================================ MMA issuer ================================
+    if (lane == 0) {
+      const uint32_t p1a = smem_u32(sP1), p2a = smem_u32(sP2);
+      auto mma1 = [&](int k) {
+        const int s = k % S, par = k & 1;
+        tc::mbar_wait(&xfull[s], (k / S) & 1);
+        tc::fence_after();
+        if (k < 16) trace(24 + k);
+        const uint32_t xs = smem_u32(sX + size_t(s) * C::X_BYTES);
+#pragma unroll
+        for (int g = 0; g < C::G1; ++g) {
+          // M = 128 rows (t, j): n2 = 64 -> the TOK tokens' j-block 0; n2 = 128 -> token g's 2 j-blocks
+          const uint32_t a0 = xs + uint32_t(N2 == 64 ? 0 : g * N1 * 128);
+          const uint32_t lbo = uint32_t(N2 == 64 ? N1 * 128 : TOK * N1 * 128);
+          const uint32_t d = tmem + uint32_t(par * C::D1C + g * N1);
+#pragma unroll
+          for (int kk = 0; kk < N1 / 16; ++kk)
+            tc::mma_ss<false>(d, tc::sdesc_sw128(a0 + kk * 2048, lbo, 1024),
+                              tc::sdesc_sw128(p1a + kk * 2048, N1 * 128, 1024), IDESC1, kk > 0);
+        }
+        tc::mma_commit(&xempty[s]);
+        tc::mma_commit(&d1full[par]);
+      };
+      auto mma2 = [&](int k) {
+        const int par = k & 1;
+        tc::mbar_wait(&a2full[par], (k >> 1) & 1);
+        tc::fence_after();
+        if (k < 16) trace(40 + k);
+        const uint32_t a0 = smem_u32(sA2 + par * C::A2_BYTES);
+        const uint32_t d = tmem + uint32_t(2 * C::D1C + par * N2);
+#pragma unroll
+        for (int kk = 0; kk < N2 / 16; ++kk)
+          tc::mma_ss<false>(d, tc::sdesc_sw128(a0 + kk * 2048, N2 * 128, 1024),
+                            tc::sdesc_sw128(p2a + kk * 2048, N2 * 128, 1024), IDESC2, kk > 0);
+        tc::mma_commit(&d2full[par]);
+      };
+      if (my_tiles > 0) mma1(0);
+      for (int k = 0; k < my_tiles; ++k) {
+        if (k + 1 < my_tiles) mma1(k + 1);
+        mma2(k);
+      }
+      trace(122);
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ================================ epilogue groups ================================
+    const int grp = (warp - 4) >> 2, qd = warp & 3;
+    const int L = qd * 32 + lane;                        // TMEM lane of this thread
+    const uint32_t lane_base = tmem + (uint32_t(qd * 32) << 16);
+    float* redg = red + grp * 8;
+    int rp = 0;
+    auto exchange = [&](float m) {                       // per-warp max -> all 4 warps' maxima
+      m = warp_max(m);
+      if (lane == 0) redg[rp * 4 + qd] = m;
+      named_bar_sync(1 + grp, 128);
+      float r[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) r[w] = redg[rp * 4 + w];
+      rp ^= 1;
+      return make_float4(r[0], r[1], r[2], r[3]);
+    };
+    constexpr int QROW = N2 / 2;                         // packed bytes per row i of a token
+    constexpr int QTOK = N1 * N2 / 2;                    // packed bytes per token
+    for (int k = grp; k < my_tiles; k += 2) {
+      const int par = k & 1;
+      const uint32_t ph = (k >> 1) & 1;
+      const int64_t t0 = int64_t(int(blockIdx.x) + k * int(gridDim.x)) * TOK;
+      // -------- stage-1 epilogue: D1 (fp32) -> prescaled fp16 A operand of stage 2 --------
+      int pe[TOK];                                       // per-token prescale exponents
+      tc::mbar_wait(&d1full[par], ph);
+      tc::fence_after();
+      if (L == 0 && k < 16) trace(56 + k);
+#define FQ_SUB(sub) \
+  if (L == 0 && k < 8) trace(128 + k * 16 + (sub))
+#pragma unroll
+      for (int g = 0; g < C::G1; ++g) {
+        uint32_t v[N1];
+#pragma unroll
+        for (int c = 0; c < N1 / 16; ++c)
+          tc::tmem_ld16(lane_base + uint32_t(par * C::D1C + g * N1 + c * 16),
+                        *reinterpret_cast<uint32_t(*)[16]>(&v[c * 16]));
+        tc::tmem_ld_wait();
+        FQ_SUB(1);
+        const float4 r = exchange(absmax<N1>(v));
+        FQ_SUB(2);
+        int tt;
+        if constexpr (N2 == 64) {                        // tokens = lane halves (quadrants 0-1, 2-3)
+          pe[0] = prescale_exp(fmaxf(r.x, r.y));
+          if constexpr (TOK > 1) pe[1] = prescale_exp(fmaxf(r.z, r.w));
+          tt = L >> 6;
+        } else {                                         // token g spans all 128 lanes
+          pe[g] = prescale_exp(fmaxf(fmaxf(r.x, r.y), fmaxf(r.z, r.w)));
+          tt = g;
+        }
+        const float pre = exp2i((TOK > 1 && tt) ? pe[TOK - 1] : pe[0]);
+        const int j = (N2 == 64) ? (L & 63) : L;         // K row (j') of the stage-2 A operand
+        const uint32_t row = smem_u32(sA2) + uint32_t(par * C::A2_BYTES + j * 128);
+#pragma unroll
+        for (int c8 = 0; c8 < N1 / 8; ++c8) {
+          const int atom = (N1 == 64) ? tt : (c8 >> 3), ch = c8 & 7;
+          tc::sts128(row + uint32_t(atom * (N2 * 128) + ((ch ^ (j & 7)) << 4)),
+                 pack_half2(__uint_as_float(v[8 * c8 + 0]) * pre, __uint_as_float(v[8 * c8 + 1]) * pre),
+                 pack_half2(__uint_as_float(v[8 * c8 + 2]) * pre, __uint_as_float(v[8 * c8 + 3]) * pre),
+                 pack_half2(__uint_as_float(v[8 * c8 + 4]) * pre, __uint_as_float(v[8 * c8 + 5]) * pre),
+                 pack_half2(__uint_as_float(v[8 * c8 + 6]) * pre, __uint_as_float(v[8 * c8 + 7]) * pre));
+        }
+      }
+      FQ_SUB(3);
+      tc::fence_proxy_async_smem();
+      FQ_SUB(4);
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&a2full[par]);
+      if (L == 0 && k < 16) trace(72 + k);
+
+      // -------- stage-2 epilogue: absmax, clip, quantize, pack, store --------
+      tc::mbar_wait(&d2full[par], ph);
+      tc::fence_after();
+      if (L == 0 && k < 16) trace(88 + k);
+      FQ_SUB(8);
+      uint32_t yv[N2];
+#pragma unroll
+      for (int c = 0; c < N2 / 16; ++c)
+        tc::tmem_ld16(lane_base + uint32_t(2 * C::D1C + par * N2 + c * 16),
+                      *reinterpret_cast<uint32_t(*)[16]>(&yv[c * 16]));
+      tc::tmem_ld_wait();
+      FQ_SUB(9);
+      tc::fence_before();
+      const int tt = (N1 == 64) ? (L >> 6) : 0;
+      const int i = (N1 == 64) ? (L & 63) : L;
+      const bool valid = (N1 == 64) || (L < N1);
+      const float4 r = exchange(valid ? absmax<N2>(yv) : 0.f);
+      FQ_SUB(10);
+      float mp;                                          // max |Y_t| * 2^pe (prescaled)
+      if constexpr (N1 == 64) mp = tt == 0 ? fmaxf(r.x, r.y) : fmaxf(r.z, r.w);
+      else mp = fmaxf(fmaxf(r.x, r.y), fmaxf(r.z, r.w));
+      const int64_t t = t0 + tt;
+      if (valid && t < T) {
+        const float inv_pre = exp2i(-((TOK > 1 && tt) ? pe[TOK - 1] : pe[0]));
+        // code = clamp(rint(y * cq), -8, 7) with cq = 7 / (alpha m) (on the prescaled values, exactly
+        // (7 / (alpha m)) / 2^pe).  The clamp rides on the FMA pipe: u = sat((y cq + 8) / 15) in [0, 1],
+        // then fma(u, 15, MAGIC - 8) rounds u*15 - 8 half-to-even into the low mantissa bits; the
+        // extra rounding of u moves y*cq by < 1e-5 code units (well inside the near-tie window).
+        const float c15 = mp > 0.f ? (7.0f / (alpha * mp)) * (1.0f / 15.0f) : 0.f;
+        constexpr float B15 = 8.0f / 15.0f;
+        uint32_t w[N2 / 8];
+#pragma unroll
+        for (int c8 = 0; c8 < N2 / 8; ++c8) {
+          float z[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            z[e] = fmaf(fma_sat(__uint_as_float(yv[8 * c8 + e]), c15, B15), 15.0f, MAGIC - 8.0f);
+          w[c8] = pack8(z);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(q + t * QTOK + i * QROW);
+#pragma unroll
+        for (int c = 0; c < N2 / 32; ++c) dst[c] = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+        if (i == 0) scale[t] = mp > 0.f ? alpha * (mp * inv_pre) / 7.0f : 1.0f;
+        if constexpr (WRITE_Y) {
+          float2* yd = reinterpret_cast<float2*>(y_out + t * (N1 * N2) + i * N2);   // y is 8-B aligned (ABI)
+#pragma unroll
+          for (int c = 0; c < N2 / 2; ++c)
+            yd[c] = make_float2(__uint_as_float(yv[2 * c]) * inv_pre, __uint_as_float(yv[2 * c + 1]) * inv_pre);
+        }
+      }
+      if (L == 0 && k < 16) trace(104 + k);
+    }
+  }
+
+  tc::fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    trace(120);
+    cta_stamp(1);
+  }
+  if (threadIdx.x == 4 * 32) trace(121);
+  if (warp == 2) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, C::TMEM_COLS);
+    if (lane == 0) trace(123);
+  }
+}
+
+// ------------------------------------------------------------------------------ host side
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiled encoder() {
+  static EncodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  });
+  return fn;
+}
+
+// 16-bit tensor of `rank` dims (innermost first), SWIZZLE_128B, zero OOB fill
+static bool encode16(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                     const cuuint32_t* box) {
+  EncodeTiled enc = encoder();
+  if (!enc) return false;
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, cuuint32_t(rank), const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int N1, int N2, bool BF16, bool WRITE_Y>
+static cudaError_t launch(const TQArgs& a) {
+  using C = Cfg<N1, N2>;
+  auto kern = tq_tc05_kernel<N1, N2, BF16, WRITE_Y>;
+  static bool attr_set = false;   // benign race: idempotent attribute set
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  CUtensorMap mx, m1, m2;
+  {
+    const cuuint64_t dims[3] = {cuuint64_t(N2), cuuint64_t(N1), cuuint64_t(a.T)};
+    const cuuint64_t strides[2] = {cuuint64_t(N2) * 2, cuuint64_t(a.ldx) * 2};
+    const cuuint32_t box[3] = {64, cuuint32_t(N1), cuuint32_t(C::TOK)};
+    if (!encode16(&mx, a.x, 3, dims, strides, box)) return cudaErrorInvalidValue;
+  }
+  {
+    const cuuint64_t dims[2] = {cuuint64_t(N1), cuuint64_t(N1)};
+    const cuuint64_t strides[1] = {cuuint64_t(N1) * 2};
+    const cuuint32_t box[2] = {64, cuuint32_t(N1)};
+    if (!encode16(&m1, a.p1, 2, dims, strides, box)) return cudaErrorInvalidValue;
+  }
+  {
+    const cuuint64_t dims[2] = {cuuint64_t(N2), cuuint64_t(N2)};
+    const cuuint64_t strides[1] = {cuuint64_t(N2) * 2};
+    const cuuint32_t box[2] = {64, cuuint32_t(N2)};
+    if (!encode16(&m2, a.p2, 2, dims, strides, box)) return cudaErrorInvalidValue;
+  }
+  const int64_t tiles = (a.T + C::TOK - 1) / C::TOK;
+  const int grid = int(std::min<int64_t>(tiles, num_sms()));
+  kern<<<grid, THREADS, C::SMEM, a.stream>>>(mx, m1, m2, a.T, a.alpha, a.q, a.scale, a.y);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int N1, int N2>
+static cudaError_t dispatch(const TQArgs& a) {
+  if (a.bf16) return a.y ? launch<N1, N2, true, true>(a) : launch<N1, N2, true, false>(a);
+  return a.y ? launch<N1, N2, false, true>(a) : launch<N1, N2, false, false>(a);
+}
+
+}  // namespace tq5
+
+#ifdef FQ_TRACE
+extern "C" int fq_debug_trace_tq(unsigned long long* out, int n) {
+  if (n > tq5::TRACE_CTAS * tq5::TRACE_EV) n = tq5::TRACE_CTAS * tq5::TRACE_EV;
+  return int(cudaMemcpyFromSymbol(out, tq5::g_trace, sizeof(unsigned long long) * n));
+}
+extern "C" int fq_debug_cta_tq(unsigned long long* out) {   // [1024][start, end]
+  return int(cudaMemcpyFromSymbol(out, tq5::g_cta, sizeof(unsigned long long) * 2048));
+}
+extern "C" int fq_debug_stamp(int slot, void* stream) {     // globaltimer into stamp slot (0..7)
+  tq5::stamp_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(slot);
+  return int(cudaGetLastError());
+}
+extern "C" int fq_debug_stamps(unsigned long long* out) {
+  return int(cudaMemcpyFromSymbol(out, tq5::g_stamp, sizeof(unsigned long long) * 8));
+}
+#endif
+
+bool tq_tc05_supported(const TQArgs& a) {
+  const bool shape = (a.n1 == 64 && (a.n2 == 64 || a.n2 == 128)) ||
+                     (a.n2 == 128 && (a.n1 == 80 || a.n1 == 96 || a.n1 == 112 || a.n1 == 128));
+  const bool al = ((reinterpret_cast<uintptr_t>(a.x) | reinterpret_cast<uintptr_t>(a.p1) |
+                    reinterpret_cast<uintptr_t>(a.p2) | reinterpret_cast<uintptr_t>(a.q)) & 15u) == 0 &&
+                  (a.ldx * 2) % 16 == 0 && a.T < (int64_t(1) << 31);
+  return shape && al && tq5::encoder() != nullptr;
+}
+
+cudaError_t tq_tc05_launch(const TQArgs& a) {
+  using namespace tq5;
+  if (a.n1 == 64 && a.n2 == 64) return dispatch<64, 64>(a);
+  if (a.n1 == 64 && a.n2 == 128) return dispatch<64, 128>(a);
+  if (a.n1 == 80 && a.n2 == 128) return dispatch<80, 128>(a);
+  if (a.n1 == 96 && a.n2 == 128) return dispatch<96, 128>(a);
+  if (a.n1 == 112 && a.n2 == 128) return dispatch<112, 128>(a);
+  if (a.n1 == 128 && a.n2 == 128) return dispatch<128, 128>(a);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace fq

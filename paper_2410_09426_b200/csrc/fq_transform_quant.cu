@@ -340,16 +340,35 @@ bool tq_simt_supported(int n1, int n2) {
   return size_t(2) * n1 * n2 * sizeof(float) <= 200 * 1024;
 }
 
-cudaError_t transform_quant_launch(const TQArgs& a) {
-  // tensor-core instantiations for the shapes of the configs; everything else -> CUDA cores
-  if (!a.force_simt) {
-    if (a.n1 == 16 && a.n2 == 32) return dispatch_mma<16, 32, 8, 2>(a);
-    if (a.n1 == 64 && a.n2 == 64) return dispatch_mma<64, 64, 2, 2>(a);
-    if (a.n1 == 64 && a.n2 == 128) return dispatch_mma<64, 128, 2, 2>(a);
-    if (a.n1 == 112 && a.n2 == 128) return dispatch_mma<112, 128, 1, 2>(a);
-    if (a.n1 == 128 && a.n2 == 224) return dispatch_mma<128, 224, 1, 1>(a);
-  }
+bool tq_mma_supported(int n1, int n2) {
+  return (n1 == 16 && n2 == 32) || (n1 == 64 && n2 == 64) || (n1 == 64 && n2 == 128) ||
+         (n1 == 112 && n2 == 128) || (n1 == 128 && n2 == 224);
+}
+
+cudaError_t tq_mma_launch(const TQArgs& a) {
+  if (a.n1 == 16 && a.n2 == 32) return dispatch_mma<16, 32, 8, 2>(a);
+  if (a.n1 == 64 && a.n2 == 64) return dispatch_mma<64, 64, 2, 2>(a);
+  if (a.n1 == 64 && a.n2 == 128) return dispatch_mma<64, 128, 2, 2>(a);
+  if (a.n1 == 112 && a.n2 == 128) return dispatch_mma<112, 128, 1, 2>(a);
+  if (a.n1 == 128 && a.n2 == 224) return dispatch_mma<128, 224, 1, 1>(a);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t tq_simt_launch(const TQArgs& a) {
   return a.bf16 ? launch_simt<__nv_bfloat16>(a) : launch_simt<__half>(a);
+}
+
+// impl 0: tcgen05 kernel where supported; tiny tiles (n <= 4096, e.g. 16 x 32) on CUDA cores in
+//         fp32 (the north_star's "warp-level FMAs where n1 and n2 are tiny": no fp16 intermediate,
+//         so no tie flips); the mma.sync kernel for the remaining instantiated shapes (128 x 224).
+// impl 1: mma.sync where instantiated, else CUDA cores;  impl 2: CUDA cores.
+cudaError_t transform_quant_launch(const TQArgs& a) {
+  const int impl = tq_impl();
+  const bool tc_shape = (a.n1 % 16 == 0) && (a.n2 % 16 == 0);
+  if (impl == 0 && tq_tc05_supported(a)) return tq_tc05_launch(a);
+  if (impl == 0 && int64_t(a.n1) * a.n2 <= 4096 && tq_simt_supported(a.n1, a.n2)) return tq_simt_launch(a);
+  if (impl <= 1 && tc_shape && tq_mma_supported(a.n1, a.n2)) return tq_mma_launch(a);
+  return tq_simt_launch(a);
 }
 
 }  // namespace fq

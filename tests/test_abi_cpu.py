@@ -106,6 +106,13 @@ def test_gemm_impl_selector_validation():
         fq.fq_set_gemm_impl(-1)
 
 
+def test_tq_impl_selector_validation():
+    lib = fq.load()
+    assert lib.fq_set_tq_impl(3) == _lib.FQ_EINVAL and lib.fq_set_tq_impl(-1) == _lib.FQ_EINVAL
+    for impl in (2, 1, 0):
+        assert lib.fq_set_tq_impl(impl) == _lib.FQ_OK
+
+
 def test_product_path_does_not_import_the_oracle():
     pkg = os.path.join(ROOT, "paper_2410_09426_b200")
     for dp, _, files in os.walk(pkg):

@@ -46,15 +46,25 @@ def run_tq(x, p1, p2, alpha, n1, n2):
     return np_of(q), np_of(s), np_of(y)
 
 
-SHAPES = [(16, 32), (64, 64), (64, 128), (112, 128), (128, 224),    # tensor-core instantiations
-          (8, 8), (6, 10), (16, 48), (32, 32), (2, 3 * 2)]          # CUDA-core kernel
+SHAPES = [(64, 64), (64, 128), (80, 128), (96, 128), (112, 128), (128, 128),   # tcgen05 kernel
+          (16, 32), (128, 224),                                                   # mma.sync kernel
+          (8, 8), (6, 10), (16, 48), (32, 32), (2, 3 * 2)]                        # CUDA-core kernel
+
+
+@pytest.fixture(params=[0, 1, 2], ids=["tq_default", "tq_mma_sync", "tq_simt"])
+def tq_impl(request):
+    fq.fq_set_tq_impl(request.param)
+    yield request.param
+    fq.fq_set_tq_impl(0)
 
 
 @pytest.mark.parametrize("n1,n2", SHAPES)
 @pytest.mark.parametrize("alpha", [1.0, 0.9])
 @pytest.mark.parametrize("tdtype", [torch.float16, torch.bfloat16])
-def test_transform_quant_vs_oracle(n1, n2, alpha, tdtype):
-    T = 300 if n1 * n2 <= 16384 else 137                  # several teams/CTAs and a ragged tail
+def test_transform_quant_vs_oracle(n1, n2, alpha, tdtype, tq_impl):
+    if tq_impl == 2 and n1 * n2 > 16384:
+        pytest.skip("CUDA-core kernel: smem bound")
+    T = 300 if n1 * n2 <= 16384 else 137                  # several tiles/CTAs and a ragged tail
     x, p1, p2 = make_inputs(T, n1, n2, seed=n1 + n2, tdtype=tdtype)
     q, s, y = run_tq(x, p1, p2, alpha, n1, n2)
     qo, so, yo = O.transform_quant(x.float().numpy(), p1.float().numpy(), p2.float().numpy(), alpha)
@@ -89,6 +99,21 @@ def test_transform_special_matrices(n1, n2):
     q, s, y = run_tq(x, p1, p2, 1.0, n1, n2)
     perm = np.kron(p1.float().numpy(), p2.float().numpy()).argmax(axis=0)
     assert np.array_equal(y, x.float().numpy()[:, perm])
+
+
+@pytest.mark.parametrize("n1,n2", [(64, 64), (64, 128), (112, 128)])
+@pytest.mark.parametrize("T", [1, 2, 3, 5, 149, 295, 297, 1031])
+def test_transform_tile_tails(n1, n2, T):
+    """Token counts around the tile size (2 tokens for n1 = 64) and the grid size (148 SMs):
+    the TMA zero-fills tokens past T and the kernel must not write them."""
+    x, p1, p2 = make_inputs(T, n1, n2, seed=T)
+    q = torch.full((T + 2, n1 * n2 // 2), 0xAB, dtype=torch.uint8, device=DEV)
+    s = torch.full((T + 2,), -1.0, dtype=torch.float32, device=DEV)
+    fq.fq_transform_quant(x.to(DEV), n1, n2, p1.to(DEV), p2.to(DEV), 0.9, q[:T], s[:T])
+    torch.cuda.synchronize()
+    assert np.all(np_of(q[T:]) == 0xAB) and np.all(np_of(s[T:]) == -1.0)     # nothing past T
+    qo, so, yo = O.transform_quant(x.float().numpy(), p1.float().numpy(), p2.float().numpy(), 0.9)
+    parity.check_transform(np_of(q[:T]), np_of(s[:T]), None, yo, qo, so, label=f"tail T={T}")
 
 
 def test_transform_overflow_stress_fp16():
