@@ -9,10 +9,16 @@
 // registers with tcgen05.st) and HALF of the 192 weight rows (96) as the B operand in shared
 // memory; the leader CTA issues one M=256 N=192 K=32 MMA for both.  Per SM this halves the
 // shared-memory and L1 traffic per MAC relative to a single-CTA tile.
-//   warps 0-3 : epilogue (own TMEM lanes -> dequant -> global)
-//   warp  4   : TMEM allocator (both CTAs) + MMA issuer (leader CTA only)
-//   warps 5-8 : A converters, one activation row per thread (256-bit loads)
-//   warps 9-12: B converters, 4 threads per weight row (coalesced), SWIZZLE_128B K-major
+//   warps 0-3  : epilogue (own TMEM lanes -> dequant -> swizzled smem -> TMA bulk store)
+//   warp  4    : TMEM allocator (both CTAs) + MMA issuer (leader CTA only)
+//   warps 5-12 : A converters, half an activation row per thread (256-bit loads, PF K-blocks of
+//                register prefetch)
+//   warps 13-18: B converters, 4 threads per weight row: packed rows from the TMA ring ->
+//                widened SWIZZLE_128B K-major operand
+//   warp  19   : TMA producer of the packed weight ring (BSTAGES deep, no registers involved)
+// The B path is fully asynchronous (the ring is 8 K-blocks deep); the A path keeps zero shared-
+// memory traffic (registers -> TMEM), which leaves the SM's shared-memory bandwidth to the
+// widened B operand (12 KB written + 12 KB read by the MMA per K-block) and its packed ring.
 // Synchronisation: converters of both CTAs arrive (release.cluster) on the leader's `full`
 // barrier; the leader's tcgen05.commit multicasts to both CTAs' `empty` / `tfull` barriers;
 // both CTAs' epilogues arrive on the leader's `tempty` barrier.
@@ -44,7 +50,10 @@ constexpr int BN = 192, BN_CTA = 96;      // features per pair tile / B rows per
 constexpr int BK = 128;                   // int8 K per stage
 constexpr int UK = 32;
 constexpr int STAGES = 4;
-constexpr int B_BYTES = BN_CTA * BK;      // 12 KB per stage per CTA
+constexpr int BSTAGES = 8;                // packed B ring (TMA)
+constexpr int B_BYTES = BN_CTA * BK;      // 12 KB per stage per CTA (widened)
+constexpr int BP_BYTES = BN_CTA * BK / 2; // 6 KB per packed B stage
+constexpr int EPI_BYTES = 32 * 128;       // per epilogue warp: 32 rows x 64 fp16 columns (SW128)
 constexpr int A_COLS = BK / 4;            // TMEM columns per A stage
 constexpr int TMEM_ACC0 = 0;              // two accumulators [0, 2*BN)
 constexpr int TMEM_A0 = 2 * BN;           // A stages [2*BN, 2*BN + STAGES*A_COLS) = [384, 512)
@@ -53,13 +62,15 @@ constexpr int NUM_EPI_WARPS = 4, MMA_WARP = 4;
 constexpr int A_WARP0 = 5, NUM_A_WARPS = 8;     // 2 warps per TMEM lane quarter (each half of K)
 constexpr int B_WARP0 = 13, NUM_B_WARPS = 6;
 constexpr int NUM_CONV_WARPS = NUM_A_WARPS + NUM_B_WARPS;
-constexpr int THREADS = (B_WARP0 + NUM_B_WARPS) * 32;
+constexpr int TMA_WARP = B_WARP0 + NUM_B_WARPS;
+constexpr int THREADS = (TMA_WARP + 1) * 32;
 constexpr int B_TASKS = BN_CTA * 4 / (NUM_B_WARPS * 32);    // 16-byte packed chunks per B thread
 #ifndef FQ_GEMM_PF
 #define FQ_GEMM_PF 6
 #endif
 constexpr int PF = FQ_GEMM_PF;                              // K-blocks of register prefetch
-constexpr size_t SMEM_BYTES = size_t(STAGES) * B_BYTES + 1024 + 256;
+constexpr size_t SMEM_BYTES =
+    size_t(STAGES) * B_BYTES + size_t(BSTAGES) * BP_BYTES + NUM_EPI_WARPS * EPI_BYTES + 1024 + 512;
 constexpr uint32_t IDESC = tc::idesc_i8(BM, BN);
 static_assert(TMEM_A0 + STAGES * A_COLS <= TMEM_COLS, "TMEM budget");
 static_assert(B_TASKS * NUM_B_WARPS * 32 == BN_CTA * 4, "B task split");
@@ -108,17 +119,21 @@ struct Cursor {
 
 template <bool OUT_I32, bool BF16>
 __global__ void __launch_bounds__(THREADS, 1)
-gemm_pair_kernel(const uint8_t* __restrict__ qa, const float* __restrict__ sa, int T, int K,
-                 const uint8_t* __restrict__ qw, const float* __restrict__ sw, int N,
-                 void* __restrict__ yv) {
+gemm_pair_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmY,
+                 const uint8_t* __restrict__ qa, const float* __restrict__ sa, int T, int K,
+                 const float* __restrict__ sw, int N, void* __restrict__ yv) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(STAGES) * B_BYTES);
+  uint8_t* sBp = smem + size_t(STAGES) * B_BYTES;                 // packed B ring
+  uint8_t* sEpi = sBp + size_t(BSTAGES) * BP_BYTES;                // epilogue staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + NUM_EPI_WARPS * EPI_BYTES);
   uint64_t* full = bars;                 // [STAGES] leader: converters of both CTAs -> MMA
   uint64_t* empty = bars + STAGES;       // [STAGES] each CTA: MMA commit -> converters
   uint64_t* tfull = bars + 2 * STAGES;   // [2]      each CTA: MMA commit -> epilogue
   uint64_t* tempty = tfull + 2;          // [2]      leader: epilogues of both CTAs -> MMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bfull = tempty + 2;          // [BSTAGES] each CTA: TMA -> B converters
+  uint64_t* bempty = bfull + BSTAGES;    // [BSTAGES] each CTA: B converters -> TMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + BSTAGES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) trace(250);
@@ -135,14 +150,20 @@ gemm_pair_kernel(const uint8_t* __restrict__ qa, const float* __restrict__ sa, i
   if (warp == MMA_WARP) {
     if (lane == 0) {
       for (int s = 0; s < STAGES; ++s) {
-        tc::mbar_init(&full[s], 2);                 // one arrival per CTA of the pair
+        tc::mbar_init(&full[s], 2 * NUM_CONV_WARPS);  // one arrival per converter warp of the pair
         tc::mbar_init(&empty[s], 1);
       }
       for (int b = 0; b < 2; ++b) {
         tc::mbar_init(&tfull[b], 1);
         tc::mbar_init(&tempty[b], 2);
       }
+      for (int s = 0; s < BSTAGES; ++s) {
+        tc::mbar_init(&bfull[s], 1);
+        tc::mbar_init(&bempty[s], NUM_B_WARPS);
+      }
       tc::fence_barrier_init();
+      if constexpr (!OUT_I32) tc::tma_prefetch_desc(&tmY);
+      tc::tma_prefetch_desc(&tmB);
     }
     __syncwarp();
     tc::tmem_alloc2(tmem_slot, TMEM_COLS);
@@ -153,21 +174,37 @@ gemm_pair_kernel(const uint8_t* __restrict__ qa, const float* __restrict__ sa, i
   tc::fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // All converter warps of this CTA finish a stage, then ONE thread signals the leader's
-  // `full` barrier: a CTA-scope arrive in the leader, a single release.cluster remote arrive in
-  // the peer (one cluster-scope fence per stage instead of one per warp).
+  // Every converter warp signals the leader's `full` barrier on its own (CTA-scope arrive in the
+  // leader, release.cluster remote arrive from the peer), so the A and B paths and the warps of
+  // each path run decoupled, up to STAGES K-blocks apart; no CTA-wide barrier per stage.
   int jtrace = 0;
   auto signal_full = [&](uint64_t* bar) {
-    named_bar_sync(1, NUM_CONV_WARPS * 32);
-    if (threadIdx.x == A_WARP0 * 32) {
+    __syncwarp();
+    if (lane == 0) {
       if (rank == 0) tc::mbar_arrive(bar);
       else tc::mbar_arrive_cluster(bar, 0);
+    }
+    if (threadIdx.x == A_WARP0 * 32) {
       if (jtrace < 64) trace(jtrace);
       ++jtrace;
     }
   };
 
-  if (warp >= A_WARP0) {
+  if (warp == TMA_WARP) {
+    // ================================ TMA producer (packed weight ring) ================================
+    if (lane == 0) {
+      Cursor ld;
+      ld.init(sc);
+      for (int j = 0; ld.valid; ++j, ld.next(sc)) {
+        const int sp = j % BSTAGES;
+        tc::mbar_wait(&bempty[sp], ((j / BSTAGES) & 1) ^ 1);
+        tc::mbar_expect_tx(&bfull[sp], BP_BYTES);
+        tc::tma_load_2d(sBp + size_t(sp) * BP_BYTES, &tmB, &bfull[sp], ld.kb * (BK / 2),
+                        ld.nb * BN + int(rank) * BN_CTA);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= A_WARP0) {
     // ================================ converters ================================
     // Each thread keeps PF K-blocks of its packed data in flight in a statically indexed
     // register ring (the loop below is unrolled PF times, so slot indices are constants).
@@ -228,53 +265,39 @@ gemm_pair_kernel(const uint8_t* __restrict__ qa, const float* __restrict__ sa, i
         }
       }
     } else {
+      // packed rows land in the ring by TMA (warp TMA_WARP); 4 threads per weight row
       const int ct = threadIdx.x - B_WARP0 * 32;
       int bjob = 0;
-      uint4 ring[PF][B_TASKS];
-      auto load = [&](uint4 (&r)[B_TASKS]) {
+      while (cv.valid) {
+        const int sp = bjob % BSTAGES;
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        tc::mbar_wait(&bfull[sp], (bjob / BSTAGES) & 1);
+        const bool trB = threadIdx.x == B_WARP0 * 32 && bjob >= 16 && bjob < 28;
+        if (trB) trace(208 + (bjob - 16) * 3 + 0);
+        const uint32_t src = smem_u32(sBp + size_t(sp) * BP_BYTES);
+        const uint32_t dst = smem_u32(smem + size_t(stage) * B_BYTES);
 #pragma unroll
         for (int i = 0; i < B_TASKS; ++i) {
           const int task = ct + i * NUM_B_WARPS * 32, rl = task >> 2, c = task & 3;
-          const int row = ld.nb * BN + int(rank) * BN_CTA + rl, kbyte = ld.kb * (BK / 2) + c * 16;
-          r[i] = (ld.valid && row < N && kbyte < KB)
-                     ? __ldg(reinterpret_cast<const uint4*>(qw + size_t(row) * KB + kbyte))
-                     : make_uint4(0, 0, 0, 0);
+          const uint4 pk = tc::lds128(src + uint32_t(task * 16));      // row rl, bytes [16c, 16c+16)
+          uint32_t o[8];
+          widen8(pk.x, o[0], o[1]);
+          widen8(pk.y, o[2], o[3]);
+          widen8(pk.z, o[4], o[5]);
+          widen8(pk.w, o[6], o[7]);
+          const uint32_t rowp = dst + uint32_t(rl * 128);
+          tc::sts128(rowp + uint32_t(((2 * c) ^ (rl & 7)) << 4), o[0], o[1], o[2], o[3]);
+          tc::sts128(rowp + uint32_t(((2 * c + 1) ^ (rl & 7)) << 4), o[4], o[5], o[6], o[7]);
         }
-        ld.next(sc);
-      };
-#pragma unroll
-      for (int u = 0; u < PF; ++u) load(ring[u]);
-      while (cv.valid) {
-#pragma unroll
-        for (int u = 0; u < PF; ++u) {
-          if (!cv.valid) break;
-          tc::mbar_wait(&empty[stage], phase ^ 1);
-          const bool trB = threadIdx.x == B_WARP0 * 32 && bjob >= 16 && bjob < 28;
-          if (trB) trace(208 + (bjob - 16) * 3 + 0);
-          const uint32_t sB = smem_u32(smem + size_t(stage) * B_BYTES);
-#pragma unroll
-          for (int i = 0; i < B_TASKS; ++i) {
-            const int task = ct + i * NUM_B_WARPS * 32, rl = task >> 2, c = task & 3;
-            uint32_t o[8];
-            widen8(ring[u][i].x, o[0], o[1]);
-            widen8(ring[u][i].y, o[2], o[3]);
-            widen8(ring[u][i].z, o[4], o[5]);
-            widen8(ring[u][i].w, o[6], o[7]);
-            const uint32_t rowp = sB + uint32_t(rl * 128);
-            tc::sts128(rowp + uint32_t(((2 * c) ^ (rl & 7)) << 4), o[0], o[1], o[2], o[3]);
-            tc::sts128(rowp + uint32_t(((2 * c + 1) ^ (rl & 7)) << 4), o[4], o[5], o[6], o[7]);
-          }
-          // fence.proxy.async is a CTA membar: it would wait for every load in flight, so the
-          // prefetch for this ring slot is issued only after the stage is signalled
-          if (trB) trace(208 + (bjob - 16) * 3 + 1);
-          tc::fence_proxy_async_smem();
-          if (trB) trace(208 + (bjob - 16) * 3 + 2);
-          signal_full(&full[stage]);
-          ++bjob;
-          load(ring[u]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-          cv.next(sc);
-        }
+        if (trB) trace(208 + (bjob - 16) * 3 + 1);
+        tc::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&bempty[sp]);                  // ring slot consumed
+        if (trB) trace(208 + (bjob - 16) * 3 + 2);
+        signal_full(&full[stage]);
+        ++bjob;
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        cv.next(sc);
       }
     }
   } else if (warp == MMA_WARP) {
@@ -308,7 +331,10 @@ gemm_pair_kernel(const uint8_t* __restrict__ qa, const float* __restrict__ sa, i
     __syncwarp();
   } else {
     // ================================ epilogue ================================
+    // fp16/bf16: each warp dequantizes its 32 rows in 64-column chunks into a SWIZZLE_128B smem
+    // box and TMA-stores it (coalesced; rows >= T and columns >= N are clipped by the TMA unit).
     const int r_local = warp * 32 + lane;
+    const uint32_t stg = smem_u32(sEpi + warp * EPI_BYTES);
     int it = 0;
     for (int tile = sc.cluster; tile < sc.num_tiles; tile += sc.num_clusters, ++it) {
       int mb, nb;
@@ -319,43 +345,72 @@ gemm_pair_kernel(const uint8_t* __restrict__ qa, const float* __restrict__ sa, i
       if (threadIdx.x == 0 && it < 8) trace(136 + it);
       const int row = mb * BM + int(rank) * BM_CTA + r_local;
       const bool row_ok = row < T;
-      const float s_a = (!OUT_I32 && row_ok) ? sa[row] * (1.0f / 256.0f) : 0.f;
+      const uint32_t tacc = tmem_base + (uint32_t(warp * 32) << 16) + uint32_t(TMEM_ACC0 + buf * BN);
+      if constexpr (OUT_I32) {
 #pragma unroll 1
-      for (int cc = 0; cc < BN / 32; ++cc) {
-        uint32_t v[32];
-        tc::tmem_ld32(tmem_base + (uint32_t(warp * 32) << 16) + uint32_t(TMEM_ACC0 + buf * BN + cc * 32), v);
-        tc::tmem_ld_wait();
-        const int col0 = nb * BN + cc * 32;
-        if (row_ok) {
+        for (int cc = 0; cc < BN / 32; ++cc) {
+          uint32_t v[32];
+          tc::tmem_ld32(tacc + uint32_t(cc * 32), v);
+          tc::tmem_ld_wait();
+          const int col0 = nb * BN + cc * 32;
+          if (row_ok) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 8) {
-            const int col = col0 + j;
-            if (col >= N) break;
-            if constexpr (OUT_I32) {
+            for (int j = 0; j < 32; j += 8) {
+              const int col = col0 + j;
+              if (col >= N) break;
               int32_t* dst = static_cast<int32_t*>(yv) + size_t(row) * N + col;
               reinterpret_cast<int4*>(dst)[0] =
                   make_int4(int(v[j]) >> 8, int(v[j + 1]) >> 8, int(v[j + 2]) >> 8, int(v[j + 3]) >> 8);
               reinterpret_cast<int4*>(dst)[1] =
                   make_int4(int(v[j + 4]) >> 8, int(v[j + 5]) >> 8, int(v[j + 6]) >> 8, int(v[j + 7]) >> 8);
-            } else {
-              const float4 w0 = __ldg(reinterpret_cast<const float4*>(sw + col));
-              const float4 w1 = __ldg(reinterpret_cast<const float4*>(sw + col + 4));
-              const float f0 = float(int(v[j + 0])) * s_a * w0.x, f1 = float(int(v[j + 1])) * s_a * w0.y;
-              const float f2 = float(int(v[j + 2])) * s_a * w0.z, f3 = float(int(v[j + 3])) * s_a * w0.w;
-              const float f4 = float(int(v[j + 4])) * s_a * w1.x, f5 = float(int(v[j + 5])) * s_a * w1.y;
-              const float f6 = float(int(v[j + 6])) * s_a * w1.z, f7 = float(int(v[j + 7])) * s_a * w1.w;
-              uint4 o;
-              if constexpr (BF16) {
-                __nv_bfloat162 h0 = __floats2bfloat162_rn(f0, f1), h1 = __floats2bfloat162_rn(f2, f3);
-                __nv_bfloat162 h2 = __floats2bfloat162_rn(f4, f5), h3 = __floats2bfloat162_rn(f6, f7);
-                o = make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
-                               *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
-                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(yv) + size_t(row) * N + col) = o;
-              } else {
-                o = make_uint4(pack_half2(f0, f1), pack_half2(f2, f3), pack_half2(f4, f5), pack_half2(f6, f7));
-                *reinterpret_cast<uint4*>(static_cast<__half*>(yv) + size_t(row) * N + col) = o;
-              }
             }
+          }
+        }
+      } else {
+        const float s_a = row_ok ? sa[row] * (1.0f / 256.0f) : 0.f;
+#pragma unroll 1
+        for (int q = 0; q < BN / 64; ++q) {
+          uint32_t v[64];
+          tc::tmem_ld32(tacc + uint32_t(q * 64), *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+          tc::tmem_ld32(tacc + uint32_t(q * 64 + 32), *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+          if (lane == 0) tc::bulk_wait_read0();          // previous chunk's store has left the buffer
+          __syncwarp();
+          tc::tmem_ld_wait();
+          const int col0 = nb * BN + q * 64;
+#pragma unroll
+          for (int c8 = 0; c8 < 8; ++c8) {
+            const int col = col0 + c8 * 8;
+            float4 w0 = make_float4(0.f, 0.f, 0.f, 0.f), w1 = w0;
+            if (col < N) {                                  // N % 8 == 0: a group is all in or all out
+              w0 = __ldg(reinterpret_cast<const float4*>(sw + col));
+              w1 = __ldg(reinterpret_cast<const float4*>(sw + col + 4));
+            }
+            const uint32_t* vv = &v[c8 * 8];
+            const float f0 = float(int(vv[0])) * s_a * w0.x, f1 = float(int(vv[1])) * s_a * w0.y;
+            const float f2 = float(int(vv[2])) * s_a * w0.z, f3 = float(int(vv[3])) * s_a * w0.w;
+            const float f4 = float(int(vv[4])) * s_a * w1.x, f5 = float(int(vv[5])) * s_a * w1.y;
+            const float f6 = float(int(vv[6])) * s_a * w1.z, f7 = float(int(vv[7])) * s_a * w1.w;
+            uint32_t o[4];
+            if constexpr (BF16) {
+              __nv_bfloat162 h0 = __floats2bfloat162_rn(f0, f1), h1 = __floats2bfloat162_rn(f2, f3);
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(f4, f5), h3 = __floats2bfloat162_rn(f6, f7);
+              o[0] = *reinterpret_cast<uint32_t*>(&h0);
+              o[1] = *reinterpret_cast<uint32_t*>(&h1);
+              o[2] = *reinterpret_cast<uint32_t*>(&h2);
+              o[3] = *reinterpret_cast<uint32_t*>(&h3);
+            } else {
+              o[0] = pack_half2(f0, f1);
+              o[1] = pack_half2(f2, f3);
+              o[2] = pack_half2(f4, f5);
+              o[3] = pack_half2(f6, f7);
+            }
+            tc::sts128(stg + uint32_t(lane * 128 + ((c8 ^ (lane & 7)) << 4)), o[0], o[1], o[2], o[3]);
+          }
+          tc::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tc::tma_store_2d(&tmY, stg, col0, mb * BM + int(rank) * BM_CTA + warp * 32);
+            tc::bulk_commit();
           }
         }
       }
@@ -367,6 +422,7 @@ gemm_pair_kernel(const uint8_t* __restrict__ qa, const float* __restrict__ sa, i
         if (it < 8) trace(144 + it);
       }
     }
+    if (lane == 0) tc::bulk_wait0();
   }
 
   tc::fence_before();
@@ -388,7 +444,7 @@ extern "C" int fq_debug_trace_gemm(unsigned long long* out) {
 #endif
 
 bool gemm_pair_supported(const GemmArgs& a) {
-  return a.K % 32 == 0 && a.K <= 131072 && a.N % 8 == 0 && a.T <= int64_t(1) << 30;
+  return a.K % 32 == 0 && a.K <= 131072 && a.N % 8 == 0 && a.T <= int64_t(1) << 30 && tmap_available();
 }
 
 cudaError_t gemm_pair_launch(const GemmArgs& a) {
@@ -401,6 +457,19 @@ cudaError_t gemm_pair_launch(const GemmArgs& a) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     if (e != cudaSuccess) return e;
     attr_done[which] = true;
+  }
+  CUtensorMap mb{}, my{};
+  {
+    const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.N)};
+    const uint64_t strides[1] = {uint64_t(a.K / 2)};
+    const uint32_t box[2] = {BK / 2, BN_CTA};
+    if (!tmap_encode(&mb, a.qw, 1, 2, dims, strides, box, false)) return cudaErrorInvalidValue;
+  }
+  if (!a.out_i32) {
+    const uint64_t dims[2] = {uint64_t(a.N), uint64_t(a.T)};
+    const uint64_t strides[1] = {uint64_t(a.N) * 2};
+    const uint32_t box[2] = {64, 32};
+    if (!tmap_encode(&my, a.y, 2, 2, dims, strides, box, true)) return cudaErrorInvalidValue;
   }
   const int num_tiles = int((a.T + BM - 1) / BM) * ((a.N + BN - 1) / BN);
   const int clusters = std::max(1, std::min(num_tiles, num_sms() / 2));
@@ -416,7 +485,7 @@ cudaError_t gemm_pair_launch(const GemmArgs& a) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a.qa, a.sa, int(a.T), a.K, a.qw, a.sw, a.N, a.y);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mb, my, a.qa, a.sa, int(a.T), a.K, a.sw, a.N, a.y);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

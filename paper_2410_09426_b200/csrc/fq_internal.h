@@ -2,9 +2,15 @@
 #pragma once
 #include <cstdint>
 #include <algorithm>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace fq {
+
+// TMA tensor maps (fq_tmap.cu).  dims / box innermost first; strides_bytes has rank-1 entries.
+bool tmap_available();
+bool tmap_encode(CUtensorMap* m, const void* base, int elem_bytes, int rank, const uint64_t* dims,
+                 const uint64_t* strides_bytes, const uint32_t* box, bool swizzle128);
 
 struct TQArgs {
   const void* x;

@@ -28,7 +28,6 @@
 //               stage-1 epilogue (prescale, fp16, smem) and stage-2 epilogue (absmax, quantize,
 //               pack, store) of its own tiles; TMEM/smem buffers are indexed by the group.
 #include <cstdint>
-#include <mutex>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include "fq_device.cuh"
@@ -423,34 +422,6 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
 }
 
 // ------------------------------------------------------------------------------ host side
-using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeTiled encoder() {
-  static EncodeTiled fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult qr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
-        qr == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiled>(p);
-  });
-  return fn;
-}
-
-// 16-bit tensor of `rank` dims (innermost first), SWIZZLE_128B, zero OOB fill
-static bool encode16(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
-                     const cuuint32_t* box) {
-  EncodeTiled enc = encoder();
-  if (!enc) return false;
-  const cuuint32_t es[3] = {1, 1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, cuuint32_t(rank), const_cast<void*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 template <int N1, int N2, bool BF16, bool WRITE_Y>
 static cudaError_t launch(const TQArgs& a) {
   using C = Cfg<N1, N2>;
@@ -463,22 +434,22 @@ static cudaError_t launch(const TQArgs& a) {
   }
   CUtensorMap mx, m1, m2;
   {
-    const cuuint64_t dims[3] = {cuuint64_t(N2), cuuint64_t(N1), cuuint64_t(a.T)};
-    const cuuint64_t strides[2] = {cuuint64_t(N2) * 2, cuuint64_t(a.ldx) * 2};
-    const cuuint32_t box[3] = {64, cuuint32_t(N1), cuuint32_t(C::TOK)};
-    if (!encode16(&mx, a.x, 3, dims, strides, box)) return cudaErrorInvalidValue;
+    const uint64_t dims[3] = {uint64_t(N2), uint64_t(N1), uint64_t(a.T)};
+    const uint64_t strides[2] = {uint64_t(N2) * 2, uint64_t(a.ldx) * 2};
+    const uint32_t box[3] = {64, uint32_t(N1), uint32_t(C::TOK)};
+    if (!tmap_encode(&mx, a.x, 2, 3, dims, strides, box, true)) return cudaErrorInvalidValue;
   }
   {
-    const cuuint64_t dims[2] = {cuuint64_t(N1), cuuint64_t(N1)};
-    const cuuint64_t strides[1] = {cuuint64_t(N1) * 2};
-    const cuuint32_t box[2] = {64, cuuint32_t(N1)};
-    if (!encode16(&m1, a.p1, 2, dims, strides, box)) return cudaErrorInvalidValue;
+    const uint64_t dims[2] = {uint64_t(N1), uint64_t(N1)};
+    const uint64_t strides[1] = {uint64_t(N1) * 2};
+    const uint32_t box[2] = {64, uint32_t(N1)};
+    if (!tmap_encode(&m1, a.p1, 2, 2, dims, strides, box, true)) return cudaErrorInvalidValue;
   }
   {
-    const cuuint64_t dims[2] = {cuuint64_t(N2), cuuint64_t(N2)};
-    const cuuint64_t strides[1] = {cuuint64_t(N2) * 2};
-    const cuuint32_t box[2] = {64, cuuint32_t(N2)};
-    if (!encode16(&m2, a.p2, 2, dims, strides, box)) return cudaErrorInvalidValue;
+    const uint64_t dims[2] = {uint64_t(N2), uint64_t(N2)};
+    const uint64_t strides[1] = {uint64_t(N2) * 2};
+    const uint32_t box[2] = {64, uint32_t(N2)};
+    if (!tmap_encode(&m2, a.p2, 2, 2, dims, strides, box, true)) return cudaErrorInvalidValue;
   }
   const int64_t tiles = (a.T + C::TOK - 1) / C::TOK;
   const int grid = int(std::min<int64_t>(tiles, num_sms()));
@@ -518,7 +489,7 @@ bool tq_tc05_supported(const TQArgs& a) {
   const bool al = ((reinterpret_cast<uintptr_t>(a.x) | reinterpret_cast<uintptr_t>(a.p1) |
                     reinterpret_cast<uintptr_t>(a.p2) | reinterpret_cast<uintptr_t>(a.q)) & 15u) == 0 &&
                   (a.ldx * 2) % 16 == 0 && a.T < (int64_t(1) << 31);
-  return shape && al && tq5::encoder() != nullptr;
+  return shape && al && tmap_available();
 }
 
 cudaError_t tq_tc05_launch(const TQArgs& a) {
