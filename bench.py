@@ -230,32 +230,33 @@ def run_ours(args):
     w = 0
     while w < max(args.warmup, 3) or time.time() - t_w < 1.0:      # >= 1 s soak so clocks settle
         flush.zero_()
+        torch.cuda._sleep(400_000)
         step()
         w += 1
         if w % 50 == 0:
             torch.cuda.synchronize()
     barrier()
 
-    # ---- timed region: K steps, L2 flushed before each step (flush itself untimed) ----
+    # ---- timed region: K steps, L2 flushed before each step (flush itself untimed).  A device
+    #      sleep after the flush lets the host enqueue the whole step before the GPU reaches it,
+    #      so neither the step span nor the per-kernel events include host launch overhead.
+    #      Step time = first event -> last event (all 2 x linears kernels and the gaps between).
     per_kernel = [[0.0, 0.0] for _ in range(2 * len(layers))]
     step_ms = []
     launches0 = fq.fq_launch_count()
     clk.mark_start()
-    if True:
-        for _ in range(args.steps):
-            flush.zero_()
-            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                   for _ in range(2 * len(layers))]
-            step(evs)
-            torch.cuda.synchronize()
-            ms = 0.0
-            for k, (a, b) in enumerate(evs):
-                d = a.elapsed_time(b)
-                per_kernel[k][0] += d
-                per_kernel[k][1] += 1
-                ms += d
-            step_ms.append(ms)
-        barrier()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda._sleep(400_000)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(2 * len(layers))]
+        step(evs)
+        torch.cuda.synchronize()
+        for k, (a, b) in enumerate(evs):
+            per_kernel[k][0] += a.elapsed_time(b)
+            per_kernel[k][1] += 1
+        step_ms.append(evs[0][0].elapsed_time(evs[-1][1]))
+    barrier()
     clk.mark_end()
     clk.stop()
     launches = fq.fq_launch_count() - launches0
@@ -300,6 +301,7 @@ def run_ours(args):
         f_ms = []
         for _ in range(max(5, args.steps // 2)):
             flush.zero_()
+            torch.cuda._sleep(400_000)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             for x, w in zip(xs, ws):
@@ -379,7 +381,8 @@ def run_ours(args):
             "tq_roofline": {"bound": "hbm", "kernel": "fq_transform_quant", "achieved": round(tq_gbs, 1),
                             "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(tq_gbs / pk["hbm_gbs"], 4),
                             "tflops": round(t_flops / (tq_ms * 1e-3) / 1e12, 1)},
-            "time_share": {"transform_quant": round(tq_ms / ms_per_step, 4), "gemm": round(gemm_ms / ms_per_step, 4)},
+            "time_share": {"transform_quant": round(tq_ms / ms_per_step, 4), "gemm": round(gemm_ms / ms_per_step, 4),
+                           "launch_gaps": round(max(0.0, 1 - (tq_ms + gemm_ms) / ms_per_step), 4)},
             "kernels": kernels,
             "fp16_baseline": fp16,
             "e2e": e2e,

@@ -11,14 +11,14 @@
 // shared-memory and L1 traffic per MAC relative to a single-CTA tile.
 //   warps 0-3  : epilogue (own TMEM lanes -> dequant -> swizzled smem -> TMA bulk store)
 //   warp  4    : TMEM allocator (both CTAs) + MMA issuer (leader CTA only)
-//   warps 5-12 : A converters, half an activation row per thread (256-bit loads, PF K-blocks of
-//                register prefetch)
+//   warps 5-12 : A converters, half an activation row per thread: packed row from the TMA ring
+//                (SWIZZLE_64B, conflict-free) -> widened in registers -> tcgen05.st into TMEM
 //   warps 13-18: B converters, 4 threads per weight row: packed rows from the TMA ring ->
-//                widened SWIZZLE_128B K-major operand
-//   warp  19   : TMA producer of the packed weight ring (BSTAGES deep, no registers involved)
-// The B path is fully asynchronous (the ring is 8 K-blocks deep); the A path keeps zero shared-
-// memory traffic (registers -> TMEM), which leaves the SM's shared-memory bandwidth to the
-// widened B operand (12 KB written + 12 KB read by the MMA per K-block) and its packed ring.
+//                widened SWIZZLE_128B K-major operand in shared memory
+//   warp  19   : TMA producer of the packed A+B ring (PSTAGES K-blocks deep)
+// Loads are fully asynchronous (TMA, no registers, no LSU queue); per K-block and SM the shared-
+// memory traffic is 14 KB (TMA) + 14 KB (converter reads) + 12 KB (widened B) + 12 KB (MMA read of
+// B), the A operand never touches shared memory after conversion.
 // Synchronisation: converters of both CTAs arrive (release.cluster) on the leader's `full`
 // barrier; the leader's tcgen05.commit multicasts to both CTAs' `empty` / `tfull` barriers;
 // both CTAs' epilogues arrive on the leader's `tempty` barrier.
@@ -50,9 +50,11 @@ constexpr int BN = 192, BN_CTA = 96;      // features per pair tile / B rows per
 constexpr int BK = 128;                   // int8 K per stage
 constexpr int UK = 32;
 constexpr int STAGES = 4;
-constexpr int BSTAGES = 8;                // packed B ring (TMA)
+constexpr int PSTAGES = 8;                // packed A+B ring (TMA)
 constexpr int B_BYTES = BN_CTA * BK;      // 12 KB per stage per CTA (widened)
-constexpr int BP_BYTES = BN_CTA * BK / 2; // 6 KB per packed B stage
+constexpr int BP_BYTES = BN_CTA * BK / 2; // 6 KB packed B per ring stage
+constexpr int AP_BYTES = BM_CTA * BK / 2; // 8 KB packed A per ring stage
+constexpr int P_BYTES = AP_BYTES + BP_BYTES;
 constexpr int EPI_BYTES = 32 * 128;       // per epilogue warp: 32 rows x 64 fp16 columns (SW128)
 constexpr int A_COLS = BK / 4;            // TMEM columns per A stage
 constexpr int TMEM_ACC0 = 0;              // two accumulators [0, 2*BN)
@@ -65,12 +67,8 @@ constexpr int NUM_CONV_WARPS = NUM_A_WARPS + NUM_B_WARPS;
 constexpr int TMA_WARP = B_WARP0 + NUM_B_WARPS;
 constexpr int THREADS = (TMA_WARP + 1) * 32;
 constexpr int B_TASKS = BN_CTA * 4 / (NUM_B_WARPS * 32);    // 16-byte packed chunks per B thread
-#ifndef FQ_GEMM_PF
-#define FQ_GEMM_PF 6
-#endif
-constexpr int PF = FQ_GEMM_PF;                              // K-blocks of register prefetch
 constexpr size_t SMEM_BYTES =
-    size_t(STAGES) * B_BYTES + size_t(BSTAGES) * BP_BYTES + NUM_EPI_WARPS * EPI_BYTES + 1024 + 512;
+    size_t(STAGES) * B_BYTES + size_t(PSTAGES) * P_BYTES + NUM_EPI_WARPS * EPI_BYTES + 1024 + 512;
 constexpr uint32_t IDESC = tc::idesc_i8(BM, BN);
 static_assert(TMEM_A0 + STAGES * A_COLS <= TMEM_COLS, "TMEM budget");
 static_assert(B_TASKS * NUM_B_WARPS * 32 == BN_CTA * 4, "B task split");
@@ -119,21 +117,21 @@ struct Cursor {
 
 template <bool OUT_I32, bool BF16>
 __global__ void __launch_bounds__(THREADS, 1)
-gemm_pair_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmY,
-                 const uint8_t* __restrict__ qa, const float* __restrict__ sa, int T, int K,
+gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmY, const float* __restrict__ sa, int T, int K,
                  const float* __restrict__ sw, int N, void* __restrict__ yv) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sBp = smem + size_t(STAGES) * B_BYTES;                 // packed B ring
-  uint8_t* sEpi = sBp + size_t(BSTAGES) * BP_BYTES;                // epilogue staging
+  uint8_t* sP = smem + size_t(STAGES) * B_BYTES;                  // packed ring: [A 8 KB | B 6 KB]
+  uint8_t* sEpi = sP + size_t(PSTAGES) * P_BYTES;                  // epilogue staging
   uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + NUM_EPI_WARPS * EPI_BYTES);
   uint64_t* full = bars;                 // [STAGES] leader: converters of both CTAs -> MMA
   uint64_t* empty = bars + STAGES;       // [STAGES] each CTA: MMA commit -> converters
   uint64_t* tfull = bars + 2 * STAGES;   // [2]      each CTA: MMA commit -> epilogue
   uint64_t* tempty = tfull + 2;          // [2]      leader: epilogues of both CTAs -> MMA
-  uint64_t* bfull = tempty + 2;          // [BSTAGES] each CTA: TMA -> B converters
-  uint64_t* bempty = bfull + BSTAGES;    // [BSTAGES] each CTA: B converters -> TMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + BSTAGES);
+  uint64_t* pfull = tempty + 2;          // [PSTAGES] each CTA: TMA -> converters
+  uint64_t* pempty = pfull + PSTAGES;    // [PSTAGES] each CTA: converter warps -> TMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty + PSTAGES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) trace(250);
@@ -157,12 +155,13 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant_
         tc::mbar_init(&tfull[b], 1);
         tc::mbar_init(&tempty[b], 2);
       }
-      for (int s = 0; s < BSTAGES; ++s) {
-        tc::mbar_init(&bfull[s], 1);
-        tc::mbar_init(&bempty[s], NUM_B_WARPS);
+      for (int s = 0; s < PSTAGES; ++s) {
+        tc::mbar_init(&pfull[s], 1);
+        tc::mbar_init(&pempty[s], NUM_CONV_WARPS);
       }
       tc::fence_barrier_init();
       if constexpr (!OUT_I32) tc::tma_prefetch_desc(&tmY);
+      tc::tma_prefetch_desc(&tmA);
       tc::tma_prefetch_desc(&tmB);
     }
     __syncwarp();
@@ -191,111 +190,120 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant_
   };
 
   if (warp == TMA_WARP) {
-    // ================================ TMA producer (packed weight ring) ================================
+    // ================================ TMA producer (packed A + B ring) ================================
     if (lane == 0) {
       Cursor ld;
       ld.init(sc);
       for (int j = 0; ld.valid; ++j, ld.next(sc)) {
-        const int sp = j % BSTAGES;
-        tc::mbar_wait(&bempty[sp], ((j / BSTAGES) & 1) ^ 1);
-        tc::mbar_expect_tx(&bfull[sp], BP_BYTES);
-        tc::tma_load_2d(sBp + size_t(sp) * BP_BYTES, &tmB, &bfull[sp], ld.kb * (BK / 2),
-                        ld.nb * BN + int(rank) * BN_CTA);
+        const int sp = j % PSTAGES;
+        tc::mbar_wait(&pempty[sp], ((j / PSTAGES) & 1) ^ 1);
+        tc::mbar_expect_tx(&pfull[sp], P_BYTES);
+        uint8_t* dst = sP + size_t(sp) * P_BYTES;
+        tc::tma_load_2d(dst, &tmA, &pfull[sp], ld.kb * (BK / 2), ld.mb * BM + int(rank) * BM_CTA);
+        tc::tma_load_2d(dst + AP_BYTES, &tmB, &pfull[sp], ld.kb * (BK / 2), ld.nb * BN + int(rank) * BN_CTA);
       }
     }
     __syncwarp();
   } else if (warp >= A_WARP0) {
     // ================================ converters ================================
-    // Each thread keeps PF K-blocks of its packed data in flight in a statically indexed
-    // register ring (the loop below is unrolled PF times, so slot indices are constants).
     const bool is_a = warp < B_WARP0;
     int stage = 0;
     uint32_t phase = 0;
-    Cursor ld, cv;          // load cursor runs PF jobs ahead of the convert cursor
-    ld.init(sc);
+    Cursor cv;
     cv.init(sc);
+    int job = 0;
     if (is_a) {
+      // row r_local of the CTA's 128 activation rows, K-half khalf of the 128-element K-block:
+      // 32 packed bytes = chunks (2 khalf, 2 khalf + 1) of the SWIZZLE_64B row
       const int aw = warp - A_WARP0;
       const int quarter = warp & 3, khalf = aw >> 2;
       const int r_local = quarter * 32 + lane;                   // == TMEM lane of this row
-      const bool wide = (KB % 32) == 0;
       const uint32_t tl = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(TMEM_A0 + khalf * (A_COLS / 2));
-      uint32_t ring[PF][8];
-      auto load = [&](uint32_t (&r)[8]) {
-        const int row = ld.mb * BM + int(rank) * BM_CTA + r_local;
-        const int kbyte = ld.kb * (BK / 2) + khalf * 32;
-        const bool ok = ld.valid && row < T && kbyte < KB;
-        const uint8_t* p = qa + size_t(ok ? row : 0) * KB + (ok ? kbyte : 0);
-        if (!ok) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) r[i] = 0;
-        } else if (wide) {
-          tc::ldg256(p, r);
-        } else {
-          const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(p));
-          const uint4 v1 = (kbyte + 16 < KB) ? __ldg(reinterpret_cast<const uint4*>(p + 16)) : make_uint4(0, 0, 0, 0);
-          r[0] = v0.x; r[1] = v0.y; r[2] = v0.z; r[3] = v0.w;
-          r[4] = v1.x; r[5] = v1.y; r[6] = v1.z; r[7] = v1.w;
-        }
-        ld.next(sc);
+      const uint32_t sw = uint32_t((r_local >> 1) & 3);
+      const uint32_t roff = uint32_t(r_local * 64);
+      // Two K-blocks per iteration: both are converted and their tcgen05.st issued before one
+      // tcgen05.wait::st + signal, which halves the per-K-block synchronisation latency (the
+      // A path is latency-bound, not throughput-bound).
+      auto prep = [&](int jb, int st, uint32_t ph) {
+        const int sp = jb % PSTAGES;
+        tc::mbar_wait(&empty[st], ph ^ 1);
+        tc::mbar_wait(&pfull[sp], (jb / PSTAGES) & 1);
+        const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES) + roff;
+        const uint4 p0 = tc::lds128(src + ((uint32_t(2 * khalf) ^ sw) << 4));
+        const uint4 p1 = tc::lds128(src + ((uint32_t(2 * khalf + 1) ^ sw) << 4));
+        uint32_t w[16];
+        widen8(p0.x, w[0], w[1]);
+        widen8(p0.y, w[2], w[3]);
+        widen8(p0.z, w[4], w[5]);
+        widen8(p0.w, w[6], w[7]);
+        widen8(p1.x, w[8], w[9]);
+        widen8(p1.y, w[10], w[11]);
+        widen8(p1.z, w[12], w[13]);
+        widen8(p1.w, w[14], w[15]);
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&pempty[sp]);               // packed A consumed (registers)
+        tmem_st16(tl + uint32_t(st * A_COLS), w);
       };
-#pragma unroll
-      for (int u = 0; u < PF; ++u) load(ring[u]);
       while (cv.valid) {
-#pragma unroll
-        for (int u = 0; u < PF; ++u) {
-          if (!cv.valid) break;
-          tc::mbar_wait(&empty[stage], phase ^ 1);
-          const int jt = jtrace;
-          const bool trA = threadIdx.x == A_WARP0 * 32 && jt >= 16 && jt < 28;
-          if (trA) trace(160 + (jt - 16) * 4 + 0);
-          uint32_t w[16];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) widen8(ring[u][i], w[2 * i], w[2 * i + 1]);
-          tmem_st16(tl + uint32_t(stage * A_COLS), w);
-          if (trA) trace(160 + (jt - 16) * 4 + 1);
-          tc::tmem_st_wait();
-          tc::fence_before();
-          if (trA) trace(160 + (jt - 16) * 4 + 2);
-          signal_full(&full[stage]);
-          if (trA) trace(160 + (jt - 16) * 4 + 3);
-          load(ring[u]);            // refill this slot PF jobs ahead (after the barrier: nothing waits on it)
+        const int jt = jtrace;
+        const bool trA = threadIdx.x == A_WARP0 * 32 && jt >= 16 && jt < 26;
+        if (trA) trace(160 + (jt - 16) * 5 + 0);
+        const int st0 = stage;
+        prep(job, stage, phase);
+        ++job;
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        cv.next(sc);
+        const bool two = cv.valid;
+        const int st1 = stage;
+        if (two) {
+          prep(job, stage, phase);
+          ++job;
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           cv.next(sc);
         }
+        if (trA) trace(160 + (jt - 16) * 5 + 2);
+        tc::tmem_st_wait();
+        tc::fence_before();
+        if (trA) trace(160 + (jt - 16) * 5 + 3);
+        signal_full(&full[st0]);
+        if (two) signal_full(&full[st1]);
+        if (trA) trace(160 + (jt - 16) * 5 + 4);
       }
     } else {
-      // packed rows land in the ring by TMA (warp TMA_WARP); 4 threads per weight row
+      // 4 threads per weight row (16 packed bytes each) -> widened SWIZZLE_128B K-major rows
       const int ct = threadIdx.x - B_WARP0 * 32;
-      int bjob = 0;
       while (cv.valid) {
-        const int sp = bjob % BSTAGES;
+        const int sp = job % PSTAGES;
         tc::mbar_wait(&empty[stage], phase ^ 1);
-        tc::mbar_wait(&bfull[sp], (bjob / BSTAGES) & 1);
-        const bool trB = threadIdx.x == B_WARP0 * 32 && bjob >= 16 && bjob < 28;
-        if (trB) trace(208 + (bjob - 16) * 3 + 0);
-        const uint32_t src = smem_u32(sBp + size_t(sp) * BP_BYTES);
+        tc::mbar_wait(&pfull[sp], (job / PSTAGES) & 1);
+        const bool trB = threadIdx.x == B_WARP0 * 32 && job >= 16 && job < 26;
+        if (trB) trace(210 + (job - 16) * 3 + 0);
+        const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES + AP_BYTES);
         const uint32_t dst = smem_u32(smem + size_t(stage) * B_BYTES);
+        uint32_t o[B_TASKS][8];
+#pragma unroll
+        for (int i = 0; i < B_TASKS; ++i) {
+          const int task = ct + i * NUM_B_WARPS * 32;
+          const uint4 pk = tc::lds128(src + uint32_t(task * 16));      // row task/4, bytes [16c, 16c+16)
+          widen8(pk.x, o[i][0], o[i][1]);
+          widen8(pk.y, o[i][2], o[i][3]);
+          widen8(pk.z, o[i][4], o[i][5]);
+          widen8(pk.w, o[i][6], o[i][7]);
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&pempty[sp]);               // packed B consumed (registers)
 #pragma unroll
         for (int i = 0; i < B_TASKS; ++i) {
           const int task = ct + i * NUM_B_WARPS * 32, rl = task >> 2, c = task & 3;
-          const uint4 pk = tc::lds128(src + uint32_t(task * 16));      // row rl, bytes [16c, 16c+16)
-          uint32_t o[8];
-          widen8(pk.x, o[0], o[1]);
-          widen8(pk.y, o[2], o[3]);
-          widen8(pk.z, o[4], o[5]);
-          widen8(pk.w, o[6], o[7]);
           const uint32_t rowp = dst + uint32_t(rl * 128);
-          tc::sts128(rowp + uint32_t(((2 * c) ^ (rl & 7)) << 4), o[0], o[1], o[2], o[3]);
-          tc::sts128(rowp + uint32_t(((2 * c + 1) ^ (rl & 7)) << 4), o[4], o[5], o[6], o[7]);
+          tc::sts128(rowp + uint32_t(((2 * c) ^ (rl & 7)) << 4), o[i][0], o[i][1], o[i][2], o[i][3]);
+          tc::sts128(rowp + uint32_t(((2 * c + 1) ^ (rl & 7)) << 4), o[i][4], o[i][5], o[i][6], o[i][7]);
         }
-        if (trB) trace(208 + (bjob - 16) * 3 + 1);
+        if (trB) trace(210 + (job - 16) * 3 + 1);
         tc::fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&bempty[sp]);                  // ring slot consumed
-        if (trB) trace(208 + (bjob - 16) * 3 + 2);
+        if (trB) trace(210 + (job - 16) * 3 + 2);
         signal_full(&full[stage]);
-        ++bjob;
+        ++job;
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
         cv.next(sc);
       }
@@ -458,18 +466,24 @@ cudaError_t gemm_pair_launch(const GemmArgs& a) {
     if (e != cudaSuccess) return e;
     attr_done[which] = true;
   }
-  CUtensorMap mb{}, my{};
+  CUtensorMap ma{}, mb{}, my{};
+  {
+    const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.T)};
+    const uint64_t strides[1] = {uint64_t(a.K / 2)};
+    const uint32_t box[2] = {BK / 2, BM_CTA};
+    if (!tmap_encode(&ma, a.qa, 1, 2, dims, strides, box, TMAP_SW64)) return cudaErrorInvalidValue;
+  }
   {
     const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.N)};
     const uint64_t strides[1] = {uint64_t(a.K / 2)};
     const uint32_t box[2] = {BK / 2, BN_CTA};
-    if (!tmap_encode(&mb, a.qw, 1, 2, dims, strides, box, false)) return cudaErrorInvalidValue;
+    if (!tmap_encode(&mb, a.qw, 1, 2, dims, strides, box, TMAP_SW_NONE)) return cudaErrorInvalidValue;
   }
   if (!a.out_i32) {
     const uint64_t dims[2] = {uint64_t(a.N), uint64_t(a.T)};
     const uint64_t strides[1] = {uint64_t(a.N) * 2};
     const uint32_t box[2] = {64, 32};
-    if (!tmap_encode(&my, a.y, 2, 2, dims, strides, box, true)) return cudaErrorInvalidValue;
+    if (!tmap_encode(&my, a.y, 2, 2, dims, strides, box, TMAP_SW128)) return cudaErrorInvalidValue;
   }
   const int num_tiles = int((a.T + BM - 1) / BM) * ((a.N + BN - 1) / BN);
   const int clusters = std::max(1, std::min(num_tiles, num_sms() / 2));
@@ -485,7 +499,7 @@ cudaError_t gemm_pair_launch(const GemmArgs& a) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mb, my, a.qa, a.sa, int(a.T), a.K, a.sw, a.N, a.y);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, my, a.sa, int(a.T), a.K, a.sw, a.N, a.y);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

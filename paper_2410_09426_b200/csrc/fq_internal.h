@@ -9,8 +9,9 @@ namespace fq {
 
 // TMA tensor maps (fq_tmap.cu).  dims / box innermost first; strides_bytes has rank-1 entries.
 bool tmap_available();
+enum TmapSwizzle { TMAP_SW_NONE = 0, TMAP_SW64 = 64, TMAP_SW128 = 128 };
 bool tmap_encode(CUtensorMap* m, const void* base, int elem_bytes, int rank, const uint64_t* dims,
-                 const uint64_t* strides_bytes, const uint32_t* box, bool swizzle128);
+                 const uint64_t* strides_bytes, const uint32_t* box, TmapSwizzle swizzle);
 
 struct TQArgs {
   const void* x;

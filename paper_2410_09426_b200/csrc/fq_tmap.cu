@@ -27,7 +27,7 @@ static EncodeTiled encoder() {
 bool tmap_available() { return encoder() != nullptr; }
 
 bool tmap_encode(CUtensorMap* m, const void* base, int elem_bytes, int rank, const uint64_t* dims,
-                 const uint64_t* strides_bytes, const uint32_t* box, bool swizzle128) {
+                 const uint64_t* strides_bytes, const uint32_t* box, TmapSwizzle swizzle) {
   EncodeTiled enc = encoder();
   if (!enc || rank < 1 || rank > 5) return false;
   const CUtensorMapDataType dt = elem_bytes == 1   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
@@ -42,7 +42,9 @@ bool tmap_encode(CUtensorMap* m, const void* base, int elem_bytes, int rank, con
     if (i + 1 < rank) s[i] = strides_bytes[i];
   }
   return enc(m, dt, cuuint32_t(rank), const_cast<void*>(base), d, s, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             swizzle == TMAP_SW128  ? CU_TENSOR_MAP_SWIZZLE_128B
+             : swizzle == TMAP_SW64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                    : CU_TENSOR_MAP_SWIZZLE_NONE,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

@@ -437,19 +437,19 @@ static cudaError_t launch(const TQArgs& a) {
     const uint64_t dims[3] = {uint64_t(N2), uint64_t(N1), uint64_t(a.T)};
     const uint64_t strides[2] = {uint64_t(N2) * 2, uint64_t(a.ldx) * 2};
     const uint32_t box[3] = {64, uint32_t(N1), uint32_t(C::TOK)};
-    if (!tmap_encode(&mx, a.x, 2, 3, dims, strides, box, true)) return cudaErrorInvalidValue;
+    if (!tmap_encode(&mx, a.x, 2, 3, dims, strides, box, TMAP_SW128)) return cudaErrorInvalidValue;
   }
   {
     const uint64_t dims[2] = {uint64_t(N1), uint64_t(N1)};
     const uint64_t strides[1] = {uint64_t(N1) * 2};
     const uint32_t box[2] = {64, uint32_t(N1)};
-    if (!tmap_encode(&m1, a.p1, 2, 2, dims, strides, box, true)) return cudaErrorInvalidValue;
+    if (!tmap_encode(&m1, a.p1, 2, 2, dims, strides, box, TMAP_SW128)) return cudaErrorInvalidValue;
   }
   {
     const uint64_t dims[2] = {uint64_t(N2), uint64_t(N2)};
     const uint64_t strides[1] = {uint64_t(N2) * 2};
     const uint32_t box[2] = {64, uint32_t(N2)};
-    if (!tmap_encode(&m2, a.p2, 2, 2, dims, strides, box, true)) return cudaErrorInvalidValue;
+    if (!tmap_encode(&m2, a.p2, 2, 2, dims, strides, box, TMAP_SW128)) return cudaErrorInvalidValue;
   }
   const int64_t tiles = (a.T + C::TOK - 1) / C::TOK;
   const int grid = int(std::min<int64_t>(tiles, num_sms()));

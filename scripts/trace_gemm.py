@@ -52,13 +52,13 @@ for cta in range(2):
     print("  epi tfull:   " + " ".join(f"{rel(136 + i):.2f}" for i in range(8) if r[136 + i] > 0))
     print("  epi done:    " + " ".join(f"{rel(144 + i):.2f}" for i in range(8) if r[144 + i] > 0))
 r = tr[0]
-print("A thread (CTA0) jobs 16..27: [empty-wait done, STTM issued, st-wait+fence done, barrier+signal done] rel. to job start")
-for j in range(12):
-    v = [r[160 + j * 4 + i] for i in range(4)]
+print("A thread (CTA0): job start -> [empty ok, packed-A ok, STTM+wait done, signalled] (us after start)")
+for j in range(10):
+    v = [r[160 + j * 5 + i] for i in range(5)]
     if v[0] > 0:
         print(f"  job {16 + j}: start {(v[0] - t0) / 1e3:.2f} us  +" + " +".join(f"{(x - v[0]) / 1e3:.3f}" for x in v[1:]))
-print("B thread (CTA0): [empty-wait done, STS done, fence done]")
-for j in range(12):
-    v = [r[208 + j * 3 + i] for i in range(3)]
+print("B thread (CTA0): [waits done, STS done, fence done]")
+for j in range(10):
+    v = [r[210 + j * 3 + i] for i in range(3)]
     if v[0] > 0:
         print(f"  job {16 + j}: start {(v[0] - t0) / 1e3:.2f} us  +" + " +".join(f"{(x - v[0]) / 1e3:.3f}" for x in v[1:]))
