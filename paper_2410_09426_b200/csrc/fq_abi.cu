@@ -2,6 +2,7 @@
 // kernel selection and launch.  No computation happens here; every step runs in the kernels.
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <cuda_runtime.h>
@@ -18,6 +19,14 @@ static std::atomic<int> g_tq_impl{0};
 int tq_impl() { return g_tq_impl.load(); }
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FQ_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 int num_sms() {
   static int cached[64] = {0};

@@ -172,6 +172,8 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   tc::cluster_sync();            // peer barriers initialised before any remote arrive
   tc::fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) tc::griddep_launch();   // the next kernel may start launching (PDL)
+  tc::griddep_wait();                            // qa / sa written by the previous kernel are visible
 
   // Every converter warp signals the leader's `full` barrier on its own (CTA-scope arrive in the
   // leader, release.cluster remote arrive from the peer), so the A and B paths and the warps of
@@ -487,19 +489,8 @@ cudaError_t gemm_pair_launch(const GemmArgs& a) {
   }
   const int num_tiles = int((a.T + BM - 1) / BM) * ((a.N + BN - 1) / BN);
   const int clusters = std::max(1, std::min(num_tiles, num_sms() / 2));
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(unsigned(2 * clusters));
-  cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
-  cfg.stream = a.stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, my, a.sa, int(a.T), a.K, a.sw, a.N, a.y);
+  cudaError_t e = launch_pdl(kern, dim3(unsigned(2 * clusters)), dim3(THREADS), SMEM_BYTES, a.stream, 2, ma, mb, my,
+                             a.sa, int(a.T), a.K, a.sw, a.N, a.y);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

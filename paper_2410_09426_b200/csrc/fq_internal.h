@@ -2,6 +2,7 @@
 #pragma once
 #include <cstdint>
 #include <algorithm>
+#include <utility>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -43,6 +44,37 @@ struct GemmArgs {
 
 int num_sms();
 void count_launch();
+bool pdl_enabled();      // FQ_PDL=0 in the environment disables programmatic dependent launch
+
+// Launch with programmatic stream serialization (PDL: the kernel may start while the previous
+// kernel of the stream finishes; it calls griddepcontrol.wait before touching global inputs) and
+// an optional cluster size.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       int cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (cluster_x > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = unsigned(cluster_x);
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = unsigned(na);
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 cudaError_t transform_quant_launch(const TQArgs& a);   // impl selection (fq_set_tq_impl)
 bool tq_simt_supported(int n1, int n2);

@@ -179,6 +179,13 @@ FQ_DEVICE uint4 lds128(uint32_t addr) {
   return v;
 }
 
+// ---- programmatic dependent launch (PDL) ---------------------------------------------------
+// wait: block until the preceding grid in the stream has completed and its memory is visible (a
+// no-op when the kernel was not launched with programmatic stream serialization); launch:
+// allow the next grid in the stream to start launching (its CTAs still wait in griddep_wait).
+FQ_DEVICE void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+FQ_DEVICE void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // ---- clusters / CTA pairs ---------------------------------------------------------------
 FQ_DEVICE uint32_t cluster_ctarank() {
   uint32_t r;

@@ -65,7 +65,7 @@ FQ_DEVICE void trace(int) {}
 FQ_DEVICE void cta_stamp(int) {}
 #endif
 
-constexpr int THREADS = 12 * 32;
+constexpr int MAX_GROUPS = 4;
 constexpr int SMEM_LIMIT = 232448;       // max dynamic smem per block on sm_100
 constexpr int SMEM_OVERHEAD = 1024 + 512;  // 1024-B alignment slack + barriers/scratch
 
@@ -83,12 +83,16 @@ struct Cfg {
   static constexpr int X_BYTES = TOK * JB * N1 * 128;  // TOK * n * 2
   static constexpr int A2_BYTES = 2 * N2 * 128;        // 2 M-atoms x N2 K-rows x 128 B
   static constexpr int D1C = G1 * N1;                  // TMEM columns of one stage-1 result
-  static constexpr int TMEM_COLS = (2 * D1C + 2 * N2) <= 256 ? 256 : 512;
-  static constexpr int FIXED = P1_BYTES + P2_BYTES + 2 * A2_BYTES;
+  // epilogue groups = tiles in flight (each owns a D1, D2 and A2 slot), as many as TMEM allows
+  static constexpr int GROUPS = (512 / (D1C + N2)) > MAX_GROUPS ? MAX_GROUPS : (512 / (D1C + N2));
+  static constexpr int THREADS = (4 + 4 * GROUPS) * 32;
+  static constexpr int TMEM_USED = GROUPS * (D1C + N2);
+  static constexpr int TMEM_COLS = TMEM_USED <= 256 ? 256 : 512;
+  static constexpr int FIXED = P1_BYTES + P2_BYTES + GROUPS * A2_BYTES;
   static constexpr int STAGES_FIT = (SMEM_LIMIT - SMEM_OVERHEAD - FIXED) / X_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr size_t SMEM = size_t(FIXED) + size_t(STAGES) * X_BYTES + SMEM_OVERHEAD;
-  static_assert(2 * D1C + 2 * N2 <= 512, "TMEM budget");
+  static_assert(TMEM_USED <= 512, "TMEM budget");
   static_assert(STAGES >= 2, "shared-memory budget");
 };
 
@@ -132,6 +136,26 @@ FQ_DEVICE float absmax(const uint32_t* v) {
   return max3f(max3f(a[0], a[1], a[2]), max3f(a[3], a[4], a[5]), fmaxf(a[6], a[7]));
 }
 
+// Walk N TMEM columns of this warp's 32 lanes in chunks of 32 (and a 16-column tail): fn(v, n, col)
+// gets n (32 or 16) fp32 values starting at column col.  Keeps at most 32 values live.
+template <int N, typename F>
+FQ_DEVICE void tmem_chunks(uint32_t taddr, F&& fn) {
+#pragma unroll
+  for (int c = 0; c + 32 <= N; c += 32) {
+    uint32_t v[32];
+    tc::tmem_ld16(taddr + uint32_t(c), *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+    tc::tmem_ld16(taddr + uint32_t(c + 16), *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+    tc::tmem_ld_wait();
+    fn(v, 32, c);
+  }
+  if constexpr (N % 32 == 16) {
+    uint32_t v[32];
+    tc::tmem_ld16(taddr + uint32_t(N - 16), *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+    tc::tmem_ld_wait();
+    fn(v, 16, N - 16);
+  }
+}
+
 // 8 quantized values in MAGIC form (low nibble of the bit pattern = two's-complement code)
 // -> one 32-bit word, element 2m in the low nibble of byte m.
 FQ_DEVICE uint32_t pack8(const float (&v)[8]) {
@@ -143,12 +167,12 @@ FQ_DEVICE uint32_t pack8(const float (&v)[8]) {
 }
 
 template <int N1, int N2, bool BF16, bool WRITE_Y>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(Cfg<N1, N2>::THREADS, 1)
 tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmP1,
                const __grid_constant__ CUtensorMap tmP2, int64_t T, float alpha, uint8_t* __restrict__ q,
                float* __restrict__ scale, float* __restrict__ y_out) {
   using C = Cfg<N1, N2>;
-  constexpr int S = C::STAGES, TOK = C::TOK;
+  constexpr int S = C::STAGES, TOK = C::TOK, G = C::GROUPS, THREADS = C::THREADS;
   constexpr uint32_t IDESC1 = tc::idesc_f16(128, N1, BF16 ? 1 : 0, 1, 1);
   constexpr uint32_t IDESC2 = tc::idesc_f16(128, N2, 0, 1, 1);
 
@@ -157,15 +181,15 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
   uint8_t* sP1 = smem;
   uint8_t* sP2 = sP1 + C::P1_BYTES;
   uint8_t* sA2 = sP2 + C::P2_BYTES;
-  uint8_t* sX = sA2 + 2 * C::A2_BYTES;
+  uint8_t* sX = sA2 + G * C::A2_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sX + size_t(S) * C::X_BYTES);
   uint64_t* xfull = bars;            // [S]  TMA -> MMA
   uint64_t* xempty = bars + S;       // [S]  MMA commit -> TMA
   uint64_t* pfull = bars + 2 * S;    // P1, P2 landed
-  uint64_t* d1full = pfull + 1;      // [2]  MMA commit -> epilogue group
-  uint64_t* a2full = d1full + 2;     // [2]  epilogue group (4 warps) -> MMA
-  uint64_t* d2full = a2full + 2;     // [2]  MMA commit -> epilogue group
-  __shared__ float red[16];                                    // [2 groups][2 parities][4 warps]
+  uint64_t* d1full = pfull + 1;      // [G]  MMA commit -> epilogue group
+  uint64_t* a2full = d1full + G;     // [G]  epilogue group (4 warps) -> MMA
+  uint64_t* d2full = a2full + G;     // [G]  MMA commit -> epilogue group
+  __shared__ float red[MAX_GROUPS * 8];                        // [groups][2 parities][4 warps]
   __shared__ uint32_t tmem_slot[1];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -197,12 +221,14 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
       tc::mbar_init(&xempty[s], 1);
     }
     tc::mbar_init(pfull, 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < G; ++b) {
       tc::mbar_init(&d1full[b], 1);
       tc::mbar_init(&a2full[b], 4);
       tc::mbar_init(&d2full[b], 1);
     }
     tc::fence_barrier_init();
+    tc::griddep_launch();              // the next kernel may start launching (PDL)
+    tc::griddep_wait();                // inputs of this kernel are final (PDL)
     tc::mbar_expect_tx(pfull, C::P1_BYTES + C::P2_BYTES);
     for (int a = 0; a < C::P1_ATOMS; ++a) tc::tma_load_2d(sP1 + a * N1 * 128, &tmP1, pfull, a * 64, 0);
     for (int b = 0; b < C::JB; ++b) tc::tma_load_2d(sP2 + b * N2 * 128, &tmP2, pfull, b * 64, 0);
@@ -237,12 +263,14 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     if (lane == 0)
       for (int k = prefill; k < my_tiles; ++k) issue_x(k);
     __syncwarp();
-  } else if (warp == 1) {
-    // ================================ MMA issuer ================================
+  } else if (warp == 1 || warp == 3) {
+    // ================================ MMA issuers ================================
+    // warp 1 issues stage 1 of every tile, warp 3 stage 2: a stage-1 MMA waiting for its X tile
+    // never holds up a stage-2 MMA that is ready (and vice versa).
     if (lane == 0) {
       const uint32_t p1a = smem_u32(sP1), p2a = smem_u32(sP2);
       auto mma1 = [&](int k) {
-        const int s = k % S, par = k & 1;
+        const int s = k % S, par = k % G;
         tc::mbar_wait(&xfull[s], (k / S) & 1);
         tc::fence_after();
         if (k < 16) trace(24 + k);
@@ -262,24 +290,28 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
         tc::mma_commit(&d1full[par]);
       };
       auto mma2 = [&](int k) {
-        const int par = k & 1;
-        tc::mbar_wait(&a2full[par], (k >> 1) & 1);
+        const int par = k % G;
+        tc::mbar_wait(&a2full[par], (k / G) & 1);
         tc::fence_after();
         if (k < 16) trace(40 + k);
         const uint32_t a0 = smem_u32(sA2 + par * C::A2_BYTES);
-        const uint32_t d = tmem + uint32_t(2 * C::D1C + par * N2);
+        const uint32_t d = tmem + uint32_t(G * C::D1C + par * N2);
 #pragma unroll
         for (int kk = 0; kk < N2 / 16; ++kk)
           tc::mma_ss<false>(d, tc::sdesc_sw128(a0 + kk * 2048, N2 * 128, 1024),
                             tc::sdesc_sw128(p2a + kk * 2048, N2 * 128, 1024), IDESC2, kk > 0);
         tc::mma_commit(&d2full[par]);
       };
-      if (my_tiles > 0) mma1(0);
-      for (int k = 0; k < my_tiles; ++k) {
-        if (k + 1 < my_tiles) mma1(k + 1);
-        mma2(k);
+      if (warp == 1) {
+        // D1 slot k % G is free once the group finished the stage-1 epilogue of tile k - G
+        for (int k = 0; k < my_tiles; ++k) {
+          if (k >= G) tc::mbar_wait(&a2full[k % G], ((k - G) / G) & 1);
+          mma1(k);
+        }
+      } else {
+        for (int k = 0; k < my_tiles; ++k) mma2(k);
+        trace(122);
       }
-      trace(122);
     }
     __syncwarp();
   } else if (warp >= 4) {
@@ -290,7 +322,7 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     float* redg = red + grp * 8;
     int rp = 0;
     auto exchange = [&](float m) {                       // per-warp max -> all 4 warps' maxima
-      m = warp_max(m);
+      m = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(m)));   // m >= 0: uint order
       if (lane == 0) redg[rp * 4 + qd] = m;
       named_bar_sync(1 + grp, 128);
       float r[4];
@@ -301,9 +333,9 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     };
     constexpr int QROW = N2 / 2;                         // packed bytes per row i of a token
     constexpr int QTOK = N1 * N2 / 2;                    // packed bytes per token
-    for (int k = grp; k < my_tiles; k += 2) {
-      const int par = k & 1;
-      const uint32_t ph = (k >> 1) & 1;
+    for (int k = grp; k < my_tiles; k += G) {
+      const int par = grp;                               // == k % G
+      const uint32_t ph = (k / G) & 1;
       const int64_t t0 = int64_t(int(blockIdx.x) + k * int(gridDim.x)) * TOK;
       // -------- stage-1 epilogue: D1 (fp32) -> prescaled fp16 A operand of stage 2 --------
       int pe[TOK];                                       // per-token prescale exponents
@@ -314,14 +346,16 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
   if (L == 0 && k < 8) trace(128 + k * 16 + (sub))
 #pragma unroll
       for (int g = 0; g < C::G1; ++g) {
-        uint32_t v[N1];
+        const uint32_t d1 = lane_base + uint32_t(par * C::D1C + g * N1);
+        // pass 1: max |W| over this lane's row (two-pass keeps <= 32 values in registers)
+        float m1 = 0.f;
+        tmem_chunks<N1>(d1, [&](const uint32_t* v, int n, int) {
 #pragma unroll
-        for (int c = 0; c < N1 / 16; ++c)
-          tc::tmem_ld16(lane_base + uint32_t(par * C::D1C + g * N1 + c * 16),
-                        *reinterpret_cast<uint32_t(*)[16]>(&v[c * 16]));
-        tc::tmem_ld_wait();
+          for (int e = 0; e < 32; e += 2)
+            if (e < n) m1 = max3f(m1, fabsf(__uint_as_float(v[e])), fabsf(__uint_as_float(v[e + 1])));
+        });
         FQ_SUB(1);
-        const float4 r = exchange(absmax<N1>(v));
+        const float4 r = exchange(m1);
         FQ_SUB(2);
         int tt;
         if constexpr (N2 == 64) {                        // tokens = lane halves (quadrants 0-1, 2-3)
@@ -335,15 +369,21 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
         const float pre = exp2i((TOK > 1 && tt) ? pe[TOK - 1] : pe[0]);
         const int j = (N2 == 64) ? (L & 63) : L;         // K row (j') of the stage-2 A operand
         const uint32_t row = smem_u32(sA2) + uint32_t(par * C::A2_BYTES + j * 128);
+        // pass 2: prescale, fp16, swizzled MN-major row j of A2
+        tmem_chunks<N1>(d1, [&](const uint32_t* v, int n, int col) {
 #pragma unroll
-        for (int c8 = 0; c8 < N1 / 8; ++c8) {
-          const int atom = (N1 == 64) ? tt : (c8 >> 3), ch = c8 & 7;
-          tc::sts128(row + uint32_t(atom * (N2 * 128) + ((ch ^ (j & 7)) << 4)),
-                 pack_half2(__uint_as_float(v[8 * c8 + 0]) * pre, __uint_as_float(v[8 * c8 + 1]) * pre),
-                 pack_half2(__uint_as_float(v[8 * c8 + 2]) * pre, __uint_as_float(v[8 * c8 + 3]) * pre),
-                 pack_half2(__uint_as_float(v[8 * c8 + 4]) * pre, __uint_as_float(v[8 * c8 + 5]) * pre),
-                 pack_half2(__uint_as_float(v[8 * c8 + 6]) * pre, __uint_as_float(v[8 * c8 + 7]) * pre));
-        }
+          for (int e = 0; e < 32; e += 8) {
+            if (e < n) {
+              const int c8 = (col + e) >> 3;
+              const int atom = (N1 == 64) ? tt : (c8 >> 3), ch = c8 & 7;
+              tc::sts128(row + uint32_t(atom * (N2 * 128) + ((ch ^ (j & 7)) << 4)),
+                         pack_half2(__uint_as_float(v[e + 0]) * pre, __uint_as_float(v[e + 1]) * pre),
+                         pack_half2(__uint_as_float(v[e + 2]) * pre, __uint_as_float(v[e + 3]) * pre),
+                         pack_half2(__uint_as_float(v[e + 4]) * pre, __uint_as_float(v[e + 5]) * pre),
+                         pack_half2(__uint_as_float(v[e + 6]) * pre, __uint_as_float(v[e + 7]) * pre));
+            }
+          }
+        });
       }
       FQ_SUB(3);
       tc::fence_proxy_async_smem();
@@ -358,51 +398,53 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
       tc::fence_after();
       if (L == 0 && k < 16) trace(88 + k);
       FQ_SUB(8);
-      uint32_t yv[N2];
-#pragma unroll
-      for (int c = 0; c < N2 / 16; ++c)
-        tc::tmem_ld16(lane_base + uint32_t(2 * C::D1C + par * N2 + c * 16),
-                      *reinterpret_cast<uint32_t(*)[16]>(&yv[c * 16]));
-      tc::tmem_ld_wait();
-      FQ_SUB(9);
-      tc::fence_before();
+      const uint32_t d2 = lane_base + uint32_t(G * C::D1C + par * N2);
       const int tt = (N1 == 64) ? (L >> 6) : 0;
       const int i = (N1 == 64) ? (L & 63) : L;
       const bool valid = (N1 == 64) || (L < N1);
-      const float4 r = exchange(valid ? absmax<N2>(yv) : 0.f);
+      float m2 = 0.f;
+      tmem_chunks<N2>(d2, [&](const uint32_t* v, int, int) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) m2 = max3f(m2, fabsf(__uint_as_float(v[e])), fabsf(__uint_as_float(v[e + 1])));
+      });
+      FQ_SUB(9);
+      const float4 r = exchange(valid ? m2 : 0.f);
       FQ_SUB(10);
       float mp;                                          // max |Y_t| * 2^pe (prescaled)
       if constexpr (N1 == 64) mp = tt == 0 ? fmaxf(r.x, r.y) : fmaxf(r.z, r.w);
       else mp = fmaxf(fmaxf(r.x, r.y), fmaxf(r.z, r.w));
       const int64_t t = t0 + tt;
-      if (valid && t < T) {
-        const float inv_pre = exp2i(-((TOK > 1 && tt) ? pe[TOK - 1] : pe[0]));
-        // code = clamp(rint(y * cq), -8, 7) with cq = 7 / (alpha m) (on the prescaled values, exactly
-        // (7 / (alpha m)) / 2^pe).  The clamp rides on the FMA pipe: u = sat((y cq + 8) / 15) in [0, 1],
-        // then fma(u, 15, MAGIC - 8) rounds u*15 - 8 half-to-even into the low mantissa bits; the
-        // extra rounding of u moves y*cq by < 1e-5 code units (well inside the near-tie window).
-        const float c15 = mp > 0.f ? (7.0f / (alpha * mp)) * (1.0f / 15.0f) : 0.f;
-        constexpr float B15 = 8.0f / 15.0f;
-        uint32_t w[N2 / 8];
+      const bool store = valid && t < T;
+      const float inv_pre = exp2i(-((TOK > 1 && tt) ? pe[TOK - 1] : pe[0]));
+      // code = clamp(rint(y * cq), -8, 7) with cq = 7 / (alpha m) (on the prescaled values, exactly
+      // (7 / (alpha m)) / 2^pe).  The clamp rides on the FMA pipe: u = sat((y cq + 8) / 15) in [0, 1],
+      // then fma(u, 15, MAGIC - 8) rounds u*15 - 8 half-to-even into the low mantissa bits; the
+      // extra rounding of u moves y*cq by < 1e-5 code units (well inside the near-tie window).
+      const float c15 = mp > 0.f ? __fdividef(7.0f / 15.0f, alpha * mp) : 0.f;
+      constexpr float B15 = 8.0f / 15.0f;
+      uint8_t* qrow = q + (store ? t * QTOK + i * QROW : 0);
+      tmem_chunks<N2>(d2, [&](const uint32_t* v, int, int col) {   // N2 % 32 == 0: full chunks
+        uint32_t w[4];
 #pragma unroll
-        for (int c8 = 0; c8 < N2 / 8; ++c8) {
+        for (int c8 = 0; c8 < 4; ++c8) {
           float z[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e)
-            z[e] = fmaf(fma_sat(__uint_as_float(yv[8 * c8 + e]), c15, B15), 15.0f, MAGIC - 8.0f);
+            z[e] = fmaf(fma_sat(__uint_as_float(v[8 * c8 + e]), c15, B15), 15.0f, MAGIC - 8.0f);
           w[c8] = pack8(z);
         }
-        uint4* dst = reinterpret_cast<uint4*>(q + t * QTOK + i * QROW);
-#pragma unroll
-        for (int c = 0; c < N2 / 32; ++c) dst[c] = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
-        if (i == 0) scale[t] = mp > 0.f ? alpha * (mp * inv_pre) / 7.0f : 1.0f;
+        if (store) *reinterpret_cast<uint4*>(qrow + col / 2) = make_uint4(w[0], w[1], w[2], w[3]);
         if constexpr (WRITE_Y) {
-          float2* yd = reinterpret_cast<float2*>(y_out + t * (N1 * N2) + i * N2);   // y is 8-B aligned (ABI)
+          if (store) {
+            float2* yd = reinterpret_cast<float2*>(y_out + t * (N1 * N2) + i * N2 + col);   // 8-B aligned (ABI)
 #pragma unroll
-          for (int c = 0; c < N2 / 2; ++c)
-            yd[c] = make_float2(__uint_as_float(yv[2 * c]) * inv_pre, __uint_as_float(yv[2 * c + 1]) * inv_pre);
+            for (int e = 0; e < 16; ++e)
+              yd[e] = make_float2(__uint_as_float(v[2 * e]) * inv_pre, __uint_as_float(v[2 * e + 1]) * inv_pre);
+          }
         }
-      }
+      });
+      tc::fence_before();
+      if (store && i == 0) scale[t] = mp > 0.f ? alpha * (mp * inv_pre) / 7.0f : 1.0f;
       if (L == 0 && k < 16) trace(104 + k);
     }
   }
@@ -453,9 +495,10 @@ static cudaError_t launch(const TQArgs& a) {
   }
   const int64_t tiles = (a.T + C::TOK - 1) / C::TOK;
   const int grid = int(std::min<int64_t>(tiles, num_sms()));
-  kern<<<grid, THREADS, C::SMEM, a.stream>>>(mx, m1, m2, a.T, a.alpha, a.q, a.scale, a.y);
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(C::THREADS), C::SMEM, a.stream, 1, mx, m1, m2, a.T, a.alpha,
+                             a.q, a.scale, a.y);
   count_launch();
-  return cudaGetLastError();
+  return e;
 }
 
 template <int N1, int N2>

@@ -16,11 +16,12 @@ import synth  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C3")
 ap.add_argument("--linear", default="P_ug")
+ap.add_argument("--T", type=int, default=0, help="override the token count")
 a = ap.parse_args()
 cfg = synth.config(a.config)
 lin = [l for l in cfg["linears"] if l.name == a.linear][0]
 dev = torch.device("cuda:0")
-T = cfg["T"]
+T = a.T or cfg["T"]
 x = torch.from_numpy(synth.activations(T, lin.K, seed=1, tag=lin.name)).to(dev)
 p1 = torch.from_numpy(synth.well_conditioned(lin.n1, seed=0, tag="p1")).to(dev)
 p2 = torch.from_numpy(synth.well_conditioned(lin.n2, seed=0, tag="p2")).to(dev)
