@@ -242,9 +242,12 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         widen8(p1.y, w[10], w[11]);
         widen8(p1.z, w[12], w[13]);
         widen8(p1.w, w[14], w[15]);
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&pempty[sp]);               // packed A consumed (registers)
         tmem_st16(tl + uint32_t(st * A_COLS), w);
+        // release the ring slot only after the loaded values were consumed (the tcgen05.st reads
+        // them): mbarrier.arrive does not wait for an outstanding ld.shared, so an arrive right
+        // after the loads lets the TMA overwrite the slot before a delayed load has read it
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&pempty[sp]);
       };
       while (cv.valid) {
         const int jt = jtrace;
@@ -292,8 +295,6 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           widen8(pk.z, o[i][4], o[i][5]);
           widen8(pk.w, o[i][6], o[i][7]);
         }
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&pempty[sp]);               // packed B consumed (registers)
 #pragma unroll
         for (int i = 0; i < B_TASKS; ++i) {
           const int task = ct + i * NUM_B_WARPS * 32, rl = task >> 2, c = task & 3;
@@ -301,6 +302,8 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           tc::sts128(rowp + uint32_t(((2 * c) ^ (rl & 7)) << 4), o[i][0], o[i][1], o[i][2], o[i][3]);
           tc::sts128(rowp + uint32_t(((2 * c + 1) ^ (rl & 7)) << 4), o[i][4], o[i][5], o[i][6], o[i][7]);
         }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&pempty[sp]);               // packed B consumed (stored above)
         if (trB) trace(210 + (job - 16) * 3 + 1);
         tc::fence_proxy_async_smem();
         if (trB) trace(210 + (job - 16) * 3 + 2);
