@@ -34,6 +34,21 @@ FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1
 INT8_PER_BF16 = 2.0          # nominal dense ratio (4.5 / 2.25 POPS), B200_PROFILING.md
 
 
+def ncu_traffic(cfg_name, linears, kind):
+    """DRAM bytes (read + write) of one step's `kind` launches ("gemm" or "tq") from the committed
+    ncu --set full captures (profiles/ncu_traffic.json, scripts/make_profiles.py), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if cfg_name != "C3" or not os.path.exists(path):
+        return None
+    t = json.load(open(path))
+    keys = [f"{kind}_{lin.name}" for lin in linears]
+    if not all(k in t for k in keys):
+        return None
+    return {"bytes_per_step": int(sum(t[k]["dram_bytes"] for k in keys)),
+            "source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum, one launch per linear: "
+                      + ", ".join(sorted({t[k]["capture"].split(":")[0] for k in keys}))}
+
+
 def peaks():
     if os.path.exists(PEAKS_PATH):
         p = json.load(open(PEAKS_PATH))
@@ -149,6 +164,11 @@ def tq_flops(T, lin):
 
 def gemm_ops(T, lin):
     return 2 * T * lin.N * lin.K
+
+
+def gemm_min_bytes(T, lin):
+    """Compulsory HBM bytes of one W4A4 GEMM: packed codes of A and W, scales, fp16 output."""
+    return T * lin.K // 2 + lin.N * lin.K // 2 + 4 * (T + lin.N) + 2 * T * lin.N
 
 
 # ------------------------------------------------------------------------ oracle (CPU) timing
@@ -371,6 +391,8 @@ def run_ours(args):
         rate, cores, sample = cpu_oracle_rate(args.config, 128, args.alpha)
         cpu = {"value": round(rate, 2), "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample}
 
+    gemm_traffic = ncu_traffic(args.config, [L["lin"] for L in layers], "gemm")
+    tq_traffic = ncu_traffic(args.config, [L["lin"] for L in layers], "tq")
     if rank == 0:
         frac = gemm_tops / int8_peak
         out = {
@@ -386,10 +408,13 @@ def run_ours(args):
                        "l2": "flushed (256 MiB write) before every timed step; flush untimed"},
             "roofline": {"bound": "tensor", "kernel": "fq_w4a4_linear (tcgen05 kind::i8)",
                          "achieved": round(gemm_tops, 1), "peak": round(int8_peak, 1), "unit": "TOPS",
-                         "frac": round(frac, 4), "traffic": None,
+                         "frac": round(frac, 4), "traffic": gemm_traffic,
+                         "per": "aggregate of the step's GEMM launches (sum of 2TNK / sum of their durations)",
+                         "algorithmic_bytes_per_step": int(sum(gemm_min_bytes(T, L["lin"]) for L in layers)),
                          "peak_source": f"{peak_src}: bf16 {pk['bf16_tflops']} TF/s x nominal int8/bf16 ratio 2"},
             "tq_roofline": {"bound": "hbm", "kernel": "fq_transform_quant", "achieved": round(tq_gbs, 1),
                             "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(tq_gbs / pk["hbm_gbs"], 4),
+                            "traffic": tq_traffic, "algorithmic_bytes_per_step": int(t_bytes),
                             "tflops": round(t_flops / (tq_ms * 1e-3) / 1e12, 1)},
             "time_share": {"transform_quant": round(tq_ms / ms_per_step, 4), "gemm": round(gemm_ms / ms_per_step, 4),
                            "note": "shares of the serialised per-kernel times (pass 2) relative to the step span (pass 1)"},

@@ -13,7 +13,7 @@ timeout 600 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/
 if [ -z "$NO_NCU" ]; then
 timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-fp16 > gpurun_out/ncu_bench.log 2>&1
-for LIN in ${PROF_LINEARS:-P_ug P_d}; do
+for LIN in ${PROF_LINEARS:-P_a P_o P_ug P_d}; do
   timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemm -s 2 -c 1 -f \
     -o gpurun_out/prof_gemm_$LIN python scripts/prof_kernels.py --linear $LIN > gpurun_out/ncu_gemm_$LIN.log 2>&1
   timeout 600 $NCU --set full --clock-control none --import-source on -k regex:tq_ -s 2 -c 1 -f \

@@ -18,7 +18,8 @@ for _, name, grid, ns in rows:
     a = agg.setdefault(short, [])
     a.append(ns)
 tot = sum(ns for *_, ns in rows)
-ours = sum(ns for _, n, _, ns in rows if n.startswith("void fq::"))
-print(f"{len(rows)} launches, total {tot / 1e3:.1f} us, fq:: kernels {ours / tot * 100:.1f}% of it")
+OURS = ("g3::", "tq5::", "fq::", "tq_mma", "tq_simt", "gemm_pair", "gemm_tc05", "gemm_mma")
+ours = sum(ns for _, n, _, ns in rows if any(k in n for k in OURS))
+print(f"{len(rows)} launches, total {tot / 1e3:.1f} us, this library's kernels {ours / tot * 100:.1f}% of it")
 for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
     print(f"{sum(v) / tot * 100:6.2f}%  n={len(v):3d}  mean {sum(v) / len(v) / 1e3:9.2f} us  min {min(v) / 1e3:9.2f} us  {k}")
