@@ -131,9 +131,60 @@ def dequantize_rows(codes, scales) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------
+# a4-a5, asymmetric mode (reading R19).  The paper quantizes
+# activations per-token symmetric and uses asymmetric min-max quantization for
+# the KV cache; SPEC.md:135 defines asymmetric as s = clip (max - min) / (2^b - 1)
+# with a zero point on the unsigned grid {0..2^b-1} (Eq.1's Omega(b)).  Reading R19:
+# the range is widened to include 0 (lo = min(alpha min y, 0), hi = max(alpha max y, 0)), the
+# usual min-max convention, so the zero point is an integer in [0, 15] and zero is exactly
+# representable.
+#   s = (hi - lo) / 15 (s = 1 if hi == lo, i.e. an all-zero row)   z = rint(-lo / s)
+#   q = clamp(rint(y / s) + z, 0, 15)                                dequant: s (q - z)
+# ---------------------------------------------------------------------------
+AQMAX = 15                                # 2^b - 1 for b = 4
+
+
+def quantize_rows_asym(y, alpha: float = 1.0, rounding: str = "half_even"):
+    """Return (codes int8 in [0, 15] [R, C], scales float64 [R], zero points int64 [R])."""
+    if not (0.0 < alpha <= 1.0):
+        raise ValueError("alpha must be in (0, 1]")
+    y = _f64(y)
+    if y.shape[1]:
+        hi = np.maximum(alpha * np.max(y, axis=1), 0.0)
+        lo = np.minimum(alpha * np.min(y, axis=1), 0.0)
+    else:
+        hi = lo = np.zeros(y.shape[0])
+    s = (hi - lo) / AQMAX
+    s = np.where(s == 0.0, 1.0, s)
+    z = _round(-lo / s, rounding).astype(np.int64)
+    q = np.clip(_round(y / s[:, None], rounding) + z[:, None], 0, AQMAX).astype(np.int8)
+    return q, s, z
+
+
+def dequantize_rows_asym(codes, scales, zeros) -> np.ndarray:
+    return (np.asarray(codes, dtype=np.float64) - np.asarray(zeros, np.float64)[:, None]) * _f64(scales)[:, None]
+
+
+def transform_quant_asym(x, p1, p2, alpha: float = 1.0, rounding: str = "half_even"):
+    """Returns (codes int8 [0,15] [T, n], scales float64 [T], zeros int64 [T], y float64 [T, n])."""
+    y = kron_transform(x, p1, p2)
+    q, s, z = quantize_rows_asym(y, alpha, rounding)
+    return q, s, z, y
+
+
+def w4a4_linear_asym(qa, sa, za, qw, sw) -> np.ndarray:
+    """Y[t,o] = s_a[t] s_w[o] sum_k (q_a[t,k] - z_a[t]) q_w[o,k]  (asymmetric activations,
+    symmetric weights): the dequantized product, Y = deq(A) deq(W)^T."""
+    qa_c = np.asarray(qa, np.int64) - np.asarray(za, np.int64)[:, None]
+    return dequant(int_gemm(qa_c, qw), sa, sw)
+
+
+# ---------------------------------------------------------------------------
 # a5: packing (R7): byte i of a row holds element 2i (low nibble) and 2i+1.
 # ---------------------------------------------------------------------------
 def pack_int4(codes) -> np.ndarray:
+    """Signed codes in [-8, 7] -> two's-complement nibbles (asymmetric codes q in [0, 15] are
+    packed as q - 8, reading R19)."""
     c = np.asarray(codes, dtype=np.int16)
     if c.shape[-1] % 2:
         raise ValueError("row length must be even")

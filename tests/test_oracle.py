@@ -267,3 +267,54 @@ def test_near_tie_mask():
     s = np.array([0.5])
     m = O.near_tie_mask(y, s, 0.02)
     assert m.tolist() == [[False, True, False, True]]
+
+
+# ---------------------------------------------------------------- asymmetric mode (NEXT-1, R19)
+def test_asym_worked_examples():
+    """SPEC.md:135 asymmetric min-max with R19's zero-inclusive range.
+    [0, 1.5, 3] -> s = 3/15 = 0.2, z = 0, codes [0, 8 (rint(7.5) = 8, half-even), 15];
+    [-1, 0.5, 2] -> s = 3/15, z = rint(5) = 5, codes [0, rint(2.5) + 5 = 7, 15];
+    one-signed rows keep 0 in the range: [2, 3, 4] -> s = 4/15, z = 0, codes [8, 11, 15];
+    [-4, -3, -2] -> z = 15, codes [0, rint(-11.25) + 15 = 4, rint(-7.5) + 15 = 7]."""
+    q, s, z = O.quantize_rows_asym(np.array([[0.0, 1.5, 3.0]]))
+    assert np.isclose(s[0], 0.2) and z[0] == 0 and q[0].tolist() == [0, 8, 15]
+    q, s, z = O.quantize_rows_asym(np.array([[-1.0, 0.5, 2.0]]))
+    assert np.isclose(s[0], 0.2) and z[0] == 5 and q[0].tolist() == [0, 7, 15]
+    # one-signed rows still include 0 in the range: z stays in [0, 15]
+    q, s, z = O.quantize_rows_asym(np.array([[2.0, 3.0, 4.0], [-4.0, -3.0, -2.0], [0.0, 0.0, 0.0]]))
+    assert z.tolist() == [0, 15, 0] and s[2] == 1.0 and np.all(q[2] == 0)
+    assert q[0].tolist() == [8, 11, 15] and q[1].tolist() == [0, 4, 7]
+
+
+def test_asym_bruteforce_grid_and_half_step():
+    """Codes are the nearest point of the 16-point grid {s (q - z)} (brute force over the grid),
+    within s/2 inside the (clipped) range, and the extreme of the range is hit exactly."""
+    g = np.random.default_rng(11)
+    y = g.standard_normal((40, 48)) * g.uniform(0.1, 50, size=(40, 1)) + g.normal(0, 3, size=(40, 1))
+    for alpha in (1.0, 0.85):
+        q, s, z = O.quantize_rows_asym(y, alpha)
+        grid = (np.arange(16)[None, :] - z[:, None]) * s[:, None]              # [R, 16]
+        best = np.abs(y[:, :, None] - grid[:, None, :]).argmin(axis=2)
+        dist_q = np.abs(y - O.dequantize_rows_asym(q, s, z))
+        dist_b = np.abs(y - np.take_along_axis(grid, best, 1))
+        assert np.allclose(dist_q, dist_b, atol=1e-12)                        # nearest grid point
+        hi = np.maximum(alpha * y.max(1), 0)
+        lo = np.minimum(alpha * y.min(1), 0)
+        inside = (y <= hi[:, None] + 1e-12) & (y >= lo[:, None] - 1e-12)
+        assert np.all(dist_q[inside] <= s.repeat(48).reshape(40, 48)[inside] / 2 + 1e-12)
+        assert np.all((z >= 0) & (z <= 15)) and np.all((q >= 0) & (q <= 15))
+
+
+def test_asym_linear_equals_dequantized_product():
+    """w4a4_linear_asym is exactly deq(A) deq(W)^T (closed form), and equals the symmetric
+    GEMM of the q - 8 codes minus the (z - 8) colsum(W) correction the GPU epilogue applies."""
+    g = np.random.default_rng(4)
+    x = g.standard_normal((9, 64)); w = g.standard_normal((7, 64))
+    qa, sa, za = O.quantize_rows_asym(x, 0.9)
+    qw, sw = O.quantize_rows(w)
+    y = O.w4a4_linear_asym(qa, sa, za, qw, sw)
+    ref = O.dequantize_rows_asym(qa, sa, za) @ O.dequantize_rows(qw, sw).T
+    assert np.allclose(y, ref, rtol=1e-12, atol=1e-12)
+    acc8 = O.int_gemm(qa.astype(np.int64) - 8, qw)
+    corr = (za - 8)[:, None] * qw.astype(np.int64).sum(1)[None, :]
+    assert np.array_equal(acc8 - corr, O.int_gemm(qa.astype(np.int64) - za[:, None], qw))
