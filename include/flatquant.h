@@ -38,20 +38,23 @@
 extern "C" {
 #endif
 
-#define FQ_ABI_VERSION 1
+#define FQ_ABI_VERSION 2   /* 2: FQ_ASYM + fq_weight_colsum */
 
 typedef enum {
   FQ_OK = 0,
   FQ_EINVAL = 1,   /* null pointer, bad enum, alpha outside (0, 1], negative size          */
   FQ_ESHAPE = 2,   /* n1*n2 != K, odd K, K % 32 != 0 for the GEMM, misaligned pointer/stride */
-  FQ_ENOTSUP = 3,  /* well-formed but no kernel for it (e.g. n1 or n2 > 256, FQ_ASYM)       */
+  FQ_ENOTSUP = 3,  /* well-formed but no kernel for it (e.g. n1 or n2 > 256)                 */
   FQ_ECUDA = 4     /* a CUDA launch/runtime call failed; see fq_last_cuda_error()            */
 } fq_status;
 
 typedef enum { FQ_F16 = 0, FQ_BF16 = 1 } fq_dtype;
 
-/* FQ_SYM: per-token symmetric (the paper's setting).  FQ_ASYM is reserved
- * for the asymmetric mode and returns FQ_ENOTSUP in ABI v1. */
+/* FQ_SYM: per-token symmetric (the paper's setting).
+ * FQ_ASYM: per-token asymmetric min-max (DESIGN.md reading
+ *   R19): lo = min(alpha min y, 0), hi = max(alpha max y, 0), s = (hi - lo) / 15 (1 if hi == lo),
+ *   z = rint(-lo / s) in [0, 15], q = clamp(rint(y / s) + z, 0, 15); the nibble stores q - 8
+ *   (two's complement, so the GEMM's signed widening is unchanged) and zero[t] stores z - 8. */
 typedef enum { FQ_SYM = 0, FQ_ASYM = 1 } fq_qmode;
 
 /* ---------------------------------------------------------------------------------------
@@ -63,9 +66,11 @@ typedef enum { FQ_SYM = 0, FQ_ASYM = 1 } fq_qmode;
  *          Viewed as V_t = reshape(x_t, n1, n2) in C order.
  *   p1     [n1, n1] row-major, x_dtype.     p2 [n2, n2] row-major, x_dtype.
  *   alpha  post-sigmoid clipping ratio in (0, 1]; 1 = no clipping.
- *   qmode  FQ_SYM (FQ_ASYM -> FQ_ENOTSUP in v1).
+ *   qmode  FQ_SYM or FQ_ASYM.
  *   q      [T, n/2] uint8 packed codes (output).     scale [T] fp32 (output), s_t.
- *   zero   must be NULL for FQ_SYM.
+ *   zero   FQ_SYM: must be NULL.  FQ_ASYM: [T] int8 (output), z_t - 8.
+ *   FQ_ASYM runs on the tcgen05 kernel shapes and the CUDA-core kernel (n1 n2 <= 25600);
+ *   other shapes return FQ_ENOTSUP.
  *   Supported: n1, n2 >= 1, n even, n1, n2 <= 256 (tensor-core kernel when n1 % 16 == 0
  *   and n2 % 16 == 0; a CUDA-core kernel otherwise).
  * ------------------------------------------------------------------------------------- */
@@ -90,7 +95,12 @@ fq_status fq_transform_f32(const void* x, int32_t x_dtype, int64_t T, int64_t ld
  *
  *   qa [T, K/2] uint8 packed activation codes (from fq_transform_quant), sa [T] fp32.
  *   qw [N, K/2] uint8 packed weight codes (K contiguous, same nibble order), sw [N] fp32.
- *   za, colsum_w: asymmetric-mode hooks; must be NULL in ABI v1.
+ *   za, colsum_w: both NULL (symmetric activations) or both set (FQ_ASYM activations):
+ *      za [T] int8 = z_t - 8 from fq_transform_quant, colsum_w [N] int32 = sum_k qw[o,k]
+ *      (fq_weight_colsum, computed once per weight).  Then
+ *      Y[t,o] = cvt_rn( float(acc[t,o] - za[t] colsum_w[o]) * sa[t] * sw[o] ), i.e. the
+ *      dequantized product s_a (q - z) . s_w q_w.  Asymmetric inputs need the default GEMM
+ *      implementation (fq_set_gemm_impl(0)); FQ_ENOTSUP otherwise.
  *   y  [T, N] of y_dtype (FQ_F16 or FQ_BF16), row-major.
  *   Requires K % 32 == 0 and N % 8 == 0.  Exact integer accumulation (|acc| <= 64 K < 2^31).
  * ------------------------------------------------------------------------------------- */
@@ -98,6 +108,10 @@ fq_status fq_w4a4_linear(const uint8_t* qa, const float* sa, const int8_t* za, i
                          int32_t K, const uint8_t* qw, const float* sw,
                          const int32_t* colsum_w, int32_t N, void* y, int32_t y_dtype,
                          void* stream);
+
+/* fq_weight_colsum -- colsum[o] = sum_k qw[o,k] (int32, exact) of packed weight codes [N, K/2];
+ * offline preparation for asymmetric activations (fq_w4a4_linear's colsum_w). */
+fq_status fq_weight_colsum(const uint8_t* qw, int32_t N, int32_t K, int32_t* colsum, void* stream);
 
 /* fq_w4a4_gemm_i32 -- the same GEMM kernel exporting the raw int32 accumulators
  * acc [T, N] (bit-exactness bar).  Same shape requirements as fq_w4a4_linear. */

@@ -29,6 +29,7 @@ SIGNATURES = {
     "fq_transform_f32": (_i32, [_vp, _i32, _i64, _i64, _i32, _i32, _vp, _vp, _f32, _vp, _vp, _vp, _vp]),
     "fq_w4a4_linear": (_i32, [_vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _i32, _vp, _i32, _vp]),
     "fq_w4a4_gemm_i32": (_i32, [_vp, _i64, _i32, _vp, _i32, _vp, _vp]),
+    "fq_weight_colsum": (_i32, [_vp, _i32, _i32, _vp, _vp]),
     "fq_flatquant_linear": (_i32, [_vp, _i32, _i64, _i32, _i32, _vp, _vp, _f32, _vp, _vp, _i32, _vp, _i32,
                                    _vp, _vp, _vp]),
     "fq_flatquant_linear_host": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp, _vp, _f32, _vp, _vp, _i32, _vp,

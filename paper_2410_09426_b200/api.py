@@ -15,6 +15,7 @@ from ._lib import FQ_BF16, FQ_F16, FQ_SYM, check, load
 
 __all__ = [
     "fq_transform_quant", "fq_transform_f32", "fq_w4a4_linear", "fq_w4a4_gemm_i32", "fq_flatquant_linear",
+    "fq_weight_colsum", "weight_colsum", "transform_quant_asym",
     "fq_flatquant_linear_host", "fq_choose_decomposition", "fq_set_gemm_impl", "fq_set_tq_impl", "fq_launch_count",
     "fq_abi_version", "transform_quant", "transform_f32", "w4a4_linear", "w4a4_gemm_i32", "prepare_weight",
     "flatquant_linear",
@@ -77,6 +78,12 @@ def fq_w4a4_gemm_i32(qa, qw, acc, K=None, stream=None):
     check("fq_w4a4_gemm_i32", st)
 
 
+def fq_weight_colsum(qw, colsum, K=None, stream=None):
+    _cuda(qw, colsum)
+    K = qw.shape[1] * 2 if K is None else K
+    check("fq_weight_colsum", load().fq_weight_colsum(_ptr(qw), qw.shape[0], K, _ptr(colsum), _stream(stream)))
+
+
 def fq_flatquant_linear(x, n1, n2, p1, p2, alpha, qw, sw, y, q_ws, s_ws, stream=None):
     _cuda(x, p1, p2, qw, sw, y, q_ws, s_ws)
     st = load().fq_flatquant_linear(_ptr(x), _fq_dtype(x.dtype), x.shape[0], n1, n2, _ptr(p1), _ptr(p2),
@@ -128,6 +135,23 @@ def transform_quant(x, n1, n2, p1, p2, alpha=1.0, stream=None):
     return q, s
 
 
+def transform_quant_asym(x, n1, n2, p1, p2, alpha=1.0, stream=None):
+    """FQ_ASYM: returns (q packed [T, n/2] holding q - 8, scale [T], zero [T]
+    int8 holding z - 8)."""
+    T = x.shape[0]
+    q = torch.empty((T, n1 * n2 // 2), dtype=torch.uint8, device=x.device)
+    s = torch.empty((T,), dtype=torch.float32, device=x.device)
+    z = torch.empty((T,), dtype=torch.int8, device=x.device)
+    fq_transform_quant(x, n1, n2, p1, p2, alpha, q, s, zero=z, qmode=_lib.FQ_ASYM, stream=stream)
+    return q, s, z
+
+
+def weight_colsum(qw, stream=None):
+    colsum = torch.empty((qw.shape[0],), dtype=torch.int32, device=qw.device)
+    fq_weight_colsum(qw, colsum, stream=stream)
+    return colsum
+
+
 def transform_f32(x, n1, n2, p1, p2, alpha=1.0, stream=None):
     T = x.shape[0]
     q = torch.empty((T, n1 * n2 // 2), dtype=torch.uint8, device=x.device)
@@ -137,9 +161,9 @@ def transform_f32(x, n1, n2, p1, p2, alpha=1.0, stream=None):
     return q, s, y
 
 
-def w4a4_linear(qa, sa, qw, sw, out_dtype=torch.float16, stream=None):
+def w4a4_linear(qa, sa, qw, sw, out_dtype=torch.float16, za=None, colsum_w=None, stream=None):
     y = torch.empty((qa.shape[0], qw.shape[0]), dtype=out_dtype, device=qa.device)
-    fq_w4a4_linear(qa, sa, qw, sw, y, stream=stream)
+    fq_w4a4_linear(qa, sa, qw, sw, y, za=za, colsum_w=colsum_w, stream=stream)
     return y
 
 

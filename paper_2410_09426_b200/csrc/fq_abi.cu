@@ -74,7 +74,7 @@ static fq_status validate_tq(const void* x, int32_t x_dtype, int64_t T, int64_t 
 
 static fq_status run_tq(const void* x, int32_t x_dtype, int64_t T, int64_t ldx, int32_t n1, int32_t n2,
                         const void* p1, const void* p2, float alpha, uint8_t* q, float* scale, float* y,
-                        void* stream) {
+                        int8_t* zero, void* stream) {
   TQArgs a{};
   a.x = x;
   a.T = T;
@@ -87,10 +87,12 @@ static fq_status run_tq(const void* x, int32_t x_dtype, int64_t T, int64_t ldx, 
   a.q = q;
   a.scale = scale;
   a.y = y;
+  a.zero = zero;
   a.bf16 = (x_dtype == FQ_BF16);
   a.stream = static_cast<cudaStream_t>(stream);
   const bool tc = (n1 % 16 == 0) && (n2 % 16 == 0);
   if (!tc && !tq_simt_supported(n1, n2)) return FQ_ENOTSUP;
+  if (zero && !tq_asym_supported(a)) return FQ_ENOTSUP;
   return cuda_status(transform_quant_launch(a));
 }
 
@@ -107,7 +109,8 @@ static fq_status validate_gemm(const uint8_t* qa, int64_t T, int32_t K, const ui
 }
 
 static fq_status run_gemm(const uint8_t* qa, const float* sa, int64_t T, int32_t K, const uint8_t* qw,
-                          const float* sw, int32_t N, void* y, bool y_bf16, bool out_i32, void* stream) {
+                          const float* sw, int32_t N, void* y, bool y_bf16, bool out_i32, void* stream,
+                          const int8_t* za = nullptr, const int32_t* colsum = nullptr) {
   GemmArgs a{};
   a.qa = qa;
   a.sa = sa;
@@ -119,8 +122,14 @@ static fq_status run_gemm(const uint8_t* qa, const float* sa, int64_t T, int32_t
   a.y = y;
   a.y_bf16 = y_bf16;
   a.out_i32 = out_i32;
+  a.za = za;
+  a.colsum = colsum;
   a.stream = static_cast<cudaStream_t>(stream);
   const int impl = g_gemm_impl.load();
+  if (za) {                                        // asymmetric activations: pair kernel only
+    if (impl != 0 || !gemm_pair_supported(a)) return FQ_ENOTSUP;
+    return cuda_status(gemm_pair_launch(a));
+  }
   if (impl == 0 && gemm_pair_supported(a)) return cuda_status(gemm_pair_launch(a));
   if (impl == 2 && gemm_tc05_supported(a)) return cuda_status(gemm_tc05_launch(a));
   return cuda_status(gemm_mma_launch(a));
@@ -136,11 +145,10 @@ fq_status fq_transform_quant(const void* x, int32_t x_dtype, int64_t T, int64_t 
                              const void* p1, const void* p2, float alpha, int32_t qmode, uint8_t* q,
                              float* scale, int8_t* zero, void* stream) {
   if (qmode != FQ_SYM && qmode != FQ_ASYM) return FQ_EINVAL;
-  if (qmode == FQ_ASYM) return FQ_ENOTSUP;
-  if (zero != nullptr) return FQ_EINVAL;
+  if ((qmode == FQ_SYM) != (zero == nullptr)) return FQ_EINVAL;   // zero iff asymmetric
   fq_status s = validate_tq(x, x_dtype, T, ldx, n1, n2, p1, p2, alpha, q, scale);
   if (s != FQ_OK || T == 0) return s;
-  return run_tq(x, x_dtype, T, ldx, n1, n2, p1, p2, alpha, q, scale, nullptr, stream);
+  return run_tq(x, x_dtype, T, ldx, n1, n2, p1, p2, alpha, q, scale, nullptr, zero, stream);
 }
 
 fq_status fq_transform_f32(const void* x, int32_t x_dtype, int64_t T, int64_t ldx, int32_t n1, int32_t n2,
@@ -150,19 +158,19 @@ fq_status fq_transform_f32(const void* x, int32_t x_dtype, int64_t T, int64_t ld
   if (s != FQ_OK || T == 0) return s;
   if (!y) return FQ_EINVAL;
   if ((reinterpret_cast<uintptr_t>(y) & 7u) != 0) return FQ_ESHAPE;
-  return run_tq(x, x_dtype, T, ldx, n1, n2, p1, p2, alpha, q, scale, y, stream);
+  return run_tq(x, x_dtype, T, ldx, n1, n2, p1, p2, alpha, q, scale, y, nullptr, stream);
 }
 
 fq_status fq_w4a4_linear(const uint8_t* qa, const float* sa, const int8_t* za, int64_t T, int32_t K,
                          const uint8_t* qw, const float* sw, const int32_t* colsum_w, int32_t N, void* y,
                          int32_t y_dtype, void* stream) {
   if (y_dtype != FQ_F16 && y_dtype != FQ_BF16) return FQ_EINVAL;
-  if (za != nullptr || colsum_w != nullptr) return FQ_ENOTSUP;
+  if ((za == nullptr) != (colsum_w == nullptr)) return FQ_EINVAL;   // both or neither
   fq_status s = validate_gemm(qa, T, K, qw, N, y);
   if (s != FQ_OK || T == 0 || N == 0) return s;
   if (!sa || !sw) return FQ_EINVAL;
-  if (!aligned16(sw)) return FQ_ESHAPE;
-  return run_gemm(qa, sa, T, K, qw, sw, N, y, y_dtype == FQ_BF16, false, stream);
+  if (!aligned16(sw) || (colsum_w && !aligned16(colsum_w))) return FQ_ESHAPE;
+  return run_gemm(qa, sa, T, K, qw, sw, N, y, y_dtype == FQ_BF16, false, stream, za, colsum_w);
 }
 
 fq_status fq_w4a4_gemm_i32(const uint8_t* qa, int64_t T, int32_t K, const uint8_t* qw, int32_t N,
@@ -184,7 +192,7 @@ fq_status fq_flatquant_linear(const void* x, int32_t x_dtype, int64_t T, int32_t
   if (s != FQ_OK || N == 0) return s;
   if (!sw) return FQ_EINVAL;
   if (!aligned16(sw)) return FQ_ESHAPE;
-  s = run_tq(x, x_dtype, T, n, n1, n2, p1, p2, alpha, q_ws, s_ws, nullptr, stream);
+  s = run_tq(x, x_dtype, T, n, n1, n2, p1, p2, alpha, q_ws, s_ws, nullptr, nullptr, stream);
   if (s != FQ_OK) return s;
   return run_gemm(q_ws, s_ws, T, int32_t(n), qw, sw, N, y, y_dtype == FQ_BF16, false, stream);
 }
@@ -206,6 +214,15 @@ fq_status fq_flatquant_linear_host(const void* x_host, void* x_dev, int32_t x_dt
   s = cuda_status(cudaMemcpyAsync(y_host, y_dev, ybytes, cudaMemcpyDeviceToHost, st));
   if (s != FQ_OK) return s;
   return cuda_status(cudaStreamSynchronize(st));
+}
+
+fq_status fq_weight_colsum(const uint8_t* qw, int32_t N, int32_t K, int32_t* colsum, void* stream) {
+  if (N < 0 || K < 0) return FQ_EINVAL;
+  if (N == 0) return FQ_OK;
+  if (!qw || !colsum) return FQ_EINVAL;
+  if (K % 2 != 0) return FQ_ESHAPE;
+  if ((reinterpret_cast<uintptr_t>(colsum) & 3u) != 0) return FQ_ESHAPE;
+  return cuda_status(weight_colsum_launch(qw, N, K, colsum, static_cast<cudaStream_t>(stream)));
 }
 
 fq_status fq_choose_decomposition(int64_t n, int32_t* n1, int32_t* n2) {

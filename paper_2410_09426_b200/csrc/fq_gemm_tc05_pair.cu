@@ -115,11 +115,12 @@ struct Cursor {
   }
 };
 
-template <bool OUT_I32, bool BF16>
+template <bool OUT_I32, bool BF16, bool ASYM>
 __global__ void __launch_bounds__(THREADS, 1)
 gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmY, const float* __restrict__ sa, int T, int K,
-                 const float* __restrict__ sw, int N, void* __restrict__ yv) {
+                 const float* __restrict__ sw, int N, void* __restrict__ yv, const int8_t* __restrict__ za,
+                 const int32_t* __restrict__ colsum) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sP = smem + size_t(STAGES) * B_BYTES;                  // packed ring: [A 8 KB | B 6 KB]
@@ -381,6 +382,8 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         }
       } else {
         const float s_a = row_ok ? sa[row] * (1.0f / 256.0f) : 0.f;
+        // asymmetric activations: acc_true = acc - (z - 8) colsum_w; the TMEM holds 256 acc
+        const int zc256 = (ASYM && row_ok) ? int(za[row]) * 256 : 0;
 #pragma unroll 1
         for (int q = 0; q < BN / 64; ++q) {
           uint32_t v[64];
@@ -398,7 +401,22 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
               w0 = __ldg(reinterpret_cast<const float4*>(sw + col));
               w1 = __ldg(reinterpret_cast<const float4*>(sw + col + 4));
             }
-            const uint32_t* vv = &v[c8 * 8];
+            uint32_t* vv = &v[c8 * 8];
+            if constexpr (ASYM) {
+              int4 c0 = make_int4(0, 0, 0, 0), c1 = c0;
+              if (col < N) {
+                c0 = __ldg(reinterpret_cast<const int4*>(colsum + col));
+                c1 = __ldg(reinterpret_cast<const int4*>(colsum + col + 4));
+              }
+              vv[0] -= uint32_t(zc256 * c0.x);
+              vv[1] -= uint32_t(zc256 * c0.y);
+              vv[2] -= uint32_t(zc256 * c0.z);
+              vv[3] -= uint32_t(zc256 * c0.w);
+              vv[4] -= uint32_t(zc256 * c1.x);
+              vv[5] -= uint32_t(zc256 * c1.y);
+              vv[6] -= uint32_t(zc256 * c1.z);
+              vv[7] -= uint32_t(zc256 * c1.w);
+            }
             const float f0 = float(int(vv[0])) * s_a * w0.x, f1 = float(int(vv[1])) * s_a * w0.y;
             const float f2 = float(int(vv[2])) * s_a * w0.z, f3 = float(int(vv[3])) * s_a * w0.w;
             const float f4 = float(int(vv[4])) * s_a * w1.x, f5 = float(int(vv[5])) * s_a * w1.y;
@@ -462,10 +480,12 @@ bool gemm_pair_supported(const GemmArgs& a) {
 
 cudaError_t gemm_pair_launch(const GemmArgs& a) {
   using namespace g3;
-  auto kern = a.out_i32 ? gemm_pair_kernel<true, false>
-                        : (a.y_bf16 ? gemm_pair_kernel<false, true> : gemm_pair_kernel<false, false>);
-  static bool attr_done[3] = {false, false, false};
-  const int which = a.out_i32 ? 0 : (a.y_bf16 ? 1 : 2);
+  const bool asym = a.za != nullptr && !a.out_i32;
+  auto kern = a.out_i32 ? gemm_pair_kernel<true, false, false>
+              : asym    ? (a.y_bf16 ? gemm_pair_kernel<false, true, true> : gemm_pair_kernel<false, false, true>)
+                        : (a.y_bf16 ? gemm_pair_kernel<false, true, false> : gemm_pair_kernel<false, false, false>);
+  static bool attr_done[5] = {false, false, false, false, false};
+  const int which = a.out_i32 ? 0 : (a.y_bf16 ? 1 : 2) + (asym ? 2 : 0);
   if (!attr_done[which]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     if (e != cudaSuccess) return e;
@@ -493,9 +513,33 @@ cudaError_t gemm_pair_launch(const GemmArgs& a) {
   const int num_tiles = int((a.T + BM - 1) / BM) * ((a.N + BN - 1) / BN);
   const int clusters = std::max(1, std::min(num_tiles, num_sms() / 2));
   cudaError_t e = launch_pdl(kern, dim3(unsigned(2 * clusters)), dim3(THREADS), SMEM_BYTES, a.stream, 2, ma, mb, my,
-                             a.sa, int(a.T), a.K, a.sw, a.N, a.y);
+                             a.sa, int(a.T), a.K, a.sw, a.N, a.y, a.za, a.colsum);
   count_launch();
   if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+// colsum[o] = sum_k qw[o,k] over the signed nibbles of packed row o (one warp per row).
+__global__ void weight_colsum_kernel(const uint8_t* __restrict__ qw, int N, int KB, int32_t* __restrict__ colsum) {
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= N) return;
+  const uint8_t* p = qw + size_t(row) * KB;
+  int acc = 0;
+  for (int i = lane; i < KB; i += 32) {
+    const int b = p[i];
+    acc += ((b & 15) ^ 8) - 8 + ((b >> 4) ^ 8) - 8;     // sign-extended nibbles
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) colsum[row] = acc;
+}
+
+cudaError_t weight_colsum_launch(const uint8_t* qw, int N, int K, int32_t* colsum, cudaStream_t stream) {
+  const int rows_per_block = 8;
+  weight_colsum_kernel<<<(N + rows_per_block - 1) / rows_per_block, 32 * rows_per_block, 0, stream>>>(
+      qw, N, K / 2, colsum);
+  count_launch();
   return cudaGetLastError();
 }
 

@@ -24,6 +24,7 @@ struct TQArgs {
   uint8_t* q;
   float* scale;
   float* y;         // optional fp32 export of the transformed activations (debug / parity)
+  int8_t* zero;     // FQ_ASYM: per-token zero point - 8 (output); nullptr for FQ_SYM
   bool bf16;
   cudaStream_t stream;
 };
@@ -37,6 +38,8 @@ struct GemmArgs {
   const float* sw;
   int N;
   void* y;          // fp16/bf16 output, or int32 accumulators when out_i32
+  const int8_t* za;         // asymmetric activations: z - 8 per token (nullptr: symmetric)
+  const int32_t* colsum;    // asymmetric activations: sum_k qw[o,k] per output channel
   bool y_bf16;
   bool out_i32;
   cudaStream_t stream;
@@ -82,9 +85,11 @@ bool tq_mma_supported(int n1, int n2);                 // legacy mma.sync kernel
 cudaError_t tq_mma_launch(const TQArgs& a);
 cudaError_t tq_simt_launch(const TQArgs& a);
 bool tq_tc05_supported(const TQArgs& a);               // tcgen05 / TMA kernel
+bool tq_asym_supported(const TQArgs& a);               // FQ_ASYM available for this shape
 cudaError_t tq_tc05_launch(const TQArgs& a);
 int tq_impl();
 
+cudaError_t weight_colsum_launch(const uint8_t* qw, int N, int K, int32_t* colsum, cudaStream_t stream);
 cudaError_t gemm_mma_launch(const GemmArgs& a);      // legacy mma.sync cross-check kernel
 cudaError_t gemm_tc05_launch(const GemmArgs& a);     // tcgen05 kind::i8, single CTA
 bool gemm_tc05_supported(const GemmArgs& a);

@@ -166,11 +166,11 @@ FQ_DEVICE uint32_t pack8(const float (&v)[8]) {
   return (e & 0x0F0F0F0Fu) | ((o << 4) & 0xF0F0F0F0u);
 }
 
-template <int N1, int N2, bool BF16, bool WRITE_Y>
+template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM>
 __global__ void __launch_bounds__(Cfg<N1, N2>::THREADS, 1)
 tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmP1,
                const __grid_constant__ CUtensorMap tmP2, int64_t T, float alpha, uint8_t* __restrict__ q,
-               float* __restrict__ scale, float* __restrict__ y_out) {
+               float* __restrict__ scale, float* __restrict__ y_out, int8_t* __restrict__ zero) {
   using C = Cfg<N1, N2>;
   constexpr int S = C::STAGES, TOK = C::TOK, G = C::GROUPS, THREADS = C::THREADS;
   constexpr uint32_t IDESC1 = tc::idesc_f16(128, N1, BF16 ? 1 : 0, 1, 1);
@@ -402,17 +402,35 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
       const int tt = (N1 == 64) ? (L >> 6) : 0;
       const int i = (N1 == 64) ? (L & 63) : L;
       const bool valid = (N1 == 64) || (L < N1);
-      float m2 = 0.f;
+      float m2 = 0.f, hi2 = 0.f, lo2 = 0.f;             // sym: max |y|; asym: max(max y, 0), -min(min y, 0)
       tmem_chunks<N2>(d2, [&](const uint32_t* v, int, int) {
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) m2 = max3f(m2, fabsf(__uint_as_float(v[e])), fabsf(__uint_as_float(v[e + 1])));
+        for (int e = 0; e < 32; e += 2) {
+          const float a0 = __uint_as_float(v[e]), a1 = __uint_as_float(v[e + 1]);
+          if constexpr (ASYM) {
+            hi2 = max3f(hi2, a0, a1);
+            lo2 = max3f(lo2, -a0, -a1);
+          } else {
+            m2 = max3f(m2, fabsf(a0), fabsf(a1));
+          }
+        }
       });
       FQ_SUB(9);
-      const float4 r = exchange(valid ? m2 : 0.f);
+      float mp, hip = 0.f, lop = 0.f;                    // token statistics (prescaled by 2^pe)
+      {
+        auto tok_max = [&](float4 r) {
+          if constexpr (N1 == 64) return tt == 0 ? fmaxf(r.x, r.y) : fmaxf(r.z, r.w);
+          else return fmaxf(fmaxf(r.x, r.y), fmaxf(r.z, r.w));
+        };
+        if constexpr (ASYM) {
+          hip = tok_max(exchange(valid ? hi2 : 0.f));
+          lop = tok_max(exchange(valid ? lo2 : 0.f));
+          mp = hip + lop;                                // hi - lo, both >= 0 terms
+        } else {
+          mp = tok_max(exchange(valid ? m2 : 0.f));
+        }
+      }
       FQ_SUB(10);
-      float mp;                                          // max |Y_t| * 2^pe (prescaled)
-      if constexpr (N1 == 64) mp = tt == 0 ? fmaxf(r.x, r.y) : fmaxf(r.z, r.w);
-      else mp = fmaxf(fmaxf(r.x, r.y), fmaxf(r.z, r.w));
       const int64_t t = t0 + tt;
       const bool store = valid && t < T;
       const float inv_pre = exp2i(-((TOK > 1 && tt) ? pe[TOK - 1] : pe[0]));
@@ -420,8 +438,19 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
       // (7 / (alpha m)) / 2^pe).  The clamp rides on the FMA pipe: u = sat((y cq + 8) / 15) in [0, 1],
       // then fma(u, 15, MAGIC - 8) rounds u*15 - 8 half-to-even into the low mantissa bits; the
       // extra rounding of u moves y*cq by < 1e-5 code units (well inside the near-tie window).
-      const float c15 = mp > 0.f ? __fdividef(7.0f / 15.0f, alpha * mp) : 0.f;
-      constexpr float B15 = 8.0f / 15.0f;
+      // asymmetric (R19): s = alpha (hi - lo) / 15, z = rint(alpha lo' / s) with lo' = -min(min y, 0);
+      // q = clamp(rint(y / s) + z, 0, 15), stored as q - 8: the same FFMA.SAT form with
+      // c15 = 1 / (15 s) and offset z / 15 (z an integer, so rint(y/s + z) = rint(y/s) + z).
+      float c15, B15, zq = 0.f;
+      if constexpr (ASYM) {
+        const float sp = alpha * mp * (1.0f / 15.0f);
+        zq = sp > 0.f ? rintf(__fdiv_rn(alpha * lop, sp)) : 0.f;
+        c15 = sp > 0.f ? __frcp_rn(alpha * mp) : 0.f;
+        B15 = zq * (1.0f / 15.0f);
+      } else {
+        c15 = mp > 0.f ? __fdividef(7.0f / 15.0f, alpha * mp) : 0.f;
+        B15 = 8.0f / 15.0f;
+      }
       uint8_t* qrow = q + (store ? t * QTOK + i * QROW : 0);
       tmem_chunks<N2>(d2, [&](const uint32_t* v, int, int col) {   // N2 % 32 == 0: full chunks
         uint32_t w[4];
@@ -444,7 +473,14 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
         }
       });
       tc::fence_before();
-      if (store && i == 0) scale[t] = mp > 0.f ? alpha * (mp * inv_pre) / 7.0f : 1.0f;
+      if (store && i == 0) {
+        if constexpr (ASYM) {
+          scale[t] = mp > 0.f ? alpha * (mp * inv_pre) / 15.0f : 1.0f;
+          zero[t] = int8_t(int(zq) - 8);
+        } else {
+          scale[t] = mp > 0.f ? alpha * (mp * inv_pre) / 7.0f : 1.0f;
+        }
+      }
       if (L == 0 && k < 16) trace(104 + k);
     }
   }
@@ -464,10 +500,10 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
 }
 
 // ------------------------------------------------------------------------------ host side
-template <int N1, int N2, bool BF16, bool WRITE_Y>
+template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM = false>
 static cudaError_t launch(const TQArgs& a) {
   using C = Cfg<N1, N2>;
-  auto kern = tq_tc05_kernel<N1, N2, BF16, WRITE_Y>;
+  auto kern = tq_tc05_kernel<N1, N2, BF16, WRITE_Y, ASYM>;
   static bool attr_set = false;   // benign race: idempotent attribute set
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
@@ -496,13 +532,14 @@ static cudaError_t launch(const TQArgs& a) {
   const int64_t tiles = (a.T + C::TOK - 1) / C::TOK;
   const int grid = int(std::min<int64_t>(tiles, num_sms()));
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(C::THREADS), C::SMEM, a.stream, 1, mx, m1, m2, a.T, a.alpha,
-                             a.q, a.scale, a.y);
+                             a.q, a.scale, a.y, a.zero);
   count_launch();
   return e;
 }
 
 template <int N1, int N2>
 static cudaError_t dispatch(const TQArgs& a) {
+  if (a.zero) return a.bf16 ? launch<N1, N2, true, false, true>(a) : launch<N1, N2, false, false, true>(a);
   if (a.bf16) return a.y ? launch<N1, N2, true, true>(a) : launch<N1, N2, true, false>(a);
   return a.y ? launch<N1, N2, false, true>(a) : launch<N1, N2, false, false>(a);
 }

@@ -237,7 +237,8 @@ template <typename TIn, bool WRITE_Y>
 __global__ void __launch_bounds__(256)
 tq_simt_kernel(const TIn* __restrict__ x, int64_t T, int64_t ldx, int n1, int n2,
                const TIn* __restrict__ p1, const TIn* __restrict__ p2, float alpha,
-               uint8_t* __restrict__ q, float* __restrict__ scale, float* __restrict__ y_out) {
+               uint8_t* __restrict__ q, float* __restrict__ scale, float* __restrict__ y_out,
+               int8_t* __restrict__ zero) {
   extern __shared__ __align__(16) float fsm[];
   const int n = n1 * n2;
   float* v = fsm;        // [n1][n2]
@@ -254,7 +255,8 @@ tq_simt_kernel(const TIn* __restrict__ x, int64_t T, int64_t ldx, int n1, int n2
       z[i] = a;
     }
     __syncthreads();
-    float m = 0.f;
+    // sym: m = max |y|;  asym (zero != nullptr): hi = max(max y, 0), lo = max(-min y, 0)
+    float m = 0.f, hi = 0.f, lo = 0.f;
     // y[r][c] = sum_k P1[k][r] z[k][c]; each thread owns elements i = tid + j*blockDim
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const int r = i / n2, c = i % n2;
@@ -262,27 +264,51 @@ tq_simt_kernel(const TIn* __restrict__ x, int64_t T, int64_t ldx, int n1, int n2
       for (int k = 0; k < n1; ++k) a = fmaf(to_f32(p1[k * n1 + r]), z[k * n2 + c], a);
       v[i] = a;  // V no longer needed: reuse for Y
       m = fmaxf(m, fabsf(a));
+      hi = fmaxf(hi, a);
+      lo = fmaxf(lo, -a);
     }
-    m = warp_max(m);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      float mm = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.f;
-      mm = warp_max(mm);
-      if (threadIdx.x == 0) red[0] = mm;
-    }
-    __syncthreads();
-    m = red[0];
-    const float s = (m > 0.f) ? alpha * m / 7.0f : 1.0f;
-    const float inv_s = (m > 0.f) ? 7.0f / (alpha * m) : 0.0f;
+    auto block_max = [&](float x) {
+      x = warp_max(x);
+      __syncthreads();
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        float mm = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.f;
+        mm = warp_max(mm);
+        if (threadIdx.x == 0) red[0] = mm;
+      }
+      __syncthreads();
+      return red[0];
+    };
     if (WRITE_Y)
       for (int i = threadIdx.x; i < n; i += blockDim.x) y_out[t * n + i] = v[i];
-    for (int i = threadIdx.x; i < n / 2; i += blockDim.x) {
-      const int c0 = min(7, max(-8, __float2int_rn(v[2 * i] * inv_s)));
-      const int c1 = min(7, max(-8, __float2int_rn(v[2 * i + 1] * inv_s)));
-      q[t * (n / 2) + i] = uint8_t((c0 & 15) | ((c1 & 15) << 4));
+    if (zero == nullptr) {
+      m = block_max(m);
+      const float s = (m > 0.f) ? alpha * m / 7.0f : 1.0f;
+      const float inv_s = (m > 0.f) ? 7.0f / (alpha * m) : 0.0f;
+      for (int i = threadIdx.x; i < n / 2; i += blockDim.x) {
+        const int c0 = min(7, max(-8, __float2int_rn(v[2 * i] * inv_s)));
+        const int c1 = min(7, max(-8, __float2int_rn(v[2 * i + 1] * inv_s)));
+        q[t * (n / 2) + i] = uint8_t((c0 & 15) | ((c1 & 15) << 4));
+      }
+      if (threadIdx.x == 0) scale[t] = s;
+    } else {                                           // asymmetric (reading R19)
+      hi = block_max(hi);
+      lo = block_max(lo);
+      const float range = alpha * (hi + lo);           // (max(alpha max y, 0) - min(alpha min y, 0))
+      const float s = range > 0.f ? range / 15.0f : 1.0f;
+      const int zq = range > 0.f ? __float2int_rn(alpha * lo / s) : 0;
+      const float inv_s = range > 0.f ? 1.0f / s : 0.0f;
+      for (int i = threadIdx.x; i < n / 2; i += blockDim.x) {
+        const int c0 = min(15, max(0, __float2int_rn(v[2 * i] * inv_s) + zq)) - 8;
+        const int c1 = min(15, max(0, __float2int_rn(v[2 * i + 1] * inv_s) + zq)) - 8;
+        q[t * (n / 2) + i] = uint8_t((c0 & 15) | ((c1 & 15) << 4));
+      }
+      if (threadIdx.x == 0) {
+        scale[t] = s;
+        zero[t] = int8_t(zq - 8);
+      }
     }
-    if (threadIdx.x == 0) scale[t] = s;
     __syncthreads();
   }
 }
@@ -331,7 +357,7 @@ static cudaError_t launch_simt(const TQArgs& a) {
   const int64_t grid = std::min<int64_t>(a.T, int64_t(num_sms()) * 8);
   kern<<<dim3(unsigned(grid)), 256, smem, a.stream>>>(
       static_cast<const TIn*>(a.x), a.T, a.ldx, a.n1, a.n2, static_cast<const TIn*>(a.p1),
-      static_cast<const TIn*>(a.p2), a.alpha, a.q, a.scale, a.y);
+      static_cast<const TIn*>(a.p2), a.alpha, a.q, a.scale, a.y, a.zero);
   count_launch();
   return cudaGetLastError();
 }
@@ -362,8 +388,16 @@ cudaError_t tq_simt_launch(const TQArgs& a) {
 //         fp32 (the north_star's "warp-level FMAs where n1 and n2 are tiny": no fp16 intermediate,
 //         so no tie flips); the mma.sync kernel for the remaining instantiated shapes (128 x 224).
 // impl 1: mma.sync where instantiated, else CUDA cores;  impl 2: CUDA cores.
+bool tq_asym_supported(const TQArgs& a) {
+  return (tq_impl() == 0 && tq_tc05_supported(a)) || tq_simt_supported(a.n1, a.n2);
+}
+
 cudaError_t transform_quant_launch(const TQArgs& a) {
   const int impl = tq_impl();
+  if (a.zero) {                          // asymmetric: tcgen05 kernel, else the CUDA-core kernel
+    if (impl == 0 && tq_tc05_supported(a)) return tq_tc05_launch(a);
+    return tq_simt_launch(a);
+  }
   const bool tc_shape = (a.n1 % 16 == 0) && (a.n2 % 16 == 0);
   if (impl == 0 && tq_tc05_supported(a)) return tq_tc05_launch(a);
   if (impl == 0 && int64_t(a.n1) * a.n2 <= 4096 && tq_simt_supported(a.n1, a.n2)) return tq_simt_launch(a);

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_status_strings():
     lib = fq.load()
-    assert fq.fq_abi_version() == 1
+    assert fq.fq_abi_version() == 2
     for s in range(5):
         assert lib.fq_status_string(s).startswith(b"FQ_")
     assert lib.fq_status_string(99) == b"unknown fq_status"
@@ -63,9 +63,10 @@ def test_transform_quant_validation():
     assert tq(alpha=1.5) == _lib.FQ_EINVAL
     assert tq(alpha=float("nan")) == _lib.FQ_EINVAL
     assert tq(dt=7) == _lib.FQ_EINVAL
-    assert tq(qmode=1) == _lib.FQ_ENOTSUP                 # asymmetric mode reserved (NEXT-1)
+    assert tq(qmode=1) == _lib.FQ_EINVAL                  # asymmetric mode needs the zero buffer
+    assert tq(qmode=1, T=0, zero=A16) == _lib.FQ_OK
     assert tq(qmode=3) == _lib.FQ_EINVAL
-    assert tq(zero=A16) == _lib.FQ_EINVAL
+    assert tq(zero=A16) == _lib.FQ_EINVAL                 # symmetric mode takes no zero buffer
     assert tq(x=None) == _lib.FQ_EINVAL
     assert tq(q=None) == _lib.FQ_EINVAL
     assert tq(T=-1) == _lib.FQ_EINVAL
@@ -91,8 +92,13 @@ def test_w4a4_linear_validation():
     assert gemm(qa=None) == _lib.FQ_EINVAL
     assert gemm(sa=None) == _lib.FQ_EINVAL
     assert gemm(dt=5) == _lib.FQ_EINVAL
-    assert gemm(za=A16) == _lib.FQ_ENOTSUP
-    assert gemm(cs=A16) == _lib.FQ_ENOTSUP
+    assert gemm(za=A16) == _lib.FQ_EINVAL                 # zero points without colsum_w
+    assert gemm(cs=A16) == _lib.FQ_EINVAL                 # colsum_w without zero points
+    assert gemm(za=A16, cs=MIS) == _lib.FQ_ESHAPE
+    lib0 = fq.load()
+    assert lib0.fq_weight_colsum(None, 4, 64, A16, None) == _lib.FQ_EINVAL
+    assert lib0.fq_weight_colsum(A16, 4, 63, A16, None) == _lib.FQ_ESHAPE
+    assert lib0.fq_weight_colsum(A16, 0, 64, A16, None) == _lib.FQ_OK
     assert gemm(y=MIS) == _lib.FQ_ESHAPE
     assert gemm(K=262144) == _lib.FQ_ENOTSUP
     lib = fq.load()

@@ -278,3 +278,66 @@ def test_gpu_weight_prep_matches_oracle():
     deq = O.dequantize_rows(O.unpack_int4(np_of(qw)), np_of(sw).astype(np.float64))
     step = np_of(sw).astype(np.float64)[:, None]
     assert np.all(np.abs(deq - wp) <= 0.5 * step + 2e-2 * np.abs(wp).max(1, keepdims=True))
+
+
+# ---------------------------------------------------------------- asymmetric mode (NEXT-1, R19)
+@pytest.mark.parametrize("n1,n2", [(64, 64), (64, 128), (112, 128), (16, 32), (8, 8)])
+@pytest.mark.parametrize("alpha", [1.0, 0.9])
+@pytest.mark.parametrize("tdtype", [torch.float16, torch.bfloat16])
+def test_transform_quant_asym_vs_oracle(n1, n2, alpha, tdtype):
+    """FQ_ASYM: codes q in [0, 15] (stored q - 8), zero points z (stored z - 8) and scales against
+    the oracle.  Compared on the grid index q - z (a +-1 zero-point flip at a near-tie of
+    -lo/s shifts every code of its token but not q - z); mismatches only at near-ties of y/s or
+    at the clamp, by +-1, in <= 0.1% of the elements."""
+    T = 203
+    x, p1, p2 = make_inputs(T, n1, n2, seed=n1 * 3 + n2, tdtype=tdtype)
+    q, s, z = fq.transform_quant_asym(x.to(DEV), n1, n2, p1.to(DEV), p2.to(DEV), alpha)
+    torch.cuda.synchronize()
+    qo, so, zo, yo = O.transform_quant_asym(x.float().numpy(), p1.float().numpy(), p2.float().numpy(), alpha)
+    qg = O.unpack_int4(np_of(q)).astype(np.int64) + 8
+    zg = np_of(z).astype(np.int64) + 8
+    sg = np_of(s).astype(np.float64)
+    assert np.all((qg >= 0) & (qg <= 15)) and np.all((zg >= 0) & (zg <= 15))
+    assert np.max(np.abs(sg - so) / so) <= parity.SCALE_REL
+    zt = np.abs(-np.minimum(alpha * yo.min(1), 0) / so - np.floor(-np.minimum(alpha * yo.min(1), 0) / so) - 0.5)
+    assert np.all((zg == zo) | (zt <= parity.TAU))
+    d = (qg - zg[:, None]) - (qo.astype(np.int64) - zo[:, None])
+    v = yo / so[:, None]
+    tie = np.abs(v - np.floor(v) - 0.5) <= parity.TAU
+    clamp = (qo == 0) | (qo == 15) | (qg == 0) | (qg == 15)
+    mism = d != 0
+    assert np.all(np.abs(d) <= 1)
+    assert np.all(tie[mism] | clamp[mism])
+    assert mism.mean() <= parity.MISMATCH_FRAC
+
+
+def test_weight_colsum_exact():
+    qw = synth.random_codes(777, 4096, seed=5)
+    cs = fq.weight_colsum(to_dev(O.pack_int4(qw)))
+    torch.cuda.synchronize()
+    assert np.array_equal(np_of(cs).astype(np.int64), qw.astype(np.int64).sum(1))
+
+
+@pytest.mark.parametrize("out_dtype", [torch.float16, torch.bfloat16])
+def test_asym_linear_vs_oracle(out_dtype):
+    """Asymmetric activations through the GEMM: Y = s_a s_w (acc - (z - 8) colsum_w) equals the
+    oracle's dequantized product of the GPU's own codes (per token, fp16/bf16 output rounding),
+    and the whole chain stays within the end-to-end Frobenius bar of the oracle's codes."""
+    T, n1, n2, N = 1037, 64, 64, 1544
+    x, p1, p2 = make_inputs(T, n1, n2, seed=17)
+    w = synth.weights(N, n1 * n2, seed=17)
+    qw, sw, _ = O.prepare_weight(w, p1.float().numpy(), p2.float().numpy(), 1.0)
+    sw32 = sw.astype(np.float32)
+    qw_d = to_dev(O.pack_int4(qw))
+    q, s, z = fq.transform_quant_asym(x.to(DEV), n1, n2, p1.to(DEV), p2.to(DEV), 0.9)
+    cs = fq.weight_colsum(qw_d)
+    y = fq.w4a4_linear(q, s, qw_d, to_dev(sw32), out_dtype, za=z, colsum_w=cs)
+    torch.cuda.synchronize()
+    qg = O.unpack_int4(np_of(q)).astype(np.int64) + 8
+    zg = np_of(z).astype(np.int64) + 8
+    same = O.w4a4_linear_asym(qg, np_of(s).astype(np.float64), zg, qw, sw32.astype(np.float64))
+    ulp = 2.0 ** -10 if out_dtype == torch.float16 else 2.0 ** -7
+    assert np.all(np.abs(np_of(y) - same) <= ulp * np.abs(same) + 1e-6)
+    qo, so, zo, _ = O.transform_quant_asym(x.float().numpy(), p1.float().numpy(), p2.float().numpy(), 0.9)
+    ref = O.w4a4_linear_asym(qo, so, zo, qw, sw32.astype(np.float64))
+    parity.check_output(np_of(y), ref, same, label="asym linear")
