@@ -47,10 +47,10 @@ FQ_DEVICE void trace(int) {}
 
 constexpr int BM = 256, BM_CTA = 128;     // tokens per pair tile / per CTA
 constexpr int BN = 192, BN_CTA = 96;      // features per pair tile / B rows per CTA
-constexpr int BK = 128;                   // int8 K per stage
+constexpr int BK = 256;                   // int8 K per stage (two 128-byte swizzle atoms)
 constexpr int UK = 32;
-constexpr int STAGES = 4;
-constexpr int PSTAGES = 8;                // packed A+B ring (TMA)
+constexpr int STAGES = 2;                 // MMA stages (TMEM A / widened smem B)
+constexpr int PSTAGES = 4;                // packed A+B ring (TMA)
 constexpr int B_BYTES = BN_CTA * BK;      // 12 KB per stage per CTA (widened)
 constexpr int BP_BYTES = BN_CTA * BK / 2; // 6 KB packed B per ring stage
 constexpr int AP_BYTES = BM_CTA * BK / 2; // 8 KB packed A per ring stage
@@ -59,6 +59,7 @@ constexpr int EPI_BYTES = 32 * 128;       // per epilogue warp: 32 rows x 64 fp1
 constexpr int A_COLS = BK / 4;            // TMEM columns per A stage
 constexpr int TMEM_ACC0 = 0;              // two accumulators [0, 2*BN)
 constexpr int TMEM_A0 = 2 * BN;           // A stages [2*BN, 2*BN + STAGES*A_COLS) = [384, 512)
+constexpr int B_ATOM = BN_CTA * 128;      // one 128-byte K atom of the widened B stage
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_EPI_WARPS = 4, MMA_WARP = 4;
 constexpr int A_WARP0 = 5, NUM_A_WARPS = 8;     // 2 warps per TMEM lane quarter (each half of K)
@@ -66,12 +67,13 @@ constexpr int B_WARP0 = 13, NUM_B_WARPS = 6;
 constexpr int NUM_CONV_WARPS = NUM_A_WARPS + NUM_B_WARPS;
 constexpr int TMA_WARP = B_WARP0 + NUM_B_WARPS;
 constexpr int THREADS = (TMA_WARP + 1) * 32;
-constexpr int B_TASKS = BN_CTA * 4 / (NUM_B_WARPS * 32);    // 16-byte packed chunks per B thread
+constexpr int B_CHUNKS = BK / 32;                          // 16-byte packed chunks per weight row
+constexpr int B_TASKS = BN_CTA * B_CHUNKS / (NUM_B_WARPS * 32);
 constexpr size_t SMEM_BYTES =
     size_t(STAGES) * B_BYTES + size_t(PSTAGES) * P_BYTES + NUM_EPI_WARPS * EPI_BYTES + 1024 + 512;
 constexpr uint32_t IDESC = tc::idesc_i8(BM, BN);
 static_assert(TMEM_A0 + STAGES * A_COLS <= TMEM_COLS, "TMEM budget");
-static_assert(B_TASKS * NUM_B_WARPS * 32 == BN_CTA * 4, "B task split");
+static_assert(B_TASKS * NUM_B_WARPS * 32 == BN_CTA * B_CHUNKS, "B task split");
 
 FQ_DEVICE void widen8(uint32_t p, uint32_t& lo, uint32_t& hi) {   // 8 nibbles -> 8 x (16 q) int8
   lo = (p << 4) & 0xF0F0F0F0u;
@@ -216,14 +218,14 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     cv.init(sc);
     int job = 0;
     if (is_a) {
-      // row r_local of the CTA's 128 activation rows, K-half khalf of the 128-element K-block:
-      // 32 packed bytes = chunks (2 khalf, 2 khalf + 1) of the SWIZZLE_64B row
+      // row r_local of the CTA's 128 activation rows, K-half khalf of the 256-element K-block:
+      // 64 packed bytes = chunks 4 khalf .. 4 khalf + 3 of the SWIZZLE_128B row
       const int aw = warp - A_WARP0;
       const int quarter = warp & 3, khalf = aw >> 2;
       const int r_local = quarter * 32 + lane;                   // == TMEM lane of this row
       const uint32_t tl = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(TMEM_A0 + khalf * (A_COLS / 2));
-      const uint32_t sw = uint32_t((r_local >> 1) & 3);
-      const uint32_t roff = uint32_t(r_local * 64);
+      const uint32_t sw = uint32_t(r_local & 7);
+      const uint32_t roff = uint32_t(r_local * 128);
       // Two K-blocks per iteration: both are converted and their tcgen05.st issued before one
       // tcgen05.wait::st + signal, which halves the per-K-block synchronisation latency (the
       // A path is latency-bound, not throughput-bound).
@@ -232,18 +234,16 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         tc::mbar_wait(&empty[st], ph ^ 1);
         tc::mbar_wait(&pfull[sp], (jb / PSTAGES) & 1);
         const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES) + roff;
-        const uint4 p0 = tc::lds128(src + ((uint32_t(2 * khalf) ^ sw) << 4));
-        const uint4 p1 = tc::lds128(src + ((uint32_t(2 * khalf + 1) ^ sw) << 4));
-        uint32_t w[16];
-        widen8(p0.x, w[0], w[1]);
-        widen8(p0.y, w[2], w[3]);
-        widen8(p0.z, w[4], w[5]);
-        widen8(p0.w, w[6], w[7]);
-        widen8(p1.x, w[8], w[9]);
-        widen8(p1.y, w[10], w[11]);
-        widen8(p1.z, w[12], w[13]);
-        widen8(p1.w, w[14], w[15]);
-        tmem_st16(tl + uint32_t(st * A_COLS), w);
+        uint32_t w[32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint4 pk = tc::lds128(src + ((uint32_t(4 * khalf + c) ^ sw) << 4));
+          widen8(pk.x, w[8 * c + 0], w[8 * c + 1]);
+          widen8(pk.y, w[8 * c + 2], w[8 * c + 3]);
+          widen8(pk.z, w[8 * c + 4], w[8 * c + 5]);
+          widen8(pk.w, w[8 * c + 6], w[8 * c + 7]);
+        }
+        tc::tmem_st32(tl + uint32_t(st * A_COLS), w);
         // release the ring slot only after the loaded values were consumed (the tcgen05.st reads
         // them): mbarrier.arrive does not wait for an outstanding ld.shared, so an arrive right
         // after the loads lets the TMA overwrite the slot before a delayed load has read it
@@ -259,7 +259,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         ++job;
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
         cv.next(sc);
-        const bool two = cv.valid;
+        const bool two = STAGES > 2 && cv.valid;         // batch two K-blocks only with spare stages
         const int st1 = stage;
         if (two) {
           prep(job, stage, phase);
@@ -290,7 +290,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
         for (int i = 0; i < B_TASKS; ++i) {
           const int task = ct + i * NUM_B_WARPS * 32;
-          const uint4 pk = tc::lds128(src + uint32_t(task * 16));      // row task/4, bytes [16c, 16c+16)
+          const uint4 pk = tc::lds128(src + uint32_t(task * 16));      // row task/8, packed chunk task%8
           widen8(pk.x, o[i][0], o[i][1]);
           widen8(pk.y, o[i][2], o[i][3]);
           widen8(pk.z, o[i][4], o[i][5]);
@@ -298,10 +298,11 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         }
 #pragma unroll
         for (int i = 0; i < B_TASKS; ++i) {
-          const int task = ct + i * NUM_B_WARPS * 32, rl = task >> 2, c = task & 3;
-          const uint32_t rowp = dst + uint32_t(rl * 128);
-          tc::sts128(rowp + uint32_t(((2 * c) ^ (rl & 7)) << 4), o[i][0], o[i][1], o[i][2], o[i][3]);
-          tc::sts128(rowp + uint32_t(((2 * c + 1) ^ (rl & 7)) << 4), o[i][4], o[i][5], o[i][6], o[i][7]);
+          const int task = ct + i * NUM_B_WARPS * 32, rl = task / B_CHUNKS, c = task % B_CHUNKS;
+          const uint32_t rowp = dst + uint32_t((c >> 2) * B_ATOM + rl * 128);
+          const int cc = c & 3;
+          tc::sts128(rowp + uint32_t(((2 * cc) ^ (rl & 7)) << 4), o[i][0], o[i][1], o[i][2], o[i][3]);
+          tc::sts128(rowp + uint32_t(((2 * cc + 1) ^ (rl & 7)) << 4), o[i][4], o[i][5], o[i][6], o[i][7]);
         }
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&pempty[sp]);               // packed B consumed (stored above)
@@ -333,7 +334,8 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           const uint32_t b0 = smem_u32(smem + size_t(stage) * B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k)
-            tc::mma_ts_i8_pair(tmem_d, a_t + k * (UK / 4), tc::sdesc_sw128(b0 + k * UK, 16, 1024), IDESC,
+            tc::mma_ts_i8_pair(tmem_d, a_t + k * (UK / 4),
+                               tc::sdesc_sw128(b0 + (k >> 2) * B_ATOM + (k & 3) * UK, 16, 1024), IDESC,
                                (kb | k) != 0);
           tc::mma_commit_pair(&empty[stage], 0x3);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -496,7 +498,7 @@ cudaError_t gemm_pair_launch(const GemmArgs& a) {
     const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.T)};
     const uint64_t strides[1] = {uint64_t(a.K / 2)};
     const uint32_t box[2] = {BK / 2, BM_CTA};
-    if (!tmap_encode(&ma, a.qa, 1, 2, dims, strides, box, TMAP_SW64)) return cudaErrorInvalidValue;
+    if (!tmap_encode(&ma, a.qa, 1, 2, dims, strides, box, TMAP_SW128)) return cudaErrorInvalidValue;
   }
   {
     const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.N)};
