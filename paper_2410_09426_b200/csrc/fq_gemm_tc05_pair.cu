@@ -46,11 +46,23 @@ FQ_DEVICE void trace(int) {}
 #endif
 
 constexpr int BM = 256, BM_CTA = 128;     // tokens per pair tile / per CTA
-constexpr int BN = 192, BN_CTA = 96;      // features per pair tile / B rows per CTA
+#ifndef FQ_GEMM_BN
+#define FQ_GEMM_BN 192
+#endif
+#ifndef FQ_GEMM_STAGES
+#define FQ_GEMM_STAGES 2
+#endif
+#ifndef FQ_GEMM_PSTAGES
+#define FQ_GEMM_PSTAGES 4
+#endif
+#ifndef FQ_GEMM_BWARPS
+#define FQ_GEMM_BWARPS 6
+#endif
+constexpr int BN = FQ_GEMM_BN, BN_CTA = BN / 2;   // features per pair tile / B rows per CTA
 constexpr int BK = 256;                   // int8 K per stage (two 128-byte swizzle atoms)
 constexpr int UK = 32;
-constexpr int STAGES = 2;                 // MMA stages (TMEM A / widened smem B)
-constexpr int PSTAGES = 4;                // packed A+B ring (TMA)
+constexpr int STAGES = FQ_GEMM_STAGES;    // MMA stages (TMEM A / widened smem B)
+constexpr int PSTAGES = FQ_GEMM_PSTAGES;  // packed A+B ring (TMA)
 constexpr int B_BYTES = BN_CTA * BK;      // 12 KB per stage per CTA (widened)
 constexpr int BP_BYTES = BN_CTA * BK / 2; // 6 KB packed B per ring stage
 constexpr int AP_BYTES = BM_CTA * BK / 2; // 8 KB packed A per ring stage
@@ -63,7 +75,7 @@ constexpr int B_ATOM = BN_CTA * 128;      // one 128-byte K atom of the widened 
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_EPI_WARPS = 4, MMA_WARP = 4;
 constexpr int A_WARP0 = 5, NUM_A_WARPS = 8;     // 2 warps per TMEM lane quarter (each half of K)
-constexpr int B_WARP0 = 13, NUM_B_WARPS = 6;
+constexpr int B_WARP0 = 13, NUM_B_WARPS = FQ_GEMM_BWARPS;
 constexpr int NUM_CONV_WARPS = NUM_A_WARPS + NUM_B_WARPS;
 constexpr int TMA_WARP = B_WARP0 + NUM_B_WARPS;
 constexpr int THREADS = (TMA_WARP + 1) * 32;
