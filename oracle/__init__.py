@@ -7,4 +7,6 @@ from .flatquant_oracle import *  # noqa: F401,F403
 from .flatquant_oracle import (choose_decomposition, kron_transform, kron_matrix, quantize_rows,
                                dequantize_rows, pack_int4, unpack_int4, transform_quant,
                                transform_weight, prepare_weight, int_gemm, int_gemm_bruteforce,
-                               dequant, w4a4_linear, flatquant_linear, near_tie_mask)
+                               dequant, w4a4_linear, flatquant_linear, near_tie_mask,
+                               quantize_rows_asym, dequantize_rows_asym, transform_quant_asym,
+                               w4a4_linear_asym, kv_quant)

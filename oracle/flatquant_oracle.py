@@ -179,6 +179,27 @@ def w4a4_linear_asym(qa, sa, za, qw, sw) -> np.ndarray:
     return dequant(int_gemm(qa_c, qw), sa, sw)
 
 
+
+# ---------------------------------------------------------------------------
+# NEXT-3: KV-cache quantization.  PAPER.md:291-297 §3.2: P_h / P_v "transform the key and value
+# cache head by head" (P_h a full head_dim x head_dim matrix; P_v is merged into the weights, so
+# values are quantized untransformed, i.e. P = I).  PAPER.md:369 §4.1 and 1101-1104 App. "KV
+# Cache Quantization": "group-wise asymmetric quantization with the size of 128", which "matches
+# the head dimension": one group = one head vector (reading R20).  The asymmetric
+# quantizer is R19's (quantize_rows_asym); alpha is the KV clipping threshold.
+# ---------------------------------------------------------------------------
+def kv_quant(kv, p_h, alpha: float = 1.0, rounding: str = "half_even"):
+    """kv [R, D] head vectors (R = tokens x heads), p_h [D, D].  y_r = kv_r P_h (row vector times
+    matrix), then per-row asymmetric INT4.  Returns (codes int8 [0,15] [R, D], scales [R],
+    zeros int64 [R], y float64 [R, D])."""
+    kv = _f64(kv)
+    p_h = _f64(p_h)
+    if p_h.shape != (kv.shape[1], kv.shape[1]):
+        raise ValueError("p_h must be [D, D] with D = kv.shape[1]")
+    y = kv @ p_h
+    q, s, z = quantize_rows_asym(y, alpha, rounding)
+    return q, s, z, y
+
 # ---------------------------------------------------------------------------
 # a5: packing (R7): byte i of a row holds element 2i (low nibble) and 2i+1.
 # ---------------------------------------------------------------------------

@@ -318,3 +318,47 @@ def test_asym_linear_equals_dequantized_product():
     acc8 = O.int_gemm(qa.astype(np.int64) - 8, qw)
     corr = (za - 8)[:, None] * qw.astype(np.int64).sum(1)[None, :]
     assert np.array_equal(acc8 - corr, O.int_gemm(qa.astype(np.int64) - za[:, None], qw))
+
+
+# ---------------------------------------------------------------- KV cache (NEXT-3, R20)
+def test_kv_quant_worked_example():
+    """PAPER.md:293 (keys transformed head by head, row vector times P_h) + R19's quantizer.
+    Non-symmetric P_h = [[1, 2], [3, 4]] so that P_h vs P_h^T is caught:
+    k = [1, 0] -> y = [1, 2]: s = 2/15, z = 0, codes [rint(7.5) = 8, 15];
+    k = [0, -1] -> y = [-3, -4]: s = 4/15, z = 15, codes [rint(-11.25) + 15 = 4, 0]."""
+    q, s, z, y = O.kv_quant(np.array([[1.0, 0.0], [0.0, -1.0]]), np.array([[1.0, 2.0], [3.0, 4.0]]))
+    assert y.tolist() == [[1.0, 2.0], [-3.0, -4.0]]
+    assert np.allclose(s, [2 / 15, 4 / 15]) and z.tolist() == [0, 15]
+    assert q.tolist() == [[8, 15], [4, 0]]
+
+
+def test_kv_quant_orthogonal_roundtrip_bound():
+    """With an orthogonal P_h (q and k are both rotated, q k^T = (q P_h)(k P_h)^T),
+    dequantizing and undoing the rotation recovers each head vector within the quantizer's half
+    step: ||deq(k P_h) P_h^T - k||_2 <= sqrt(D) s / 2 per head vector (alpha = 1, no clipping),
+    and the attention logits of a rotated query move by at most ||q||_2 sqrt(D) s / 2."""
+    g = np.random.default_rng(3)
+    for D in (64, 128):
+        ph, _ = np.linalg.qr(g.standard_normal((D, D)))
+        k = g.standard_normal((50, D)) * g.uniform(0.1, 20, size=(50, 1))
+        q, s, z, _ = O.kv_quant(k, ph, 1.0)
+        rec = O.dequantize_rows_asym(q, s, z) @ ph.T
+        err = np.linalg.norm(rec - k, axis=1)
+        assert np.all(err <= np.sqrt(D) * s / 2 + 1e-9)
+        qry = g.standard_normal((3, D))
+        logits = (qry @ ph) @ O.dequantize_rows_asym(q, s, z).T
+        bound = np.linalg.norm(qry, axis=1)[:, None] * (np.sqrt(D) * s / 2)[None, :]
+        assert np.all(np.abs(logits - qry @ k.T) <= bound + 1e-9)
+
+
+def test_kv_quant_is_unit_kronecker():
+    """A head vector transform is the Kronecker transform with n1 = 1 (P = [1] (x) P_h):
+    kv_quant equals transform_quant_asym with p1 = [[1]]: identical codes and zero points, scales
+    and transformed values equal up to float64 summation order."""
+    g = np.random.default_rng(8)
+    kv = g.standard_normal((33, 64))
+    ph = g.standard_normal((64, 64))
+    a = O.kv_quant(kv, ph, 0.9)
+    b = O.transform_quant_asym(kv, np.ones((1, 1)), ph, 0.9)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[2], b[2])
+    assert np.allclose(a[1], b[1], rtol=1e-12, atol=0) and np.allclose(a[3], b[3], rtol=1e-12, atol=1e-12)
