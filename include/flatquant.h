@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define FQ_ABI_VERSION 2   /* 2: FQ_ASYM + fq_weight_colsum */
+#define FQ_ABI_VERSION 3   /* 2: FQ_ASYM + fq_weight_colsum; 3: fq_kv_quant */
 
 typedef enum {
   FQ_OK = 0,
@@ -138,6 +138,26 @@ fq_status fq_flatquant_linear_host(const void* x_host, void* x_dev, int32_t x_dt
                                    const void* p2, float alpha, const uint8_t* qw,
                                    const float* sw, int32_t N, void* y_host, void* y_dev,
                                    int32_t y_dtype, uint8_t* q_ws, float* s_ws, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * fq_kv_quant -- KV-cache quantization: per-head transform and
+ * group-wise asymmetric INT4 with one group per head vector.
+ *   y_r = kv_r . P_h   (§3.2: P_h transforms the keys head by head; values
+ *                       use P = I since P_v is merged into the weights)
+ *   s_r = alpha (hi - lo) / 15, z_r = rint(-alpha lo / s_r), q = clamp(rint(y / s) + z, 0, 15)
+ *   with hi = max(max_j y_rj, 0), lo = min(min_j y_rj, 0) (reading R19); group size =
+ *   head_dim ("group-wise asymmetric ... size of 128" = head dim).
+ *   kv     [R, head_dim] fp16/bf16 (kv_dtype), row stride ldkv elements; R = tokens x heads.
+ *   p_h    [head_dim, head_dim] row-major, same dtype as kv (identity for values).
+ *   alpha  KV clipping threshold in (0, 1].
+ *   q      [R, head_dim/2] uint8 packed nibbles q - 8 (output).   scale [R] fp32 (output).
+ *   zero   [R] int8, z - 8 (output).       Dequantization: s (q - z) = s ((q-8) - (z-8)).
+ *   head_dim 64 or 128 (FQ_ENOTSUP otherwise); kv, p_h, q 16-byte aligned and ldkv * 2 a
+ *   multiple of 16 (FQ_ESHAPE otherwise).  One tcgen05 kernel launch.
+ * ------------------------------------------------------------------------------------- */
+fq_status fq_kv_quant(const void* kv, int32_t kv_dtype, int64_t R, int64_t ldkv,
+                      int32_t head_dim, const void* p_h, float alpha, uint8_t* q,
+                      float* scale, int8_t* zero, void* stream);
 
 /* ---------------------------------------------------------------------------------------
  * Helpers

@@ -34,6 +34,7 @@ SIGNATURES = {
                                    _vp, _vp, _vp]),
     "fq_flatquant_linear_host": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp, _vp, _f32, _vp, _vp, _i32, _vp,
                                         _vp, _i32, _vp, _vp, _vp]),
+    "fq_kv_quant": (_i32, [_vp, _i32, _i64, _i64, _i32, _vp, _f32, _vp, _vp, _vp, _vp]),
     "fq_choose_decomposition": (_i32, [_i64, _c.POINTER(_i32), _c.POINTER(_i32)]),
     "fq_set_gemm_impl": (_i32, [_i32]),
     "fq_set_tq_impl": (_i32, [_i32]),

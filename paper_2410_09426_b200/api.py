@@ -15,7 +15,7 @@ from ._lib import FQ_BF16, FQ_F16, FQ_SYM, check, load
 
 __all__ = [
     "fq_transform_quant", "fq_transform_f32", "fq_w4a4_linear", "fq_w4a4_gemm_i32", "fq_flatquant_linear",
-    "fq_weight_colsum", "weight_colsum", "transform_quant_asym",
+    "fq_weight_colsum", "weight_colsum", "transform_quant_asym", "fq_kv_quant", "kv_quant",
     "fq_flatquant_linear_host", "fq_choose_decomposition", "fq_set_gemm_impl", "fq_set_tq_impl", "fq_launch_count",
     "fq_abi_version", "transform_quant", "transform_f32", "w4a4_linear", "w4a4_gemm_i32", "prepare_weight",
     "flatquant_linear",
@@ -82,6 +82,26 @@ def fq_weight_colsum(qw, colsum, K=None, stream=None):
     _cuda(qw, colsum)
     K = qw.shape[1] * 2 if K is None else K
     check("fq_weight_colsum", load().fq_weight_colsum(_ptr(qw), qw.shape[0], K, _ptr(colsum), _stream(stream)))
+
+
+def fq_kv_quant(kv, p_h, alpha, q, scale, zero, stream=None):
+    """kv [R, D] (row stride kv.stride(0)), p_h [D, D]; outputs q [R, D/2], scale [R], zero [R]."""
+    _cuda(kv, p_h, q, scale, zero)
+    assert kv.dim() == 2 and kv.stride(1) == 1
+    st = load().fq_kv_quant(_ptr(kv), _fq_dtype(kv.dtype), kv.shape[0], kv.stride(0), kv.shape[1], _ptr(p_h),
+                            float(alpha), _ptr(q), _ptr(scale), _ptr(zero), _stream(stream))
+    check("fq_kv_quant", st)
+
+
+def kv_quant(kv, p_h, alpha=1.0, stream=None):
+    """KV-cache quantization: returns (q packed [R, D/2] holding q - 8,
+    scale [R], zero [R] int8 holding z - 8) of kv_r P_h, one asymmetric group per head vector."""
+    R, D = kv.shape
+    q = torch.empty((R, D // 2), dtype=torch.uint8, device=kv.device)
+    s = torch.empty((R,), dtype=torch.float32, device=kv.device)
+    z = torch.empty((R,), dtype=torch.int8, device=kv.device)
+    fq_kv_quant(kv, p_h, alpha, q, s, z, stream=stream)
+    return q, s, z
 
 
 def fq_flatquant_linear(x, n1, n2, p1, p2, alpha, qw, sw, y, q_ws, s_ws, stream=None):

@@ -225,6 +225,30 @@ fq_status fq_weight_colsum(const uint8_t* qw, int32_t N, int32_t K, int32_t* col
   return cuda_status(weight_colsum_launch(qw, N, K, colsum, static_cast<cudaStream_t>(stream)));
 }
 
+fq_status fq_kv_quant(const void* kv, int32_t kv_dtype, int64_t R, int64_t ldkv, int32_t head_dim,
+                      const void* p_h, float alpha, uint8_t* q, float* scale, int8_t* zero, void* stream) {
+  if (kv_dtype != FQ_F16 && kv_dtype != FQ_BF16) return FQ_EINVAL;
+  if (R < 0 || head_dim < 1 || ldkv < head_dim) return FQ_EINVAL;
+  if (!(alpha > 0.f && alpha <= 1.f)) return FQ_EINVAL;
+  if (R == 0) return FQ_OK;
+  if (!kv || !p_h || !q || !scale || !zero) return FQ_EINVAL;
+  if (head_dim != 64 && head_dim != 128) return FQ_ENOTSUP;
+  KVArgs a{};
+  a.x = kv;
+  a.R = R;
+  a.ldx = ldkv;
+  a.D = head_dim;
+  a.p = p_h;
+  a.alpha = alpha;
+  a.q = q;
+  a.scale = scale;
+  a.zero = zero;
+  a.bf16 = kv_dtype == FQ_BF16;
+  a.stream = static_cast<cudaStream_t>(stream);
+  if (!kv_quant_supported(a)) return FQ_ESHAPE;
+  return cuda_status(kv_quant_launch(a));
+}
+
 fq_status fq_choose_decomposition(int64_t n, int32_t* n1, int32_t* n2) {
   if (n < 1 || !n1 || !n2) return FQ_EINVAL;
   if (n > INT32_MAX) return FQ_ENOTSUP;

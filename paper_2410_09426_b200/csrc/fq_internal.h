@@ -45,6 +45,19 @@ struct GemmArgs {
   cudaStream_t stream;
 };
 
+struct KVArgs {     // KV-cache quantization (fq_kv_quant)
+  const void* x;    // [R, D] head vectors, row stride ldx elements
+  int64_t R, ldx;
+  int D;
+  const void* p;    // P_h [D, D] row-major, same dtype as x
+  float alpha;
+  uint8_t* q;       // [R, D/2]
+  float* scale;     // [R]
+  int8_t* zero;     // [R] z - 8
+  bool bf16;
+  cudaStream_t stream;
+};
+
 int num_sms();
 void count_launch();
 bool pdl_enabled();      // FQ_PDL=0 in the environment disables programmatic dependent launch
@@ -95,5 +108,7 @@ cudaError_t gemm_tc05_launch(const GemmArgs& a);     // tcgen05 kind::i8, single
 bool gemm_tc05_supported(const GemmArgs& a);
 cudaError_t gemm_pair_launch(const GemmArgs& a);     // tcgen05 kind::i8, CTA pair (cta_group::2)
 bool gemm_pair_supported(const GemmArgs& a);
+bool kv_quant_supported(const KVArgs& a);            // tcgen05 KV-cache kernel
+cudaError_t kv_quant_launch(const KVArgs& a);
 
 }  // namespace fq

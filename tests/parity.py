@@ -63,3 +63,29 @@ def check_output(y_gpu, y_ora, y_same_codes=None, label=""):
     assert fro <= OUT_REL, f"{label} output rel Frobenius {fro:.3e}"
     assert tok <= OUT_REL, f"{label} output per-token rel {tok:.3e} (given identical codes)"
     return {"out_rel_fro": float(fro), "out_rel_tok": float(tok)}
+
+
+def check_asym(q_packed, s_gpu, z_gpu, y_ora, alpha, q_ora, s_ora, z_ora, tau=TAU, label=""):
+    """Asymmetric codes (R19): q in [0, 15] stored as q - 8, zero points stored as z - 8, scales.
+    Compared on the grid index q - z (a +-1 zero-point flip at a near-tie of -lo/s shifts every
+    code of its group but not q - z); mismatches only at near-ties of y/s or at the clamp, by
+    +-1, in <= MISMATCH_FRAC of the elements.  Returns the mismatch fraction."""
+    qg = O.unpack_int4(np.asarray(q_packed)).astype(np.int64) + 8
+    zg = np.asarray(z_gpu).astype(np.int64) + 8
+    sg = np.asarray(s_gpu, np.float64)
+    assert np.all((qg >= 0) & (qg <= 15)) and np.all((zg >= 0) & (zg <= 15)), label
+    srel = np.max(np.abs(sg - s_ora) / s_ora, initial=0.0)
+    assert srel <= SCALE_REL, f"{label} scale rel {srel:.3e}"
+    lo = -np.minimum(alpha * y_ora.min(1), 0) / s_ora
+    zt = np.abs(lo - np.floor(lo) - 0.5)
+    assert np.all((zg == z_ora) | (zt <= tau)), f"{label} zero points"
+    d = (qg - zg[:, None]) - (np.asarray(q_ora, np.int64) - np.asarray(z_ora, np.int64)[:, None])
+    v = y_ora / s_ora[:, None]
+    tie = np.abs(v - np.floor(v) - 0.5) <= tau
+    clamp = (q_ora == 0) | (q_ora == 15) | (qg == 0) | (qg == 15)
+    mism = d != 0
+    assert np.all(np.abs(d) <= 1), f"{label} code off by more than 1"
+    assert np.all(tie[mism] | clamp[mism]), f"{label} mismatch away from a near-tie"
+    frac = float(mism.mean()) if mism.size else 0.0
+    assert frac <= MISMATCH_FRAC, f"{label} mismatch fraction {frac:.2e}"
+    return frac

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_status_strings():
     lib = fq.load()
-    assert fq.fq_abi_version() == 2
+    assert fq.fq_abi_version() == 3
     for s in range(5):
         assert lib.fq_status_string(s).startswith(b"FQ_")
     assert lib.fq_status_string(99) == b"unknown fq_status"
@@ -104,6 +104,27 @@ def test_w4a4_linear_validation():
     lib = fq.load()
     assert lib.fq_w4a4_gemm_i32(A16, 8, 40, A16, 16, A16, None) == _lib.FQ_ESHAPE
     assert lib.fq_w4a4_gemm_i32(None, 8, 64, A16, 16, A16, None) == _lib.FQ_EINVAL
+
+
+def kvq(**kw):
+    a = dict(kv=A16, dt=0, R=8, ld=128, D=128, p=A16, alpha=1.0, q=A16, s=A16, z=A16, stream=None)
+    a.update(kw)
+    return fq.load().fq_kv_quant(a["kv"], a["dt"], a["R"], a["ld"], a["D"], a["p"], a["alpha"], a["q"], a["s"],
+                                 a["z"], a["stream"])
+
+
+def test_kv_quant_validation():
+    assert kvq(R=0) == _lib.FQ_OK
+    assert kvq(R=-1) == _lib.FQ_EINVAL
+    assert kvq(dt=3) == _lib.FQ_EINVAL
+    assert kvq(alpha=0.0) == _lib.FQ_EINVAL
+    assert kvq(alpha=float("nan")) == _lib.FQ_EINVAL
+    assert kvq(ld=64) == _lib.FQ_EINVAL                   # row stride < head_dim
+    for k in ("kv", "p", "q", "s", "z"):
+        assert kvq(**{k: None}) == _lib.FQ_EINVAL
+    assert kvq(D=96, ld=96) == _lib.FQ_ENOTSUP            # head_dim 64 or 128
+    assert kvq(kv=MIS) == _lib.FQ_ESHAPE
+    assert kvq(ld=132) == _lib.FQ_ESHAPE                  # row stride not a 16-byte multiple
 
 
 def test_gemm_impl_selector_validation():

@@ -294,21 +294,7 @@ def test_transform_quant_asym_vs_oracle(n1, n2, alpha, tdtype):
     q, s, z = fq.transform_quant_asym(x.to(DEV), n1, n2, p1.to(DEV), p2.to(DEV), alpha)
     torch.cuda.synchronize()
     qo, so, zo, yo = O.transform_quant_asym(x.float().numpy(), p1.float().numpy(), p2.float().numpy(), alpha)
-    qg = O.unpack_int4(np_of(q)).astype(np.int64) + 8
-    zg = np_of(z).astype(np.int64) + 8
-    sg = np_of(s).astype(np.float64)
-    assert np.all((qg >= 0) & (qg <= 15)) and np.all((zg >= 0) & (zg <= 15))
-    assert np.max(np.abs(sg - so) / so) <= parity.SCALE_REL
-    zt = np.abs(-np.minimum(alpha * yo.min(1), 0) / so - np.floor(-np.minimum(alpha * yo.min(1), 0) / so) - 0.5)
-    assert np.all((zg == zo) | (zt <= parity.TAU))
-    d = (qg - zg[:, None]) - (qo.astype(np.int64) - zo[:, None])
-    v = yo / so[:, None]
-    tie = np.abs(v - np.floor(v) - 0.5) <= parity.TAU
-    clamp = (qo == 0) | (qo == 15) | (qg == 0) | (qg == 15)
-    mism = d != 0
-    assert np.all(np.abs(d) <= 1)
-    assert np.all(tie[mism] | clamp[mism])
-    assert mism.mean() <= parity.MISMATCH_FRAC
+    parity.check_asym(np_of(q), np_of(s), np_of(z), yo, alpha, qo, so, zo, label=f"asym {n1}x{n2}")
 
 
 def test_weight_colsum_exact():
