@@ -38,14 +38,15 @@
 extern "C" {
 #endif
 
-#define FQ_ABI_VERSION 3   /* 2: FQ_ASYM + fq_weight_colsum; 3: fq_kv_quant */
+#define FQ_ABI_VERSION 3   /* 2: FQ_ASYM + fq_weight_colsum; 3: fq_kv_quant, fq_prepare_weight */
 
 typedef enum {
   FQ_OK = 0,
   FQ_EINVAL = 1,   /* null pointer, bad enum, alpha outside (0, 1], negative size          */
   FQ_ESHAPE = 2,   /* n1*n2 != K, odd K, K % 32 != 0 for the GEMM, misaligned pointer/stride */
   FQ_ENOTSUP = 3,  /* well-formed but no kernel for it (e.g. n1 or n2 > 256)                 */
-  FQ_ECUDA = 4     /* a CUDA launch/runtime call failed; see fq_last_cuda_error()            */
+  FQ_ECUDA = 4,    /* a CUDA launch/runtime call failed; see fq_last_cuda_error()            */
+  FQ_ESINGULAR = 5 /* fq_prepare_weight: P1 or P2 singular, or its inverse overflows the dtype */
 } fq_status;
 
 typedef enum { FQ_F16 = 0, FQ_BF16 = 1 } fq_dtype;
@@ -138,6 +139,32 @@ fq_status fq_flatquant_linear_host(const void* x_host, void* x_dev, int32_t x_dt
                                    const void* p2, float alpha, const uint8_t* qw,
                                    const float* sw, int32_t N, void* y_host, void* y_dev,
                                    int32_t y_dtype, uint8_t* q_ws, float* s_ws, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * fq_prepare_weight -- offline weight side of Eq. 3 on the GPU:
+ *   W'_o = P1^{-1} W~_o P2^{-T}     (W~_o = row o of W reshaped n1 x n2)
+ *   then per-output-channel symmetric INT4 with clipping alpha_w:
+ *   sw[o] = alpha_w max|W'_o| / 7, qw[o] = clamp(rint(W'_o / sw[o]), -8, 7), packed as the
+ *   activations are (R7).  Steps, all on `stream`: P1^{-T} and P2^{-T} by Gauss-Jordan with
+ *   partial pivoting in float64 (rounded to w_dtype), then the fq_transform_quant kernel with
+ *   (P1^{-T}, P2^{-T}, alpha_w) -- (P1^{-T})^T W~ P2^{-T} is the weight factor -- and, if
+ *   colsum_w is not NULL, fq_weight_colsum.
+ *   w       [N, n1 n2] fp16/bf16 (w_dtype), row stride ldw elements.
+ *   p1, p2  [n1, n1], [n2, n2] row-major, same dtype (the activation-side transforms).
+ *   qw      [N, n1 n2 / 2] uint8 (output).  sw [N] fp32 (output).  colsum_w [N] int32 or NULL.
+ *   workspace  device buffer of fq_prepare_weight_workspace_size(n1, n2) bytes, 256-byte
+ *           aligned; scratch, contents undefined on return.
+ *   SYNCHRONOUS: waits for `stream` to read the inversion status; returns FQ_ESINGULAR if a
+ *   pivot is zero/non-finite or the inverse does not fit the dtype (nothing else launched).
+ *   n1, n2 <= 256 and the shape rules of fq_transform_quant.
+ * ------------------------------------------------------------------------------------- */
+fq_status fq_prepare_weight(const void* w, int32_t w_dtype, int32_t N, int64_t ldw, int32_t n1,
+                            int32_t n2, const void* p1, const void* p2, float alpha_w,
+                            uint8_t* qw, float* sw, int32_t* colsum_w, void* workspace,
+                            uint64_t workspace_bytes, void* stream);
+
+/* Workspace bytes fq_prepare_weight needs for (n1, n2); 0 for invalid sizes. */
+uint64_t fq_prepare_weight_workspace_size(int32_t n1, int32_t n2);
 
 /* ---------------------------------------------------------------------------------------
  * fq_kv_quant -- KV-cache quantization: per-head transform and

@@ -6,6 +6,6 @@ exposed through the C ABI in include/flatquant.h.  See DESIGN.md.
 """
 from .api import *  # noqa: F401,F403
 from .api import __all__ as _api_all
-from ._lib import FQ_BF16, FQ_F16, FQ_SYM, FQ_ASYM, FlatQuantError, LIB_PATH, load  # noqa: F401
+from ._lib import FQ_BF16, FQ_F16, FQ_SYM, FQ_ASYM, FQ_ESINGULAR, FlatQuantError, LIB_PATH, load  # noqa: F401
 
-__all__ = list(_api_all) + ["FQ_BF16", "FQ_F16", "FQ_SYM", "FQ_ASYM", "FlatQuantError", "LIB_PATH", "load"]
+__all__ = list(_api_all) + ["FQ_BF16", "FQ_F16", "FQ_SYM", "FQ_ASYM", "FQ_ESINGULAR", "FlatQuantError", "LIB_PATH", "load"]

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(HERE, "libflatquant.so")
 if os.environ.get("FQ_TRACE_LIB") == "1":
     LIB_PATH = os.path.join(HERE, "libflatquant_trace.so")
 
-FQ_OK, FQ_EINVAL, FQ_ESHAPE, FQ_ENOTSUP, FQ_ECUDA = 0, 1, 2, 3, 4
+FQ_OK, FQ_EINVAL, FQ_ESHAPE, FQ_ENOTSUP, FQ_ECUDA, FQ_ESINGULAR = 0, 1, 2, 3, 4, 5
 FQ_F16, FQ_BF16 = 0, 1
 FQ_SYM, FQ_ASYM = 0, 1
 
@@ -34,6 +34,9 @@ SIGNATURES = {
                                    _vp, _vp, _vp]),
     "fq_flatquant_linear_host": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp, _vp, _f32, _vp, _vp, _i32, _vp,
                                         _vp, _i32, _vp, _vp, _vp]),
+    "fq_prepare_weight": (_i32, [_vp, _i32, _i32, _i64, _i32, _i32, _vp, _vp, _f32, _vp, _vp, _vp, _vp, _u64,
+                                 _vp]),
+    "fq_prepare_weight_workspace_size": (_u64, [_i32, _i32]),
     "fq_kv_quant": (_i32, [_vp, _i32, _i64, _i64, _i32, _vp, _f32, _vp, _vp, _vp, _vp]),
     "fq_choose_decomposition": (_i32, [_i64, _c.POINTER(_i32), _c.POINTER(_i32)]),
     "fq_set_gemm_impl": (_i32, [_i32]),

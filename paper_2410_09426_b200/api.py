@@ -15,7 +15,7 @@ from ._lib import FQ_BF16, FQ_F16, FQ_SYM, check, load
 
 __all__ = [
     "fq_transform_quant", "fq_transform_f32", "fq_w4a4_linear", "fq_w4a4_gemm_i32", "fq_flatquant_linear",
-    "fq_weight_colsum", "weight_colsum", "transform_quant_asym", "fq_kv_quant", "kv_quant",
+    "fq_weight_colsum", "weight_colsum", "transform_quant_asym", "fq_kv_quant", "kv_quant", "fq_prepare_weight",
     "fq_flatquant_linear_host", "fq_choose_decomposition", "fq_set_gemm_impl", "fq_set_tq_impl", "fq_launch_count",
     "fq_abi_version", "transform_quant", "transform_f32", "w4a4_linear", "w4a4_gemm_i32", "prepare_weight",
     "flatquant_linear",
@@ -193,17 +193,31 @@ def w4a4_gemm_i32(qa, qw, stream=None):
     return acc
 
 
-def prepare_weight(w, n1, n2, p1, p2, alpha_w=1.0, stream=None):
+def fq_prepare_weight(w, n1, n2, p1, p2, alpha_w, qw, sw, colsum_w=None, workspace=None, stream=None):
+    """Raw entry point (synchronous, see include/flatquant.h); allocates the workspace if not given."""
+    _cuda(w, p1, p2, qw, sw, colsum_w)
+    assert w.dim() == 2 and w.stride(1) == 1
+    lib = load()
+    need = int(lib.fq_prepare_weight_workspace_size(n1, n2))
+    if workspace is None:
+        workspace = torch.empty((max(need, 1),), dtype=torch.uint8, device=w.device)
+    st = lib.fq_prepare_weight(_ptr(w), _fq_dtype(w.dtype), w.shape[0], w.stride(0), n1, n2, _ptr(p1), _ptr(p2),
+                               float(alpha_w), _ptr(qw), _ptr(sw), _ptr(colsum_w), _ptr(workspace),
+                               workspace.numel() * workspace.element_size(), _stream(stream))
+    check("fq_prepare_weight", st)
+
+
+def prepare_weight(w, n1, n2, p1, p2, alpha_w=1.0, with_colsum=False, stream=None):
     """Offline weight side of Eq.3: W'_o = P1^{-1} W~_o P2^{-T}, quantized per
-    output channel.  This IS the activation kernel applied with
-    (P1^{-T}, P2^{-T}): (P1^{-T})^T W~ (P2^{-T}).  The two small inverses are computed once
-    on the host in float64 (offline preparation, not the hot path); the transform and the
-    per-channel quantization run in fq_transform_quant."""
-    p1i_t = torch.linalg.inv(p1.detach().to("cpu", torch.float64)).T.contiguous()
-    p2i_t = torch.linalg.inv(p2.detach().to("cpu", torch.float64)).T.contiguous()
-    p1i_t = p1i_t.to(device=w.device, dtype=w.dtype)
-    p2i_t = p2i_t.to(device=w.device, dtype=w.dtype)
-    return transform_quant(w, n1, n2, p1i_t, p2i_t, alpha_w, stream=stream)
+    output channel, entirely on the GPU through fq_prepare_weight: float64
+    Gauss-Jordan inverses, then the activation kernel with (P1^{-T}, P2^{-T}, alpha_w).
+    Returns (qw [N, K/2] uint8, sw [N] fp32) or, with_colsum, also colsum_w [N] int32."""
+    N = w.shape[0]
+    qw = torch.empty((N, n1 * n2 // 2), dtype=torch.uint8, device=w.device)
+    sw = torch.empty((N,), dtype=torch.float32, device=w.device)
+    cs = torch.empty((N,), dtype=torch.int32, device=w.device) if with_colsum else None
+    fq_prepare_weight(w, n1, n2, p1, p2, alpha_w, qw, sw, colsum_w=cs, stream=stream)
+    return (qw, sw, cs) if with_colsum else (qw, sw)
 
 
 def flatquant_linear(x, n1, n2, p1, p2, alpha, qw, sw, out_dtype=torch.float16, stream=None):

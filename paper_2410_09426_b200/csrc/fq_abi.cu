@@ -225,6 +225,45 @@ fq_status fq_weight_colsum(const uint8_t* qw, int32_t N, int32_t K, int32_t* col
   return cuda_status(weight_colsum_launch(qw, N, K, colsum, static_cast<cudaStream_t>(stream)));
 }
 
+uint64_t fq_prepare_weight_workspace_size(int32_t n1, int32_t n2) {
+  if (n1 < 1 || n2 < 1 || n1 > 256 || n2 > 256) return 0;
+  return uint64_t(weight_prep_workspace(n1, n2));
+}
+
+fq_status fq_prepare_weight(const void* w, int32_t w_dtype, int32_t N, int64_t ldw, int32_t n1, int32_t n2,
+                            const void* p1, const void* p2, float alpha_w, uint8_t* qw, float* sw,
+                            int32_t* colsum_w, void* workspace, uint64_t workspace_bytes, void* stream) {
+  fq_status s = validate_tq(w, w_dtype, N, ldw, n1, n2, p1, p2, alpha_w, qw, sw);
+  if (s != FQ_OK || N == 0) return s;
+  if (n1 > 256 || n2 > 256) return FQ_ENOTSUP;
+  if (!workspace) return FQ_EINVAL;
+  if (workspace_bytes < weight_prep_workspace(n1, n2)) return FQ_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255u) != 0) return FQ_ESHAPE;
+  if (colsum_w && (reinterpret_cast<uintptr_t>(colsum_w) & 3u) != 0) return FQ_ESHAPE;
+  const size_t nm = size_t(n1 > n2 ? n1 : n2);
+  auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  void* aug = ws;
+  uint8_t* inv1 = ws + up(nm * 2 * nm * sizeof(double));
+  uint8_t* inv2 = inv1 + up(size_t(n1) * n1 * 2);
+  int* status = reinterpret_cast<int*>(inv2 + up(size_t(n2) * n2 * 2));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool bf16 = w_dtype == FQ_BF16;
+  int h_status[2] = {0, 0};
+  s = cuda_status(inverse_t_launch(p1, n1, bf16, aug, inv1, status, st));
+  if (s != FQ_OK) return s;
+  s = cuda_status(inverse_t_launch(p2, n2, bf16, aug, inv2, status + 1, st));
+  if (s != FQ_OK) return s;
+  s = cuda_status(cudaMemcpyAsync(h_status, status, sizeof(h_status), cudaMemcpyDeviceToHost, st));
+  if (s != FQ_OK) return s;
+  s = cuda_status(cudaStreamSynchronize(st));
+  if (s != FQ_OK) return s;
+  if (h_status[0] != 0 || h_status[1] != 0) return FQ_ESINGULAR;
+  s = run_tq(w, w_dtype, N, ldw, n1, n2, inv1, inv2, alpha_w, qw, sw, nullptr, nullptr, stream);
+  if (s != FQ_OK || !colsum_w) return s;
+  return cuda_status(weight_colsum_launch(qw, N, n1 * n2, colsum_w, st));
+}
+
 fq_status fq_kv_quant(const void* kv, int32_t kv_dtype, int64_t R, int64_t ldkv, int32_t head_dim,
                       const void* p_h, float alpha, uint8_t* q, float* scale, int8_t* zero, void* stream) {
   if (kv_dtype != FQ_F16 && kv_dtype != FQ_BF16) return FQ_EINVAL;
@@ -284,6 +323,7 @@ const char* fq_status_string(int32_t status) {
     case FQ_ESHAPE: return "FQ_ESHAPE: unsupported shape, stride or alignment";
     case FQ_ENOTSUP: return "FQ_ENOTSUP: no kernel for this configuration";
     case FQ_ECUDA: return "FQ_ECUDA: CUDA error (see fq_last_cuda_error)";
+    case FQ_ESINGULAR: return "FQ_ESINGULAR: transform matrix singular or its inverse overflows the dtype";
     default: return "unknown fq_status";
   }
 }

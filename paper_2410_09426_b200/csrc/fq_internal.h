@@ -108,6 +108,9 @@ cudaError_t gemm_tc05_launch(const GemmArgs& a);     // tcgen05 kind::i8, single
 bool gemm_tc05_supported(const GemmArgs& a);
 cudaError_t gemm_pair_launch(const GemmArgs& a);     // tcgen05 kind::i8, CTA pair (cta_group::2)
 bool gemm_pair_supported(const GemmArgs& a);
+size_t weight_prep_workspace(int n1, int n2);
+cudaError_t inverse_t_launch(const void* p, int n, bool bf16, void* aug, void* out, int* status,
+                             cudaStream_t stream);
 bool kv_quant_supported(const KVArgs& a);            // tcgen05 KV-cache kernel
 cudaError_t kv_quant_launch(const KVArgs& a);
 

@@ -127,6 +127,29 @@ def test_kv_quant_validation():
     assert kvq(ld=132) == _lib.FQ_ESHAPE                  # row stride not a 16-byte multiple
 
 
+def test_prepare_weight_validation():
+    lib = fq.load()
+    ws_need = lib.fq_prepare_weight_workspace_size(64, 64)
+    assert ws_need >= 64 * 128 * 8 + 2 * 64 * 64 * 2
+    assert lib.fq_prepare_weight_workspace_size(0, 64) == 0 and lib.fq_prepare_weight_workspace_size(64, 512) == 0
+
+    def pw(**kw):
+        a = dict(w=A16, dt=0, N=8, ld=4096, n1=64, n2=64, p1=A16, p2=A16, alpha=1.0, qw=A16, sw=A16, cs=None,
+                 ws=A16, wsb=ws_need, stream=None)
+        a.update(kw)
+        return lib.fq_prepare_weight(a["w"], a["dt"], a["N"], a["ld"], a["n1"], a["n2"], a["p1"], a["p2"],
+                                     a["alpha"], a["qw"], a["sw"], a["cs"], a["ws"], a["wsb"], a["stream"])
+    assert pw(N=0) == _lib.FQ_OK
+    assert pw(ws=None) == _lib.FQ_EINVAL
+    assert pw(wsb=ws_need - 1) == _lib.FQ_EINVAL
+    assert pw(ws=VP(0x1010)) == _lib.FQ_ESHAPE            # workspace must be 256-byte aligned
+    assert pw(cs=MIS) == _lib.FQ_ESHAPE
+    assert pw(p1=None) == _lib.FQ_EINVAL
+    assert pw(alpha=0.0) == _lib.FQ_EINVAL
+    assert pw(n1=300, n2=2, ld=600) == _lib.FQ_ENOTSUP
+    assert "singular" in lib.fq_status_string(_lib.FQ_ESINGULAR).decode()
+
+
 def test_gemm_impl_selector_validation():
     assert fq.load().fq_set_gemm_impl(7) == _lib.FQ_EINVAL
     with pytest.raises(fq.FlatQuantError):

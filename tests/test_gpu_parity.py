@@ -259,25 +259,48 @@ def test_determinism():
     assert torch.equal(outs[0], outs[1])
 
 
-def test_gpu_weight_prep_matches_oracle():
-    """NEXT-2 preview: W' = P1^{-1} W~ P2^{-T} via the activation kernel with
-    (P1^{-T}, P2^{-T}) rounded to fp16 on the host.  Parity: the oracle's transform+quant of W
-    with those same fp16 matrices (bars 2-3, per output channel); plus the dequantized weights
-    against the exact float64 W' within the 4-bit RTN step (half a step + the fp16 rounding of
-    the inverses)."""
-    n1, n2, N = 64, 64, 512
-    w = synth.weights(N, n1 * n2, seed=3)
-    p1 = synth.well_conditioned(n1, seed=3, tag="p1")
-    p2 = synth.well_conditioned(n2, seed=3, tag="p2")
-    qw, sw = fq.prepare_weight(to_dev(w), n1, n2, to_dev(p1), to_dev(p2), 1.0)
-    p1i_t = np.linalg.inv(p1.astype(np.float64)).T.astype(np.float16)
-    p2i_t = np.linalg.inv(p2.astype(np.float64)).T.astype(np.float16)
-    qo, so, yo = O.transform_quant(w, p1i_t, p2i_t, 1.0)
-    parity.check_transform(np_of(qw), np_of(sw), None, yo, qo, so, label="weight prep")
-    _, _, wp = O.prepare_weight(w, p1, p2, 1.0)
-    deq = O.dequantize_rows(O.unpack_int4(np_of(qw)), np_of(sw).astype(np.float64))
+@pytest.mark.parametrize("n1,n2,N,tdtype,alpha_w", [(64, 64, 512, torch.float16, 1.0),
+                                                    (64, 128, 264, torch.bfloat16, 0.95),
+                                                    (112, 128, 136, torch.float16, 1.0),
+                                                    (16, 32, 72, torch.float16, 0.9)])
+def test_gpu_weight_prep_matches_oracle(n1, n2, N, tdtype, alpha_w):
+    """NEXT-2: fq_prepare_weight computes W' = P1^{-1} W~ P2^{-T} on the GPU:
+    float64 Gauss-Jordan inverses rounded to the weights' dtype, then the activation kernel with
+    (P1^{-T}, P2^{-T}, alpha_w).  Parity: the oracle's transform+quant of W with the inverses
+    numpy computes in float64 and rounds to the same dtype (bars 2-3 per output channel); the
+    dequantized weights against the exact float64 W' within the 4-bit RTN step; colsum_w exact."""
+    w = torch.from_numpy(synth.weights(N, n1 * n2, seed=3, dtype=np.float32)).to(tdtype)
+    p1 = torch.from_numpy(synth.well_conditioned(n1, seed=3, tag="p1", dtype=np.float32)).to(tdtype)
+    p2 = torch.from_numpy(synth.well_conditioned(n2, seed=3, tag="p2", dtype=np.float32)).to(tdtype)
+    qw, sw, cs = fq.prepare_weight(w.to(DEV), n1, n2, p1.to(DEV), p2.to(DEV), alpha_w, with_colsum=True)
+    torch.cuda.synchronize()
+    wf, p1f, p2f = (t.float().numpy().astype(np.float64) for t in (w, p1, p2))
+    p1i_t = torch.from_numpy(np.linalg.inv(p1f).T.copy()).to(tdtype).float().numpy()
+    p2i_t = torch.from_numpy(np.linalg.inv(p2f).T.copy()).to(tdtype).float().numpy()
+    qo, so, yo = O.transform_quant(wf, p1i_t, p2i_t, alpha_w)
+    parity.check_transform(np_of(qw), np_of(sw), None, yo, qo, so, label=f"weight prep {n1}x{n2}")
+    codes = O.unpack_int4(np_of(qw))
+    assert np.array_equal(np_of(cs).astype(np.int64), codes.astype(np.int64).sum(1))
+    _, _, wp = O.prepare_weight(wf, p1f, p2f, alpha_w)
+    deq = O.dequantize_rows(codes, np_of(sw).astype(np.float64))
     step = np_of(sw).astype(np.float64)[:, None]
-    assert np.all(np.abs(deq - wp) <= 0.5 * step + 2e-2 * np.abs(wp).max(1, keepdims=True))
+    inside = np.abs(wp) <= 7 * step
+    tol = 0.5 * step + 2e-2 * np.abs(wp).max(1, keepdims=True)
+    assert np.all((np.abs(deq - wp) <= tol)[inside])
+
+
+def test_gpu_weight_prep_singular():
+    """A singular P (a zero row) or one whose inverse overflows fp16 (1e-5 I) is reported as
+    FQ_ESINGULAR before anything is quantized."""
+    n1, n2, N = 16, 32, 8
+    w = to_dev(synth.weights(N, n1 * n2, seed=1))
+    p2 = to_dev(synth.well_conditioned(n2, seed=1, tag="p2"))
+    bad = synth.well_conditioned(n1, seed=1, tag="p1").copy()
+    bad[3] = 0
+    for p1 in (to_dev(bad), to_dev((np.eye(n1) * 1e-5).astype(np.float16))):
+        with pytest.raises(fq.FlatQuantError) as e:
+            fq.prepare_weight(w, n1, n2, p1, p2, 1.0)
+        assert e.value.status == fq.FQ_ESINGULAR
 
 
 # ---------------------------------------------------------------- asymmetric mode (NEXT-1, R19)
