@@ -193,8 +193,10 @@ fq_status fq_kv_quant(const void* kv, int32_t kv_dtype, int64_t R, int64_t ldkv,
 fq_status fq_choose_decomposition(int64_t n, int32_t* n1, int32_t* n2);
 
 /* Selects the GEMM implementation for subsequent calls in this process (testing aid):
- * 0 = default (tcgen05 kind::i8 on a CTA pair, cta_group::2), 1 = legacy mma.sync
- * cross-check kernel, 2 = tcgen05 kind::i8 on a single CTA.  Returns FQ_EINVAL otherwise. */
+ * 0 = default (tcgen05 kind::i8 on a CTA pair, cta_group::2, tile width 192/160/128 features
+ * picked per shape to fill the last wave), 1 = legacy mma.sync cross-check kernel, 2 = tcgen05
+ * kind::i8 on a single CTA, 3 / 4 / 5 = the pair kernel with the tile width forced to 192 /
+ * 160 / 128.  All bit-identical.  Returns FQ_EINVAL otherwise. */
 fq_status fq_set_gemm_impl(int32_t impl);
 
 /* Selects the transform+quant implementation for subsequent calls in this process (testing

@@ -126,11 +126,15 @@ static fq_status run_gemm(const uint8_t* qa, const float* sa, int64_t T, int32_t
   a.colsum = colsum;
   a.stream = static_cast<cudaStream_t>(stream);
   const int impl = g_gemm_impl.load();
+  // impl 0: pair kernel with the tile width picked per shape; 3 / 4 / 5: forced 192 / 160 / 128
+  const bool pair = impl == 0 || impl >= 3;
+  const int bn = impl == 3 ? 192 : impl == 4 ? 160 : impl == 5 ? 128 : 0;
   if (za) {                                        // asymmetric activations: pair kernel only
-    if (impl != 0 || !gemm_pair_supported(a)) return FQ_ENOTSUP;
-    return cuda_status(gemm_pair_launch(a));
+    if (!pair || !gemm_pair_supported(a)) return FQ_ENOTSUP;
+    return cuda_status(gemm_pair_launch(a, bn));
   }
-  if (impl == 0 && gemm_pair_supported(a)) return cuda_status(gemm_pair_launch(a));
+  if (pair && gemm_pair_supported(a)) return cuda_status(gemm_pair_launch(a, bn));
+  if (impl >= 3) return FQ_ENOTSUP;
   if (impl == 2 && gemm_tc05_supported(a)) return cuda_status(gemm_tc05_launch(a));
   return cuda_status(gemm_mma_launch(a));
 }
@@ -309,7 +313,7 @@ fq_status fq_set_tq_impl(int32_t impl) {
 }
 
 fq_status fq_set_gemm_impl(int32_t impl) {
-  if (impl < 0 || impl > 2) return FQ_EINVAL;
+  if (impl < 0 || impl > 5) return FQ_EINVAL;
   g_gemm_impl.store(impl);
   return FQ_OK;
 }

@@ -23,6 +23,7 @@
 // barrier; the leader's tcgen05.commit multicasts to both CTAs' `empty` / `tfull` barriers;
 // both CTAs' epilogues arrive on the leader's `tempty` barrier.
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 #include "fq_device.cuh"
 #include "fq_internal.h"
@@ -46,9 +47,6 @@ FQ_DEVICE void trace(int) {}
 #endif
 
 constexpr int BM = 256, BM_CTA = 128;     // tokens per pair tile / per CTA
-#ifndef FQ_GEMM_BN
-#define FQ_GEMM_BN 192
-#endif
 #ifndef FQ_GEMM_STAGES
 #define FQ_GEMM_STAGES 2
 #endif
@@ -58,20 +56,14 @@ constexpr int BM = 256, BM_CTA = 128;     // tokens per pair tile / per CTA
 #ifndef FQ_GEMM_BWARPS
 #define FQ_GEMM_BWARPS 6
 #endif
-constexpr int BN = FQ_GEMM_BN, BN_CTA = BN / 2;   // features per pair tile / B rows per CTA
 constexpr int BK = 256;                   // int8 K per stage (two 128-byte swizzle atoms)
 constexpr int UK = 32;
 constexpr int STAGES = FQ_GEMM_STAGES;    // MMA stages (TMEM A / widened smem B)
 constexpr int PSTAGES = FQ_GEMM_PSTAGES;  // packed A+B ring (TMA)
-constexpr int B_BYTES = BN_CTA * BK;      // 12 KB per stage per CTA (widened)
-constexpr int BP_BYTES = BN_CTA * BK / 2; // 6 KB packed B per ring stage
 constexpr int AP_BYTES = BM_CTA * BK / 2; // 8 KB packed A per ring stage
-constexpr int P_BYTES = AP_BYTES + BP_BYTES;
 constexpr int EPI_BYTES = 32 * 128;       // per epilogue warp: 32 rows x 64 fp16 columns (SW128)
 constexpr int A_COLS = BK / 4;            // TMEM columns per A stage
 constexpr int TMEM_ACC0 = 0;              // two accumulators [0, 2*BN)
-constexpr int TMEM_A0 = 2 * BN;           // A stages [2*BN, 2*BN + STAGES*A_COLS) = [384, 512)
-constexpr int B_ATOM = BN_CTA * 128;      // one 128-byte K atom of the widened B stage
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_EPI_WARPS = 4, MMA_WARP = 4;
 constexpr int A_WARP0 = 5, NUM_A_WARPS = 8;     // 2 warps per TMEM lane quarter (each half of K)
@@ -80,12 +72,26 @@ constexpr int NUM_CONV_WARPS = NUM_A_WARPS + NUM_B_WARPS;
 constexpr int TMA_WARP = B_WARP0 + NUM_B_WARPS;
 constexpr int THREADS = (TMA_WARP + 1) * 32;
 constexpr int B_CHUNKS = BK / 32;                          // 16-byte packed chunks per weight row
-constexpr int B_TASKS = BN_CTA * B_CHUNKS / (NUM_B_WARPS * 32);
-constexpr size_t SMEM_BYTES =
-    size_t(STAGES) * B_BYTES + size_t(PSTAGES) * P_BYTES + NUM_EPI_WARPS * EPI_BYTES + 1024 + 512;
-constexpr uint32_t IDESC = tc::idesc_i8(BM, BN);
-static_assert(TMEM_A0 + STAGES * A_COLS <= TMEM_COLS, "TMEM budget");
-static_assert(B_TASKS * NUM_B_WARPS * 32 == BN_CTA * B_CHUNKS, "B task split");
+
+// Tile width BN (features per pair tile) is a template parameter: the host picks it per shape to
+// fill the last wave (fewer, narrower waves when N / 192 tiles would leave most clusters idle).
+template <int BN>
+struct Geo {
+  static_assert(BN % 32 == 0 && BN >= 64 && BN <= 192, "BN: multiple of 32 in [64, 192]");
+  static constexpr int BN_CTA = BN / 2;                    // B rows per CTA
+  static constexpr int B_BYTES = BN_CTA * BK;              // widened B per stage per CTA
+  static constexpr int BP_BYTES = BN_CTA * BK / 2;         // packed B per ring stage
+  static constexpr int P_BYTES = AP_BYTES + BP_BYTES;
+  static constexpr int TMEM_A0 = 2 * BN;                   // A stages after the two accumulators
+  static constexpr int B_ATOM = BN_CTA * 128;              // one 128-byte K atom of the widened B stage
+  static constexpr int B_TOTAL = BN_CTA * B_CHUNKS;        // B conversion tasks per stage
+  static constexpr int B_TASKS = (B_TOTAL + NUM_B_WARPS * 32 - 1) / (NUM_B_WARPS * 32);
+  static constexpr size_t SMEM_BYTES =
+      size_t(STAGES) * B_BYTES + size_t(PSTAGES) * P_BYTES + NUM_EPI_WARPS * EPI_BYTES + 1024 + 512;
+  static constexpr uint32_t IDESC = tc::idesc_i8(BM, BN);
+  static_assert(TMEM_A0 + STAGES * A_COLS <= TMEM_COLS, "TMEM budget");
+  static_assert(B_ATOM % 1024 == 0 && P_BYTES % 1024 == 0, "SWIZZLE_128B atoms stay 1024-B aligned");
+};
 
 FQ_DEVICE void widen8(uint32_t p, uint32_t& lo, uint32_t& hi) {   // 8 nibbles -> 8 x (16 q) int8
   lo = (p << 4) & 0xF0F0F0F0u;
@@ -129,12 +135,16 @@ struct Cursor {
   }
 };
 
-template <bool OUT_I32, bool BF16, bool ASYM>
+template <int BN, bool OUT_I32, bool BF16, bool ASYM>
 __global__ void __launch_bounds__(THREADS, 1)
 gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const __grid_constant__ CUtensorMap tmY, const float* __restrict__ sa, int T, int K,
-                 const float* __restrict__ sw, int N, void* __restrict__ yv, const int8_t* __restrict__ za,
-                 const int32_t* __restrict__ colsum) {
+                 const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmY32,
+                 const float* __restrict__ sa, int T, int K, const float* __restrict__ sw, int N,
+                 void* __restrict__ yv, const int8_t* __restrict__ za, const int32_t* __restrict__ colsum) {
+  using GE = Geo<BN>;
+  constexpr int BN_CTA = GE::BN_CTA, B_BYTES = GE::B_BYTES, P_BYTES = GE::P_BYTES, TMEM_A0 = GE::TMEM_A0;
+  constexpr int B_ATOM = GE::B_ATOM, B_TASKS = GE::B_TASKS;
+  constexpr uint32_t IDESC = GE::IDESC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sP = smem + size_t(STAGES) * B_BYTES;                  // packed ring: [A 8 KB | B 6 KB]
@@ -175,7 +185,10 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         tc::mbar_init(&pempty[s], NUM_CONV_WARPS);
       }
       tc::fence_barrier_init();
-      if constexpr (!OUT_I32) tc::tma_prefetch_desc(&tmY);
+      if constexpr (!OUT_I32) {
+        tc::tma_prefetch_desc(&tmY);
+        if constexpr (BN % 64 != 0) tc::tma_prefetch_desc(&tmY32);
+      }
       tc::tma_prefetch_desc(&tmA);
       tc::tma_prefetch_desc(&tmB);
     }
@@ -302,6 +315,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
         for (int i = 0; i < B_TASKS; ++i) {
           const int task = ct + i * NUM_B_WARPS * 32;
+          if (GE::B_TOTAL % (NUM_B_WARPS * 32) != 0 && task >= GE::B_TOTAL) break;
           const uint4 pk = tc::lds128(src + uint32_t(task * 16));      // row task/8, packed chunk task%8
           widen8(pk.x, o[i][0], o[i][1]);
           widen8(pk.y, o[i][2], o[i][3]);
@@ -311,6 +325,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
         for (int i = 0; i < B_TASKS; ++i) {
           const int task = ct + i * NUM_B_WARPS * 32, rl = task / B_CHUNKS, c = task % B_CHUNKS;
+          if (GE::B_TOTAL % (NUM_B_WARPS * 32) != 0 && task >= GE::B_TOTAL) break;
           const uint32_t rowp = dst + uint32_t((c >> 2) * B_ATOM + rl * 128);
           const int cc = c & 3;
           tc::sts128(rowp + uint32_t(((2 * cc) ^ (rl & 7)) << 4), o[i][0], o[i][1], o[i][2], o[i][3]);
@@ -398,17 +413,19 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const float s_a = row_ok ? sa[row] * (1.0f / 256.0f) : 0.f;
         // asymmetric activations: acc_true = acc - (z - 8) colsum_w; the TMEM holds 256 acc
         const int zc256 = (ASYM && row_ok) ? int(za[row]) * 256 : 0;
-#pragma unroll 1
-        for (int q = 0; q < BN / 64; ++q) {
-          uint32_t v[64];
-          tc::tmem_ld32(tacc + uint32_t(q * 64), *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
-          tc::tmem_ld32(tacc + uint32_t(q * 64 + 32), *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+        // one chunk of NC (64 or 32) columns: TMEM -> dequant -> swizzled staging -> TMA store
+        auto emit = [&](auto nc_tag, int c0off) {
+          constexpr int NC = decltype(nc_tag)::value;
+          uint32_t v[NC];
+          tc::tmem_ld32(tacc + uint32_t(c0off), *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+          if constexpr (NC == 64)
+            tc::tmem_ld32(tacc + uint32_t(c0off + 32), *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
           if (lane == 0) tc::bulk_wait_read0();          // previous chunk's store has left the buffer
           __syncwarp();
           tc::tmem_ld_wait();
-          const int col0 = nb * BN + q * 64;
+          const int col0 = nb * BN + c0off;
 #pragma unroll
-          for (int c8 = 0; c8 < 8; ++c8) {
+          for (int c8 = 0; c8 < NC / 8; ++c8) {
             const int col = col0 + c8 * 8;
             float4 w0 = make_float4(0.f, 0.f, 0.f, 0.f), w1 = w0;
             if (col < N) {                                  // N % 8 == 0: a group is all in or all out
@@ -449,15 +466,21 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
               o[2] = pack_half2(f4, f5);
               o[3] = pack_half2(f6, f7);
             }
-            tc::sts128(stg + uint32_t(lane * 128 + ((c8 ^ (lane & 7)) << 4)), o[0], o[1], o[2], o[3]);
+            if constexpr (NC == 64)      // 32 rows x 128 B, SWIZZLE_128B: chunk ^= row % 8
+              tc::sts128(stg + uint32_t(lane * 128 + ((c8 ^ (lane & 7)) << 4)), o[0], o[1], o[2], o[3]);
+            else                         // 32 rows x 64 B, SWIZZLE_64B: chunk ^= (row / 2) % 4
+              tc::sts128(stg + uint32_t(lane * 64 + ((c8 ^ ((lane >> 1) & 3)) << 4)), o[0], o[1], o[2], o[3]);
           }
           tc::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tc::tma_store_2d(&tmY, stg, col0, mb * BM + int(rank) * BM_CTA + warp * 32);
+            tc::tma_store_2d(NC == 64 ? &tmY : &tmY32, stg, col0, mb * BM + int(rank) * BM_CTA + warp * 32);
             tc::bulk_commit();
           }
-        }
+        };
+#pragma unroll 1
+        for (int q = 0; q < BN / 64; ++q) emit(std::integral_constant<int, 64>{}, q * 64);
+        if constexpr (BN % 64 != 0) emit(std::integral_constant<int, 32>{}, (BN / 64) * 64);
       }
       tc::fence_before();
       named_bar_sync(2, NUM_EPI_WARPS * 32);
@@ -492,20 +515,42 @@ bool gemm_pair_supported(const GemmArgs& a) {
   return a.K % 32 == 0 && a.K <= 131072 && a.N % 8 == 0 && a.T <= int64_t(1) << 30 && tmap_available();
 }
 
-cudaError_t gemm_pair_launch(const GemmArgs& a) {
+// Tile width per shape: the candidates cost waves * BN MMA-cycles per cluster (a pair tile's
+// main loop is proportional to BN at fixed K); a narrower tile wins only if it saves >= 4%.
+int gemm_pair_pick_bn(int64_t T, int N, int clusters) {
+  using g3::BM;
+  const int cands[3] = {192, 160, 128};
+  int best = 192;
+  double best_cost = 0;
+  for (int i = 0; i < 3; ++i) {
+    const int bn = cands[i];
+    const int64_t tiles = ((T + BM - 1) / BM) * ((N + bn - 1) / bn);
+    const double cost = double((tiles + clusters - 1) / clusters) * bn * (i == 0 ? 1.0 : 1.04);
+    if (i == 0 || cost < best_cost) {
+      best = bn;
+      best_cost = cost;
+    }
+  }
+  return best;
+}
+
+template <int BN>
+static cudaError_t launch_bn(const GemmArgs& a) {
   using namespace g3;
+  using GE = Geo<BN>;
   const bool asym = a.za != nullptr && !a.out_i32;
-  auto kern = a.out_i32 ? gemm_pair_kernel<true, false, false>
-              : asym    ? (a.y_bf16 ? gemm_pair_kernel<false, true, true> : gemm_pair_kernel<false, false, true>)
-                        : (a.y_bf16 ? gemm_pair_kernel<false, true, false> : gemm_pair_kernel<false, false, false>);
+  auto kern = a.out_i32 ? gemm_pair_kernel<BN, true, false, false>
+              : asym    ? (a.y_bf16 ? gemm_pair_kernel<BN, false, true, true> : gemm_pair_kernel<BN, false, false, true>)
+                        : (a.y_bf16 ? gemm_pair_kernel<BN, false, true, false>
+                                    : gemm_pair_kernel<BN, false, false, false>);
   static bool attr_done[5] = {false, false, false, false, false};
   const int which = a.out_i32 ? 0 : (a.y_bf16 ? 1 : 2) + (asym ? 2 : 0);
   if (!attr_done[which]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(GE::SMEM_BYTES));
     if (e != cudaSuccess) return e;
     attr_done[which] = true;
   }
-  CUtensorMap ma{}, mb{}, my{};
+  CUtensorMap ma{}, mb{}, my{}, my32{};
   {
     const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.T)};
     const uint64_t strides[1] = {uint64_t(a.K / 2)};
@@ -515,7 +560,7 @@ cudaError_t gemm_pair_launch(const GemmArgs& a) {
   {
     const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.N)};
     const uint64_t strides[1] = {uint64_t(a.K / 2)};
-    const uint32_t box[2] = {BK / 2, BN_CTA};
+    const uint32_t box[2] = {BK / 2, uint32_t(GE::BN_CTA)};
     if (!tmap_encode(&mb, a.qw, 1, 2, dims, strides, box, TMAP_SW_NONE)) return cudaErrorInvalidValue;
   }
   if (!a.out_i32) {
@@ -523,14 +568,25 @@ cudaError_t gemm_pair_launch(const GemmArgs& a) {
     const uint64_t strides[1] = {uint64_t(a.N) * 2};
     const uint32_t box[2] = {64, 32};
     if (!tmap_encode(&my, a.y, 2, 2, dims, strides, box, TMAP_SW128)) return cudaErrorInvalidValue;
+    const uint32_t box32[2] = {32, 32};
+    if (BN % 64 != 0 && !tmap_encode(&my32, a.y, 2, 2, dims, strides, box32, TMAP_SW64)) return cudaErrorInvalidValue;
   }
   const int num_tiles = int((a.T + BM - 1) / BM) * ((a.N + BN - 1) / BN);
   const int clusters = std::max(1, std::min(num_tiles, num_sms() / 2));
-  cudaError_t e = launch_pdl(kern, dim3(unsigned(2 * clusters)), dim3(THREADS), SMEM_BYTES, a.stream, 2, ma, mb, my,
-                             a.sa, int(a.T), a.K, a.sw, a.N, a.y, a.za, a.colsum);
+  cudaError_t e = launch_pdl(kern, dim3(unsigned(2 * clusters)), dim3(THREADS), GE::SMEM_BYTES, a.stream, 2, ma, mb,
+                             my, my32, a.sa, int(a.T), a.K, a.sw, a.N, a.y, a.za, a.colsum);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+cudaError_t gemm_pair_launch(const GemmArgs& a, int bn) {
+  if (bn == 0) bn = gemm_pair_pick_bn(a.T, a.N, std::max(1, num_sms() / 2));
+  switch (bn) {
+    case 160: return launch_bn<160>(a);
+    case 128: return launch_bn<128>(a);
+    default: return launch_bn<192>(a);
+  }
 }
 
 // colsum[o] = sum_k qw[o,k] over the signed nibbles of packed row o (one warp per row).

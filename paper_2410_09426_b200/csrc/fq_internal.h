@@ -106,7 +106,9 @@ cudaError_t weight_colsum_launch(const uint8_t* qw, int N, int K, int32_t* colsu
 cudaError_t gemm_mma_launch(const GemmArgs& a);      // legacy mma.sync cross-check kernel
 cudaError_t gemm_tc05_launch(const GemmArgs& a);     // tcgen05 kind::i8, single CTA
 bool gemm_tc05_supported(const GemmArgs& a);
-cudaError_t gemm_pair_launch(const GemmArgs& a);     // tcgen05 kind::i8, CTA pair (cta_group::2)
+cudaError_t gemm_pair_launch(const GemmArgs& a, int bn = 0);   // tcgen05 kind::i8, CTA pair (cta_group::2);
+                                                          // bn: tile width 192/160/128, 0 = per shape
+int gemm_pair_pick_bn(int64_t T, int N, int clusters);
 bool gemm_pair_supported(const GemmArgs& a);
 size_t weight_prep_workspace(int n1, int n2);
 cudaError_t inverse_t_launch(const void* p, int n, bool bf16, void* aug, void* out, int* status,

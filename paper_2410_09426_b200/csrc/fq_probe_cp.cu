@@ -48,11 +48,19 @@ cp_probe_kernel(const __grid_constant__ CUtensorMap tm, const uint8_t* __restric
   if ((mode & 3) == 1) {
     // TMA, 16U4_ALIGN16B, SWIZZLE_128B, two boxes of {128 elements, 128 rows} (16 KB each)
     if (threadIdx.x == 0) {
-      tc::mbar_expect_tx(&bar_tma, SM_BYTES);
+      tc::mbar_expect_tx(&bar_tma, (mode & 8) ? SM_BYTES / 2 : SM_BYTES);
       tc::tma_load_2d(smem, &tm, &bar_tma, 0, int(rank) * ROWS);
       tc::tma_load_2d(smem + SM_BYTES / 2, &tm, &bar_tma, 128, int(rank) * ROWS);
     }
-    tc::mbar_wait(&bar_tma, 0);
+    // bounded wait: report instead of hanging if the transaction count never completes
+    uint32_t done = 0;
+    for (int it = 0; it < (1 << 22) && !done; ++it)
+      asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}\n"
+                   : "=r"(done) : "r"(smem_u32(&bar_tma)) : "memory");
+    if (!done) {
+      if (threadIdx.x == 0) tmem_dump[0] = 0xDEADBEEFu;
+      asm volatile("trap;");
+    }
   } else {
     // manual SW128 K-major image: row r, group g (16 elements = 8 packed bytes): 16-byte unit at
     // half (g / 8) * 16 KB + r * 128 + ((g % 8) ^ (r % 8)) * 16; packed bytes in the first 8
@@ -116,7 +124,7 @@ using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, 
 }  // namespace fq
 
 // packed: [2 * 128, 128] bytes (device).  mode bit0-1: 0 manual (data first 8 B), 1 TMA
-// 16U4_ALIGN16B, 2 manual (data last 8 B); bit2: CTA pair.  smem_dump [2 * 32768] bytes,
+// 16U4_ALIGN16B, 2 manual (data last 8 B); bit2: CTA pair; bit3: TMA expect_tx = packed bytes.  smem_dump [2 * 32768] bytes,
 // tmem_dump [2 * 128 * 64] u32.  Returns 0 on success, else a CUDA / driver error code.
 extern "C" int fq_debug_cp_probe(const uint8_t* packed, int mode, uint8_t* smem_dump, uint32_t* tmem_dump) {
   using namespace fq::probe_cp;
@@ -149,10 +157,10 @@ extern "C" int fq_debug_cp_probe(const uint8_t* packed, int mode, uint8_t* smem_
   cudaError_t e;
   if (pair) {
     cudaFuncSetAttribute(cp_probe_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    e = cudaLaunchKernelEx(&cfg, cp_probe_kernel<true>, tm, packed, mode & 3, smem_dump, tmem_dump);
+    e = cudaLaunchKernelEx(&cfg, cp_probe_kernel<true>, tm, packed, mode & 11, smem_dump, tmem_dump);
   } else {
     cudaFuncSetAttribute(cp_probe_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    e = cudaLaunchKernelEx(&cfg, cp_probe_kernel<false>, tm, packed, mode & 3, smem_dump, tmem_dump);
+    e = cudaLaunchKernelEx(&cfg, cp_probe_kernel<false>, tm, packed, mode & 11, smem_dump, tmem_dump);
   }
   if (e != cudaSuccess) return int(e);
   return int(cudaDeviceSynchronize());

@@ -33,7 +33,7 @@ cands = {
     "(n<<2)^0x20": lambda n: (n << 2) ^ 0x20,
 }
 
-for mode in (0, 2, 1, 5, 4):
+for mode in [int(m) for m in (sys.argv[1:] or ['0', '4', '9', '1', '13', '5'])]:
     sd = torch.zeros(2 * 32768, dtype=torch.uint8, device="cuda")
     td = torch.zeros(2 * 128 * 64, dtype=torch.int32, device="cuda")
     e = f(pk.data_ptr(), mode, sd.data_ptr(), td.data_ptr())

@@ -145,9 +145,15 @@ def test_transform_strided_rows_and_empty():
     assert q0.shape == (0, n1 * n2 // 2)
 
 
-@pytest.mark.parametrize("impl", [0, 1, 2])
+# GEMM implementations (fq_set_gemm_impl): 0 pair kernel, tile width per shape; 1 legacy mma.sync;
+# 2 single-CTA tcgen05; 3 / 4 / 5 pair kernel with the tile width forced to 192 / 160 / 128.
+GEMM_IMPLS = [0, 1, 2, 3, 4, 5]
+
+
+@pytest.mark.parametrize("impl", GEMM_IMPLS)
 @pytest.mark.parametrize("T,N,K", [(1, 8, 32), (37, 24, 96), (128, 256, 128), (300, 520, 4096),
-                                   (2048, 4096, 4096), (257, 4096, 14336), (64, 28672, 4096)])
+                                   (2048, 4096, 4096), (257, 4096, 14336), (64, 28672, 4096), (513, 200, 352),
+                                   (700, 168, 4096)])
 def test_gemm_i32_bit_exact(impl, T, N, K):
     qa = synth.random_codes(T, K, seed=T, tag="qa")
     qw = synth.random_codes(N, K, seed=N, tag="qw")
@@ -172,7 +178,7 @@ def test_gemm_i32_extreme_values():
 
 
 @pytest.mark.parametrize("out_dtype", [torch.float16, torch.bfloat16])
-@pytest.mark.parametrize("impl", [0, 1, 2])
+@pytest.mark.parametrize("impl", GEMM_IMPLS)
 def test_w4a4_linear_dequant(out_dtype, impl):
     T, N, K = 333, 776, 2048
     qa = synth.random_codes(T, K, seed=1, tag="qa")
@@ -327,8 +333,9 @@ def test_weight_colsum_exact():
     assert np.array_equal(np_of(cs).astype(np.int64), qw.astype(np.int64).sum(1))
 
 
+@pytest.mark.parametrize("impl", [0, 4])
 @pytest.mark.parametrize("out_dtype", [torch.float16, torch.bfloat16])
-def test_asym_linear_vs_oracle(out_dtype):
+def test_asym_linear_vs_oracle(out_dtype, impl):
     """Asymmetric activations through the GEMM: Y = s_a s_w (acc - (z - 8) colsum_w) equals the
     oracle's dequantized product of the GPU's own codes (per token, fp16/bf16 output rounding),
     and the whole chain stays within the end-to-end Frobenius bar of the oracle's codes."""
@@ -340,8 +347,12 @@ def test_asym_linear_vs_oracle(out_dtype):
     qw_d = to_dev(O.pack_int4(qw))
     q, s, z = fq.transform_quant_asym(x.to(DEV), n1, n2, p1.to(DEV), p2.to(DEV), 0.9)
     cs = fq.weight_colsum(qw_d)
-    y = fq.w4a4_linear(q, s, qw_d, to_dev(sw32), out_dtype, za=z, colsum_w=cs)
-    torch.cuda.synchronize()
+    fq.fq_set_gemm_impl(impl)
+    try:
+        y = fq.w4a4_linear(q, s, qw_d, to_dev(sw32), out_dtype, za=z, colsum_w=cs)
+        torch.cuda.synchronize()
+    finally:
+        fq.fq_set_gemm_impl(0)
     qg = O.unpack_int4(np_of(q)).astype(np.int64) + 8
     zg = np_of(z).astype(np.int64) + 8
     same = O.w4a4_linear_asym(qg, np_of(s).astype(np.float64), zg, qw, sw32.astype(np.float64))
