@@ -319,6 +319,7 @@ def run_ours(args):
             "tq_us": round(tq_i * 1e3, 2), "tq_gbs": round(tq_bytes(T, lin) / (tq_i * 1e-3) / 1e9, 1),
             "tq_tflops": round(tq_flops(T, lin) / (tq_i * 1e-3) / 1e12, 1),
             "gemm_us": round(gm_i * 1e3, 2), "gemm_tops": round(gemm_ops(T, lin) / (gm_i * 1e-3) / 1e12, 1),
+            "gemm_gbs": round(gemm_min_bytes(T, lin) / (gm_i * 1e-3) / 1e9, 1),
         }
 
     # ---- FP16 baseline (torch.matmul / cuBLAS on the same shapes), context for "vs FP16" ----
@@ -435,10 +436,27 @@ def run_ours(args):
 
     gemm_traffic = ncu_traffic(args.config, [L["lin"] for L in layers], "gemm")
     tq_traffic = ncu_traffic(args.config, [L["lin"] for L in layers], "tq")
+    decode = T <= 64     # decode step (C4): the GEMM streams the weights, HBM-bound (SURVEY 8(a) sizes)
+    g_bytes = sum(gemm_min_bytes(T, L["lin"]) for L in layers)
+    if decode:
+        g_gbs = g_bytes / (gemm_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": "fq_w4a4_linear (decode kernel: tcgen05 kind::i8, cluster split-K)",
+                "achieved": round(g_gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": round(g_gbs / pk["hbm_gbs"], 4), "traffic": gemm_traffic,
+                "per": "aggregate of the step's GEMM launches (sum of compulsory bytes / sum of their durations)",
+                "algorithmic_bytes_per_step": int(g_bytes), "tops": round(gemm_tops, 1),
+                "peak_source": f"{peak_src}: hbm_gbs"}
+    else:
+        roof = {"bound": "tensor", "kernel": "fq_w4a4_linear (tcgen05 kind::i8)",
+                "achieved": round(gemm_tops, 1), "peak": round(int8_peak, 1), "unit": "TOPS",
+                "frac": round(gemm_tops / int8_peak, 4), "traffic": gemm_traffic,
+                "per": "aggregate of the step's GEMM launches (sum of 2TNK / sum of their durations)",
+                "algorithmic_bytes_per_step": int(g_bytes),
+                "peak_source": f"{peak_src}: bf16 {pk['bf16_tflops']} TF/s x nominal int8/bf16 ratio 2"}
     if rank == 0:
-        frac = gemm_tops / int8_peak
         out = {
-            "metric": "prefill tokens/s, FlatQuant W4A4 layer linears (transform+quant -> W4A4 GEMM)",
+            "metric": ("decode" if decode else "prefill")
+                      + " tokens/s, FlatQuant W4A4 layer linears (transform+quant -> W4A4 GEMM)",
             "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "fp16 in / int4 x int4 -> int32 / fp16 out",
@@ -448,12 +466,7 @@ def run_ours(args):
                                    for L in layers],
                        "alpha": args.alpha, "parallelism": f"token-shard x{world}",
                        "l2": "flushed (256 MiB write) before every timed step; flush untimed"},
-            "roofline": {"bound": "tensor", "kernel": "fq_w4a4_linear (tcgen05 kind::i8)",
-                         "achieved": round(gemm_tops, 1), "peak": round(int8_peak, 1), "unit": "TOPS",
-                         "frac": round(frac, 4), "traffic": gemm_traffic,
-                         "per": "aggregate of the step's GEMM launches (sum of 2TNK / sum of their durations)",
-                         "algorithmic_bytes_per_step": int(sum(gemm_min_bytes(T, L["lin"]) for L in layers)),
-                         "peak_source": f"{peak_src}: bf16 {pk['bf16_tflops']} TF/s x nominal int8/bf16 ratio 2"},
+            "roofline": roof,
             "tq_roofline": {"bound": "hbm", "kernel": "fq_transform_quant", "achieved": round(tq_gbs, 1),
                             "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(tq_gbs / pk["hbm_gbs"], 4),
                             "traffic": tq_traffic, "algorithmic_bytes_per_step": int(t_bytes),

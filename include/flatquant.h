@@ -101,7 +101,8 @@ fq_status fq_transform_f32(const void* x, int32_t x_dtype, int64_t T, int64_t ld
  *      (fq_weight_colsum, computed once per weight).  Then
  *      Y[t,o] = cvt_rn( float(acc[t,o] - za[t] colsum_w[o]) * sa[t] * sw[o] ), i.e. the
  *      dequantized product s_a (q - z) . s_w q_w.  Asymmetric inputs need the default GEMM
- *      implementation (fq_set_gemm_impl(0)); FQ_ENOTSUP otherwise.
+ *      implementation (fq_set_gemm_impl 0) or a tcgen05 pair / decode one (3-6); FQ_ENOTSUP
+ *      otherwise.
  *   y  [T, N] of y_dtype (FQ_F16 or FQ_BF16), row-major.
  *   Requires K % 32 == 0 and N % 8 == 0.  Exact integer accumulation (|acc| <= 64 K < 2^31).
  * ------------------------------------------------------------------------------------- */
@@ -193,10 +194,13 @@ fq_status fq_kv_quant(const void* kv, int32_t kv_dtype, int64_t R, int64_t ldkv,
 fq_status fq_choose_decomposition(int64_t n, int32_t* n1, int32_t* n2);
 
 /* Selects the GEMM implementation for subsequent calls in this process (testing aid):
- * 0 = default (tcgen05 kind::i8 on a CTA pair, cta_group::2, tile width 192/160/128 features
- * picked per shape to fill the last wave), 1 = legacy mma.sync cross-check kernel, 2 = tcgen05
- * kind::i8 on a single CTA, 3 / 4 / 5 = the pair kernel with the tile width forced to 192 /
- * 160 / 128.  All bit-identical.  Returns FQ_EINVAL otherwise. */
+ * 0 = default (T <= 64: the decode kernel; otherwise tcgen05 kind::i8 on a CTA pair,
+ * cta_group::2, tile width 192/160/128 features picked per shape to fill the last wave),
+ * 1 = legacy mma.sync cross-check kernel, 2 = tcgen05 kind::i8 on a single CTA, 3 / 4 / 5 = the
+ * pair kernel with the tile width forced to 192 / 160 / 128, 6 = the decode kernel forced
+ * (swapped operands: 128 weight rows x T tokens per CTA, K split across a cluster and reduced
+ * through distributed shared memory; T <= 64, FQ_ENOTSUP otherwise).  All bit-identical.
+ * Returns FQ_EINVAL otherwise. */
 fq_status fq_set_gemm_impl(int32_t impl);
 
 /* Selects the transform+quant implementation for subsequent calls in this process (testing

@@ -126,8 +126,13 @@ static fq_status run_gemm(const uint8_t* qa, const float* sa, int64_t T, int32_t
   a.colsum = colsum;
   a.stream = static_cast<cudaStream_t>(stream);
   const int impl = g_gemm_impl.load();
-  // impl 0: pair kernel with the tile width picked per shape; 3 / 4 / 5: forced 192 / 160 / 128
-  const bool pair = impl == 0 || impl >= 3;
+  // impl 0: decode kernel for T <= 64, else the pair kernel with the tile width picked per shape;
+  // 3 / 4 / 5: pair kernel with the width forced to 192 / 160 / 128; 6: decode kernel forced
+  if (impl == 6 || (impl == 0 && gemm_dec_supported(a))) {
+    if (!gemm_dec_supported(a)) return FQ_ENOTSUP;
+    return cuda_status(gemm_dec_launch(a));
+  }
+  const bool pair = impl == 0 || (impl >= 3 && impl <= 5);
   const int bn = impl == 3 ? 192 : impl == 4 ? 160 : impl == 5 ? 128 : 0;
   if (za) {                                        // asymmetric activations: pair kernel only
     if (!pair || !gemm_pair_supported(a)) return FQ_ENOTSUP;
@@ -313,7 +318,7 @@ fq_status fq_set_tq_impl(int32_t impl) {
 }
 
 fq_status fq_set_gemm_impl(int32_t impl) {
-  if (impl < 0 || impl > 5) return FQ_EINVAL;
+  if (impl < 0 || impl > 6) return FQ_EINVAL;
   g_gemm_impl.store(impl);
   return FQ_OK;
 }

@@ -1,0 +1,345 @@
+// fq_gemm_dec.cu -- W4A4 GEMM + dequant for SMALL token counts (decode, T <= 64) on tcgen05.
+//
+//   acc[t,o] = sum_k qa[t,k] qw[o,k]               (Eq.3; PAPER.md:315 INT4 GEMM)
+//   y[t,o]   = cvt_rn(float(acc) * sa[t] * sw[o])  (per-token x per-channel)
+//
+// At decode (64 tokens per step) the linear layer is bound by the weight
+// bytes, not by the tensor pipe: a 256-token pair tile would waste 3/4 of every MMA and leave
+// most SMs idle (48 qkv tiles of 128 features on 148 SMs).  This kernel therefore
+//   * swaps the operands: the MMA's M side is 128 weight rows (output features), its N side the
+//     T <= 64 tokens (N = T rounded up to 16), D[o][t] in TMEM;
+//   * splits K across a thread-block CLUSTER of S CTAs (S <= 8) working on the same 128 features,
+//     and reduces the S int32 partial tiles through distributed shared memory (exact: integer
+//     addition, so the result is bit-identical for every S);
+//   * sizes every CTA to two per SM (about 110 KB shared memory, 64 TMEM columns), so that the
+//     whole grid (num_feature_blocks x S <= 2 x SMs) is resident at once and every CTA streams an
+//     equal share of the weights -- no partial last wave;
+//   * issues the TMA loads of its first weight stages BEFORE griddepcontrol.wait, so the weight
+//     stream overlaps the tail of the transform kernel that produces the activation codes (PDL).
+// Same INT4 -> INT8 widening contract as the other GEMMs (x16 per operand, the accumulator holds
+// 256 acc exactly; the K permutation inside each 32-element group is identical for both operands).
+//
+//   warp 0      : TMA producer (packed weights + packed activations, PSTAGES-deep ring)
+//   warp 1      : MMA issuer (one thread, tcgen05.mma.cta_group::1.kind::i8, both operands smem)
+//   warp 2      : TMEM allocator
+//   warps 4-7   : TMEM -> shared-memory partial tile (lane quarter = warp % 4)
+//   warps 8-15  : converters: packed rows -> widened SWIZZLE_128B K-major operands
+//   all warps   : cluster reduction of the partial tiles + dequant epilogue (coalesced stores)
+#include <cstdint>
+#include <cstdlib>
+#include <cuda_runtime.h>
+#include "fq_device.cuh"
+#include "fq_internal.h"
+#include "fq_tc05.cuh"
+
+namespace fq {
+namespace gd {
+
+constexpr int BM = 128;                       // output features per CTA (MMA M)
+constexpr int TN_MAX = 64;                    // tokens (MMA N, multiple of 16)
+constexpr int BK = 128;                       // int8 K per stage (one 128-byte swizzle atom)
+constexpr int UK = 32;                        // K per tcgen05.mma kind::i8
+#ifndef FQ_DEC_STAGES
+#define FQ_DEC_STAGES 2
+#endif
+#ifndef FQ_DEC_PSTAGES
+#define FQ_DEC_PSTAGES 5
+#endif
+#ifndef FQ_DEC_MINB
+#define FQ_DEC_MINB 2
+#endif
+constexpr int STAGES = FQ_DEC_STAGES;         // widened operand stages
+constexpr int PSTAGES = FQ_DEC_PSTAGES;       // packed TMA ring
+constexpr int WP_BYTES = BM * BK / 2;         // 8 KB packed weights per stage
+constexpr int AP_BYTES = TN_MAX * BK / 2;     // 4 KB packed activations per stage (max)
+constexpr int P_BYTES = WP_BYTES + AP_BYTES;  // ring stage (1 KB multiple)
+constexpr int WW_BYTES = BM * BK;             // 16 KB widened weights per stage
+constexpr int AW_BYTES = TN_MAX * BK;         // 8 KB widened activations per stage
+constexpr int W_BYTES = WW_BYTES + AW_BYTES;
+constexpr int RED_BYTES = TN_MAX * BM * 4;    // 32 KB int32 partial tile [token][feature]
+constexpr int TMA_WARP = 0, MMA_WARP = 1, ALLOC_WARP = 2;
+constexpr int EPI_WARP0 = 4;                  // warps 4-7 (TMEM lane quarter = warp % 4)
+constexpr int CONV_WARP0 = 8, NUM_CONV_WARPS = 8;
+constexpr int THREADS = (CONV_WARP0 + NUM_CONV_WARPS) * 32;
+constexpr int CONV_THREADS = NUM_CONV_WARPS * 32;
+constexpr int TMEM_COLS = 64;
+constexpr int MAX_SPLIT = 8;                  // portable cluster size
+constexpr size_t SMEM_BYTES = size_t(STAGES) * W_BYTES + size_t(PSTAGES) * P_BYTES + 1024 + 256;
+static_assert(RED_BYTES <= STAGES * W_BYTES, "the partial tile reuses the widened-operand stages");
+static_assert(P_BYTES % 1024 == 0 && W_BYTES % 1024 == 0 && WW_BYTES % 1024 == 0, "1 KB alignment");
+
+FQ_DEVICE void widen8(uint32_t p, uint32_t& lo, uint32_t& hi) {   // 8 nibbles -> 8 x (16 q) int8
+  lo = (p << 4) & 0xF0F0F0F0u;
+  hi = p & 0xF0F0F0F0u;
+}
+
+FQ_DEVICE uint4 ld_cluster128(uint32_t local_addr, uint32_t cta) {
+  uint4 v;
+  asm volatile(
+      "{\n.reg .b32 ra;\n"
+      "mapa.shared::cluster.u32 ra, %4, %5;\n"
+      "ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [ra];\n}\n"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "r"(local_addr), "r"(cta)
+      : "memory");
+  return v;
+}
+
+// One packed 16-byte chunk (32 codes) of row `row` -> 32 widened bytes at K positions 32c..32c+31
+// of a SWIZZLE_128B K-major row (16-byte chunk index ^= row % 8).
+FQ_DEVICE void convert_chunk(uint32_t src, uint32_t dst_rows, int row, int c) {
+  const uint4 pk = tc::lds128(src);
+  uint32_t o[8];
+  widen8(pk.x, o[0], o[1]);
+  widen8(pk.y, o[2], o[3]);
+  widen8(pk.z, o[4], o[5]);
+  widen8(pk.w, o[6], o[7]);
+  const uint32_t rowp = dst_rows + uint32_t(row * 128);
+  tc::sts128(rowp + uint32_t(((2 * c) ^ (row & 7)) << 4), o[0], o[1], o[2], o[3]);
+  tc::sts128(rowp + uint32_t(((2 * c + 1) ^ (row & 7)) << 4), o[4], o[5], o[6], o[7]);
+}
+
+template <bool OUT_I32, bool BF16, bool ASYM>
+__global__ void __launch_bounds__(THREADS, FQ_DEC_MINB)
+gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA,
+                const float* __restrict__ sa, int T, int TN, int K, const float* __restrict__ sw, int N,
+                void* __restrict__ yv, const int8_t* __restrict__ za, const int32_t* __restrict__ colsum,
+                int S) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sW = smem;                                        // widened stages [W 16 KB | A 8 KB]
+  uint8_t* sP = smem + size_t(STAGES) * W_BYTES;             // packed ring    [W 8 KB | A 4 KB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + size_t(PSTAGES) * P_BYTES);
+  uint64_t* full = bars;                   // [STAGES]  converters -> MMA
+  uint64_t* empty = bars + STAGES;         // [STAGES]  MMA commit -> converters
+  uint64_t* pfull = bars + 2 * STAGES;     // [PSTAGES] TMA -> converters
+  uint64_t* pempty = pfull + PSTAGES;      // [PSTAGES] converter warps -> TMA
+  uint64_t* tfull = pempty + PSTAGES;      // [1]       last MMA commit -> partial-tile warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = S > 1 ? int(tc::cluster_ctarank()) : 0;
+  const int fb = blockIdx.x / S;                             // feature block of this cluster
+  const int NKB = (K + BK - 1) / BK;
+  const int kb0 = rank * NKB / S, kb1 = (rank + 1) * NKB / S, nk = kb1 - kb0;
+  const uint32_t idesc = tc::idesc_i8(BM, TN);
+  const int ap_bytes = TN * (BK / 2);
+
+  if (warp == MMA_WARP && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], NUM_CONV_WARPS);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < PSTAGES; ++s) {
+      tc::mbar_init(&pfull[s], 1);
+      tc::mbar_init(&pempty[s], NUM_CONV_WARPS);
+    }
+    tc::mbar_init(tfull, 1);
+    tc::fence_barrier_init();
+    tc::tma_prefetch_desc(&tmW);
+    tc::tma_prefetch_desc(&tmA);
+  }
+  if (warp == ALLOC_WARP) tc::tmem_alloc(tmem_slot, TMEM_COLS);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) tc::griddep_launch();   // the next kernel may start launching (PDL)
+
+  if (warp == TMA_WARP) {
+    // ======================= TMA producer =======================
+    if (lane == 0) {
+      // the weights do not depend on the previous kernel: start streaming them before the wait
+      const int pre = nk < PSTAGES ? nk : PSTAGES;
+      for (int j = 0; j < pre; ++j) {
+        tc::mbar_expect_tx(&pfull[j], uint32_t(WP_BYTES + ap_bytes));
+        tc::tma_load_2d(sP + size_t(j) * P_BYTES, &tmW, &pfull[j], (kb0 + j) * (BK / 2), fb * BM);
+      }
+      tc::griddep_wait();                        // qa written by the transform kernel is visible
+      for (int j = 0; j < pre; ++j)
+        tc::tma_load_2d(sP + size_t(j) * P_BYTES + WP_BYTES, &tmA, &pfull[j], (kb0 + j) * (BK / 2), 0);
+      for (int j = pre; j < nk; ++j) {
+        const int sp = j % PSTAGES;
+        tc::mbar_wait(&pempty[sp], ((j / PSTAGES) & 1) ^ 1);
+        tc::mbar_expect_tx(&pfull[sp], uint32_t(WP_BYTES + ap_bytes));
+        uint8_t* dst = sP + size_t(sp) * P_BYTES;
+        tc::tma_load_2d(dst, &tmW, &pfull[sp], (kb0 + j) * (BK / 2), fb * BM);
+        tc::tma_load_2d(dst + WP_BYTES, &tmA, &pfull[sp], (kb0 + j) * (BK / 2), 0);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= CONV_WARP0) {
+    // ======================= converters =======================
+    // tasks per stage: BM weight rows x 4 chunks, then TN activation rows x 4 chunks; a warp's
+    // 32 tasks cover 8 consecutive rows (conflict-free 16-byte loads and swizzled stores)
+    const int ct = threadIdx.x - CONV_WARP0 * 32;
+    const int ntask = (BM + TN) * 4;
+    for (int j = 0; j < nk; ++j) {
+      const int sp = j % PSTAGES, st = j % STAGES;
+      tc::mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1);
+      tc::mbar_wait(&pfull[sp], (j / PSTAGES) & 1);
+      const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES);
+      const uint32_t dst = smem_u32(sW + size_t(st) * W_BYTES);
+      for (int task = ct; task < ntask; task += CONV_THREADS) {
+        const int row = task >> 2, c = task & 3;
+        if (row < BM) convert_chunk(src + uint32_t(task * 16), dst, row, c);
+        else convert_chunk(src + uint32_t(WP_BYTES + (task - 4 * BM) * 16), dst + WW_BYTES, row - BM, c);
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&pempty[sp]);   // packed slot consumed (stored above)
+      tc::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&full[st]);
+    }
+  } else if (warp == MMA_WARP) {
+    // ======================= MMA issuer =======================
+    if (lane == 0) {
+      for (int j = 0; j < nk; ++j) {
+        const int st = j % STAGES;
+        tc::mbar_wait(&full[st], (j / STAGES) & 1);
+        tc::fence_after();
+        const uint32_t w0 = smem_u32(sW + size_t(st) * W_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / UK; ++k)
+          tc::mma_ss<true>(tmem_base, tc::sdesc_sw128(w0 + k * UK, 16, 1024),
+                           tc::sdesc_sw128(w0 + WW_BYTES + k * UK, 16, 1024), idesc, (j | k) != 0);
+        tc::mma_commit(&empty[st]);
+      }
+      tc::mma_commit(tfull);
+    }
+    __syncwarp();
+  } else if (warp >= EPI_WARP0) {
+    // ======================= TMEM -> shared-memory partial tile =======================
+    tc::mbar_wait(tfull, 0);
+    tc::fence_after();
+    const int q = warp & 3, f = q * 32 + lane;
+    int32_t* red = reinterpret_cast<int32_t*>(sW);           // [token][BM] (MMAs have finished)
+    for (int c = 0; c < TN / 16; ++c) {
+      uint32_t v[16];
+      tc::tmem_ld16(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(c * 16), v);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) red[(c * 16 + i) * BM + f] = int32_t(v[i]);
+    }
+  }
+
+  // ======================= cluster reduction + dequant epilogue (all warps) =======================
+  tc::griddep_wait();                          // sa / za of the previous kernel are visible to every thread
+  tc::fence_before();
+  __syncthreads();
+  if (S > 1) tc::cluster_sync();               // every CTA's partial tile is in its shared memory
+  {
+    const int groups = TN * (BM / 4);          // 4 consecutive features of one token per group
+    const int g0 = rank * groups / S, g1 = (rank + 1) * groups / S;
+    const uint32_t red0 = smem_u32(sW);
+    for (int g = g0 + int(threadIdx.x); g < g1; g += THREADS) {
+      const int t = g / (BM / 4), f0 = (g % (BM / 4)) * 4;
+      const int o = fb * BM + f0;
+      int4 acc = make_int4(0, 0, 0, 0);
+      for (int r = 0; r < S; ++r) {            // fixed order; integer sums are exact anyway
+        const uint4 p = S > 1 ? ld_cluster128(red0 + uint32_t(g * 16), uint32_t(r))
+                              : tc::lds128(red0 + uint32_t(g * 16));
+        acc.x += int(p.x);
+        acc.y += int(p.y);
+        acc.z += int(p.z);
+        acc.w += int(p.w);
+      }
+      if (t >= T || o >= N) continue;          // N % 8 == 0: a group is all in or all out
+      if constexpr (OUT_I32) {
+        *reinterpret_cast<int4*>(static_cast<int32_t*>(yv) + size_t(t) * N + o) =
+            make_int4(acc.x >> 8, acc.y >> 8, acc.z >> 8, acc.w >> 8);
+      } else {
+        if constexpr (ASYM) {                  // acc_true = acc - (z - 8) colsum_w; TMEM held 256 acc
+          const int zc = int(za[t]) * 256;
+          const int4 cs = __ldg(reinterpret_cast<const int4*>(colsum + o));
+          acc.x -= zc * cs.x;
+          acc.y -= zc * cs.y;
+          acc.z -= zc * cs.z;
+          acc.w -= zc * cs.w;
+        }
+        const float s_a = sa[t] * (1.0f / 256.0f);
+        const float4 w = __ldg(reinterpret_cast<const float4*>(sw + o));
+        const float f0v = float(acc.x) * s_a * w.x, f1v = float(acc.y) * s_a * w.y;
+        const float f2v = float(acc.z) * s_a * w.z, f3v = float(acc.w) * s_a * w.w;
+        uint2 out;
+        if constexpr (BF16) {
+          __nv_bfloat162 h0 = __floats2bfloat162_rn(f0v, f1v), h1 = __floats2bfloat162_rn(f2v, f3v);
+          out = make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+          *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(yv) + size_t(t) * N + o) = out;
+        } else {
+          out = make_uint2(pack_half2(f0v, f1v), pack_half2(f2v, f3v));
+          *reinterpret_cast<uint2*>(static_cast<__half*>(yv) + size_t(t) * N + o) = out;
+        }
+      }
+    }
+  }
+  if (S > 1) tc::cluster_sync();               // peers have finished reading this CTA's tile
+  else __syncthreads();
+  if (warp == ALLOC_WARP) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+}  // namespace gd
+
+bool gemm_dec_supported(const GemmArgs& a) {
+  return a.T >= 1 && a.T <= gd::TN_MAX && a.K % 32 == 0 && a.K <= 131072 && a.N % 8 == 0 && tmap_available();
+}
+
+// Split: the largest S <= 8 (and <= the number of K-blocks) that keeps the whole grid resident
+// at two CTAs per SM; shapes with more feature blocks than that run unsplit.
+int gemm_dec_pick_split(int N, int K) {
+  const int fbs = (N + gd::BM - 1) / gd::BM;
+  const int nkb = (K + gd::BK - 1) / gd::BK;
+  const int slots = FQ_DEC_MINB * num_sms();
+  int s = 1;
+  for (int c = 2; c <= gd::MAX_SPLIT && c <= nkb; ++c)
+    if (fbs * c <= slots) s = c;
+  return s;
+}
+
+cudaError_t gemm_dec_launch(const GemmArgs& a, int split) {
+  using namespace gd;
+  const bool asym = a.za != nullptr && !a.out_i32;
+  auto kern = a.out_i32 ? gemm_dec_kernel<true, false, false>
+              : asym    ? (a.y_bf16 ? gemm_dec_kernel<false, true, true> : gemm_dec_kernel<false, false, true>)
+                        : (a.y_bf16 ? gemm_dec_kernel<false, true, false> : gemm_dec_kernel<false, false, false>);
+  static bool attr_done[5] = {false, false, false, false, false};
+  const int which = a.out_i32 ? 0 : (a.y_bf16 ? 1 : 2) + (asym ? 2 : 0);
+  if (!attr_done[which]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    if (e != cudaSuccess) return e;
+    attr_done[which] = true;
+  }
+  const int TN = int((a.T + 15) / 16) * 16;
+  CUtensorMap mw{}, ma{};
+  {
+    const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.N)};
+    const uint64_t strides[1] = {uint64_t(a.K / 2)};
+    const uint32_t box[2] = {BK / 2, BM};
+    if (!tmap_encode(&mw, a.qw, 1, 2, dims, strides, box, TMAP_SW_NONE)) return cudaErrorInvalidValue;
+  }
+  {
+    const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.T)};
+    const uint64_t strides[1] = {uint64_t(a.K / 2)};
+    const uint32_t box[2] = {BK / 2, uint32_t(TN)};
+    if (!tmap_encode(&ma, a.qa, 1, 2, dims, strides, box, TMAP_SW_NONE)) return cudaErrorInvalidValue;
+  }
+  const int nkb = (a.K + BK - 1) / BK;
+  static const int env_split = [] {                 // FQ_DEC_SPLIT: testing aid (forces S)
+    const char* v = std::getenv("FQ_DEC_SPLIT");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (split <= 0) split = env_split;
+  int S = split > 0 ? split : gemm_dec_pick_split(a.N, a.K);
+  S = std::max(1, std::min({S, MAX_SPLIT, nkb}));
+  const int fbs = (a.N + BM - 1) / BM;
+  cudaError_t e = launch_pdl(kern, dim3(unsigned(fbs * S)), dim3(THREADS), SMEM_BYTES, a.stream, S, mw, ma, a.sa,
+                             int(a.T), TN, a.K, a.sw, a.N, a.y, a.za, a.colsum, S);
+  count_launch();
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+}  // namespace fq

@@ -109,6 +109,9 @@ bool gemm_tc05_supported(const GemmArgs& a);
 cudaError_t gemm_pair_launch(const GemmArgs& a, int bn = 0);   // tcgen05 kind::i8, CTA pair (cta_group::2);
                                                           // bn: tile width 192/160/128, 0 = per shape
 int gemm_pair_pick_bn(int64_t T, int N, int clusters);
+cudaError_t gemm_dec_launch(const GemmArgs& a, int split = 0);  // decode (T <= 64): swapped operands,
+bool gemm_dec_supported(const GemmArgs& a);                     // cluster split-K; split 0 = per shape
+int gemm_dec_pick_split(int N, int K);
 bool gemm_pair_supported(const GemmArgs& a);
 size_t weight_prep_workspace(int n1, int n2);
 cudaError_t inverse_t_launch(const void* p, int n, bool bf16, void* aug, void* out, int* status,

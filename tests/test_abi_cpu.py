@@ -104,7 +104,7 @@ def test_w4a4_linear_validation():
     lib = fq.load()
     assert lib.fq_w4a4_gemm_i32(A16, 8, 40, A16, 16, A16, None) == _lib.FQ_ESHAPE
     assert lib.fq_w4a4_gemm_i32(None, 8, 64, A16, 16, A16, None) == _lib.FQ_EINVAL
-    assert lib.fq_set_gemm_impl(6) == _lib.FQ_EINVAL and lib.fq_set_gemm_impl(-1) == _lib.FQ_EINVAL
+    assert lib.fq_set_gemm_impl(7) == _lib.FQ_EINVAL and lib.fq_set_gemm_impl(-1) == _lib.FQ_EINVAL
 
 
 def kvq(**kw):

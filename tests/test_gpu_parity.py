@@ -167,6 +167,64 @@ def test_gemm_i32_bit_exact(impl, T, N, K):
     assert np.array_equal(np_of(acc).astype(np.int64), ref)
 
 
+# Decode kernel (impl 6; the default for T <= 64): swapped operands, K split across a cluster of
+# S CTAs reduced through distributed shared memory.  The shapes cover S = 1 (one K-block;
+# 224 feature blocks), S = 4 (ragged N and K), S = 6 (qkv) and S = 8 (down_proj), ragged token
+# counts (MMA N = T rounded up to 16) and the 64-token maximum.
+DEC_SHAPES = [(8, 32), (24, 96), (264, 416), (200, 352), (6144, 4096), (4096, 14336), (28672, 4096)]
+
+
+@pytest.mark.parametrize("impl", [0, 6])
+@pytest.mark.parametrize("T", [1, 7, 16, 33, 64])
+@pytest.mark.parametrize("N,K", DEC_SHAPES)
+def test_gemm_decode_i32_bit_exact(impl, T, N, K):
+    qa = synth.random_codes(T, K, seed=T + 11, tag="qa")
+    qw = synth.random_codes(N, K, seed=N + 11, tag="qw")
+    fq.fq_set_gemm_impl(impl)
+    try:
+        acc = fq.w4a4_gemm_i32(to_dev(O.pack_int4(qa)), to_dev(O.pack_int4(qw)))
+        torch.cuda.synchronize()
+    finally:
+        fq.fq_set_gemm_impl(0)
+    assert np.array_equal(np_of(acc).astype(np.int64), O.int_gemm(qa, qw))
+
+
+def test_gemm_decode_extreme_values_and_limits():
+    """Extreme codes at the largest K of the configs (|acc| = 64 K) through an 8-way split, and
+    T = 65 (one past the decode kernel's limit) is refused when the decode kernel is forced."""
+    T, N, K = 64, 264, 28672
+    qa = np.full((T, K), -8, np.int8)
+    qw = np.full((N, K), -8, np.int8)
+    qw[1::2] = 7
+    fq.fq_set_gemm_impl(6)
+    try:
+        acc = fq.w4a4_gemm_i32(to_dev(O.pack_int4(qa)), to_dev(O.pack_int4(qw)))
+        torch.cuda.synchronize()
+        assert np.array_equal(np_of(acc).astype(np.int64), O.int_gemm(qa, qw))
+        qa65 = to_dev(O.pack_int4(np.zeros((65, 64), np.int8)))
+        qw65 = to_dev(O.pack_int4(np.zeros((8, 64), np.int8)))
+        with pytest.raises(RuntimeError, match="ENOTSUP"):
+            fq.w4a4_gemm_i32(qa65, qw65)
+    finally:
+        fq.fq_set_gemm_impl(0)
+
+
+@pytest.mark.parametrize("out_dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("T", [1, 29, 64])
+def test_w4a4_linear_dequant_decode(out_dtype, T):
+    N, K = 776, 2080
+    qa = synth.random_codes(T, K, seed=3, tag="qa")
+    qw = synth.random_codes(N, K, seed=4, tag="qw")
+    sa = synth.random_scales(T, seed=3, tag="sa")
+    sw = synth.random_scales(N, seed=4, tag="sw")
+    y = fq.w4a4_linear(to_dev(O.pack_int4(qa)), to_dev(sa), to_dev(O.pack_int4(qw)), to_dev(sw), out_dtype)
+    torch.cuda.synchronize()
+    ref = O.w4a4_linear(qa, sa, qw, sw)
+    parity.check_output(np_of(y), ref, label="w4a4_linear decode")
+    ulp = 2.0 ** -10 if out_dtype == torch.float16 else 2.0 ** -7
+    assert np.all(np.abs(np_of(y) - ref) <= ulp * np.abs(ref) + 1e-6)
+
+
 def test_gemm_i32_extreme_values():
     T, N, K = 130, 264, 28672
     qa = np.full((T, K), -8, np.int8)
@@ -333,13 +391,13 @@ def test_weight_colsum_exact():
     assert np.array_equal(np_of(cs).astype(np.int64), qw.astype(np.int64).sum(1))
 
 
-@pytest.mark.parametrize("impl", [0, 4])
+@pytest.mark.parametrize("impl,T", [(0, 1037), (4, 1037), (0, 64), (6, 23)])
 @pytest.mark.parametrize("out_dtype", [torch.float16, torch.bfloat16])
-def test_asym_linear_vs_oracle(out_dtype, impl):
+def test_asym_linear_vs_oracle(out_dtype, impl, T):
     """Asymmetric activations through the GEMM: Y = s_a s_w (acc - (z - 8) colsum_w) equals the
     oracle's dequantized product of the GPU's own codes (per token, fp16/bf16 output rounding),
     and the whole chain stays within the end-to-end Frobenius bar of the oracle's codes."""
-    T, n1, n2, N = 1037, 64, 64, 1544
+    n1, n2, N = 64, 64, 1544
     x, p1, p2 = make_inputs(T, n1, n2, seed=17)
     w = synth.weights(N, n1 * n2, seed=17)
     qw, sw, _ = O.prepare_weight(w, p1.float().numpy(), p2.float().numpy(), 1.0)
