@@ -35,6 +35,23 @@
 namespace fq {
 namespace gd {
 
+// Optional device timeline of 4 CTAs (build with -DFQ_TRACE; scripts/trace_dec.py): globaltimer
+// stamps of [0] start, [1] setup done, [2] TMA issue of stage j (4+j), converters done (40+j),
+// MMA issued (76+j), [112] tfull, [113] partial tile stored, [114] reduced, [115] end.
+#ifdef FQ_TRACE
+__device__ unsigned long long g_dtrace[4 * 128];
+__device__ int g_dtrace_cta[4];
+FQ_DEVICE void dtrace(int slot, int ev) {
+  if (slot >= 0 && ev < 128) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+    g_dtrace[slot * 128 + ev] = t;
+  }
+}
+#else
+FQ_DEVICE void dtrace(int, int) {}
+#endif
+
 constexpr int BM = 128;                       // output features per CTA (MMA M)
 constexpr int TN_MAX = 64;                    // tokens (MMA N, multiple of 16)
 constexpr int BK = 128;                       // int8 K per stage (one 128-byte swizzle atom)
@@ -104,7 +121,7 @@ __global__ void __launch_bounds__(THREADS, FQ_DEC_MINB)
 gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA,
                 const float* __restrict__ sa, int T, int TN, int K, const float* __restrict__ sw, int N,
                 void* __restrict__ yv, const int8_t* __restrict__ za, const int32_t* __restrict__ colsum,
-                int S) {
+                int S, const uint8_t* __restrict__ qw_raw) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;                                        // widened stages [W 16 KB | A 8 KB]
@@ -118,6 +135,8 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tslot = blockIdx.x < 2 ? int(blockIdx.x) : (blockIdx.x + 2 >= gridDim.x ? int(blockIdx.x + 4 - gridDim.x) : -1);
+  if (threadIdx.x == 0) dtrace(tslot, 0);
   const int rank = S > 1 ? int(tc::cluster_ctarank()) : 0;
   const int fb = blockIdx.x / S;                             // feature block of this cluster
   const int NKB = (K + BK - 1) / BK;
@@ -145,13 +164,35 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   tc::fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) tc::griddep_launch();   // the next kernel may start launching (PDL)
+  if (threadIdx.x == 0) dtrace(tslot, 1);
 
   if (warp == TMA_WARP) {
     // ======================= TMA producer =======================
+#ifndef FQ_DEC_NO_L2PF
+    // The stage loads fetch 64 bytes per weight row; issued one K-block at a time across the whole
+    // GPU they hit DRAM as short scattered bursts.  Prefetching each row's whole K range of this
+    // CTA into L2 up front (one bulk request per row, contiguous bytes) streams the weights in long
+    // bursts; the stage loads then hit L2.
+    {
+      const int kbytes0 = kb0 * (BK / 2), kbytes = nk * (BK / 2);
+      const int row_bytes = K / 2;
+      for (int r = lane; r < BM; r += 32) {
+        const int row = fb * BM + r;
+        if (row < N) {
+          const uint8_t* src = qw_raw + size_t(row) * row_bytes + kbytes0;
+          const int len = (kbytes0 + kbytes <= row_bytes ? kbytes : row_bytes - kbytes0) & ~15;
+          if (len > 0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(len) : "memory");
+        }
+      }
+      __syncwarp();
+    }
+#endif
     if (lane == 0) {
       // the weights do not depend on the previous kernel: start streaming them before the wait
       const int pre = nk < PSTAGES ? nk : PSTAGES;
       for (int j = 0; j < pre; ++j) {
+        if (j < 36) dtrace(tslot, 4 + j);
         tc::mbar_expect_tx(&pfull[j], uint32_t(WP_BYTES + ap_bytes));
         tc::tma_load_2d(sP + size_t(j) * P_BYTES, &tmW, &pfull[j], (kb0 + j) * (BK / 2), fb * BM);
       }
@@ -161,6 +202,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       for (int j = pre; j < nk; ++j) {
         const int sp = j % PSTAGES;
         tc::mbar_wait(&pempty[sp], ((j / PSTAGES) & 1) ^ 1);
+        if (j < 36) dtrace(tslot, 4 + j);
         tc::mbar_expect_tx(&pfull[sp], uint32_t(WP_BYTES + ap_bytes));
         uint8_t* dst = sP + size_t(sp) * P_BYTES;
         tc::tma_load_2d(dst, &tmW, &pfull[sp], (kb0 + j) * (BK / 2), fb * BM);
@@ -190,6 +232,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       tc::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&full[st]);
+      if (threadIdx.x == CONV_WARP0 * 32 && j < 36) dtrace(tslot, 40 + j);
     }
   } else if (warp == MMA_WARP) {
     // ======================= MMA issuer =======================
@@ -204,6 +247,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
           tc::mma_ss<true>(tmem_base, tc::sdesc_sw128(w0 + k * UK, 16, 1024),
                            tc::sdesc_sw128(w0 + WW_BYTES + k * UK, 16, 1024), idesc, (j | k) != 0);
         tc::mma_commit(&empty[st]);
+        if (j < 36) dtrace(tslot, 76 + j);
       }
       tc::mma_commit(tfull);
     }
@@ -212,6 +256,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     // ======================= TMEM -> shared-memory partial tile =======================
     tc::mbar_wait(tfull, 0);
     tc::fence_after();
+    if (threadIdx.x == EPI_WARP0 * 32) dtrace(tslot, 112);
     const int q = warp & 3, f = q * 32 + lane;
     int32_t* red = reinterpret_cast<int32_t*>(sW);           // [token][BM] (MMAs have finished)
     for (int c = 0; c < TN / 16; ++c) {
@@ -228,6 +273,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   tc::fence_before();
   __syncthreads();
   if (S > 1) tc::cluster_sync();               // every CTA's partial tile is in its shared memory
+  if (threadIdx.x == 0) dtrace(tslot, 113);
   {
     const int groups = TN * (BM / 4);          // 4 consecutive features of one token per group
     const int g0 = rank * groups / S, g1 = (rank + 1) * groups / S;
@@ -273,8 +319,10 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       }
     }
   }
+  if (threadIdx.x == 0) dtrace(tslot, 114);
   if (S > 1) tc::cluster_sync();               // peers have finished reading this CTA's tile
   else __syncthreads();
+  if (threadIdx.x == 0) dtrace(tslot, 115);
   if (warp == ALLOC_WARP) {
     tc::fence_after();
     tc::tmem_dealloc(tmem_base, TMEM_COLS);
@@ -282,6 +330,12 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
 }
 
 }  // namespace gd
+
+#ifdef FQ_TRACE
+extern "C" int fq_debug_trace_dec(unsigned long long* out) {
+  return int(cudaMemcpyFromSymbol(out, gd::g_dtrace, sizeof(unsigned long long) * 512));
+}
+#endif
 
 bool gemm_dec_supported(const GemmArgs& a) {
   return a.T >= 1 && a.T <= gd::TN_MAX && a.K % 32 == 0 && a.K <= 131072 && a.N % 8 == 0 && tmap_available();
@@ -336,7 +390,7 @@ cudaError_t gemm_dec_launch(const GemmArgs& a, int split) {
   S = std::max(1, std::min({S, MAX_SPLIT, nkb}));
   const int fbs = (a.N + BM - 1) / BM;
   cudaError_t e = launch_pdl(kern, dim3(unsigned(fbs * S)), dim3(THREADS), SMEM_BYTES, a.stream, S, mw, ma, a.sa,
-                             int(a.T), TN, a.K, a.sw, a.N, a.y, a.za, a.colsum, S);
+                             int(a.T), TN, a.K, a.sw, a.N, a.y, a.za, a.colsum, S, a.qw);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

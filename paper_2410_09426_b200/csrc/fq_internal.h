@@ -100,6 +100,8 @@ cudaError_t tq_simt_launch(const TQArgs& a);
 bool tq_tc05_supported(const TQArgs& a);               // tcgen05 / TMA kernel
 bool tq_asym_supported(const TQArgs& a);               // FQ_ASYM available for this shape
 cudaError_t tq_tc05_launch(const TQArgs& a);
+bool tq_wide_supported(const TQArgs& a);               // tcgen05, n1 = 128, n2 in {160, 192, 224, 256}
+cudaError_t tq_wide_launch(const TQArgs& a);
 int tq_impl();
 
 cudaError_t weight_colsum_launch(const uint8_t* qw, int N, int K, int32_t* colsum, cudaStream_t stream);

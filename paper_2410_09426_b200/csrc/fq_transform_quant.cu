@@ -389,17 +389,19 @@ cudaError_t tq_simt_launch(const TQArgs& a) {
 //         so no tie flips); the mma.sync kernel for the remaining instantiated shapes (128 x 224).
 // impl 1: mma.sync where instantiated, else CUDA cores;  impl 2: CUDA cores.
 bool tq_asym_supported(const TQArgs& a) {
-  return (tq_impl() == 0 && tq_tc05_supported(a)) || tq_simt_supported(a.n1, a.n2);
+  return (tq_impl() == 0 && (tq_tc05_supported(a) || tq_wide_supported(a))) || tq_simt_supported(a.n1, a.n2);
 }
 
 cudaError_t transform_quant_launch(const TQArgs& a) {
   const int impl = tq_impl();
   if (a.zero) {                          // asymmetric: tcgen05 kernel, else the CUDA-core kernel
     if (impl == 0 && tq_tc05_supported(a)) return tq_tc05_launch(a);
+    if (impl == 0 && tq_wide_supported(a)) return tq_wide_launch(a);
     return tq_simt_launch(a);
   }
   const bool tc_shape = (a.n1 % 16 == 0) && (a.n2 % 16 == 0);
   if (impl == 0 && tq_tc05_supported(a)) return tq_tc05_launch(a);
+  if (impl == 0 && tq_wide_supported(a)) return tq_wide_launch(a);
   if (impl == 0 && int64_t(a.n1) * a.n2 <= 4096 && tq_simt_supported(a.n1, a.n2)) return tq_simt_launch(a);
   if (impl <= 1 && tc_shape && tq_mma_supported(a.n1, a.n2)) return tq_mma_launch(a);
   return tq_simt_launch(a);

@@ -47,7 +47,8 @@ def run_tq(x, p1, p2, alpha, n1, n2):
 
 
 SHAPES = [(64, 64), (64, 128), (80, 128), (96, 128), (112, 128), (128, 128),   # tcgen05 kernel
-          (16, 32), (128, 224),                                                   # mma.sync kernel
+          (128, 160), (128, 192), (128, 224),                                     # tcgen05 wide kernel
+          (16, 32),                                                               # mma.sync kernel
           (8, 8), (6, 10), (16, 48), (32, 32), (2, 3 * 2)]                        # CUDA-core kernel
 
 
@@ -101,7 +102,7 @@ def test_transform_special_matrices(n1, n2):
     assert np.array_equal(y, x.float().numpy()[:, perm])
 
 
-@pytest.mark.parametrize("n1,n2", [(64, 64), (64, 128), (112, 128)])
+@pytest.mark.parametrize("n1,n2", [(64, 64), (64, 128), (112, 128), (128, 224)])
 @pytest.mark.parametrize("T", [1, 2, 3, 5, 149, 295, 297, 1031])
 def test_transform_tile_tails(n1, n2, T):
     """Token counts around the tile size (2 tokens for n1 = 64) and the grid size (148 SMs):
@@ -114,6 +115,16 @@ def test_transform_tile_tails(n1, n2, T):
     assert np.all(np_of(q[T:]) == 0xAB) and np.all(np_of(s[T:]) == -1.0)     # nothing past T
     qo, so, yo = O.transform_quant(x.float().numpy(), p1.float().numpy(), p2.float().numpy(), 0.9)
     parity.check_transform(np_of(q[:T]), np_of(s[:T]), None, yo, qo, so, label=f"tail T={T}")
+
+
+@pytest.mark.parametrize("alpha", [1.0, 0.9])
+@pytest.mark.parametrize("tdtype", [torch.float16, torch.bfloat16])
+def test_transform_wide_n2_256(alpha, tdtype):
+    """n1 x n2 = 128 x 256 exists only on the wide tcgen05 kernel (P2 alone is 128 KB of smem)."""
+    x, p1, p2 = make_inputs(300, 128, 256, seed=31, tdtype=tdtype)
+    q, s, y = run_tq(x, p1, p2, alpha, 128, 256)
+    qo, so, yo = O.transform_quant(x.float().numpy(), p1.float().numpy(), p2.float().numpy(), alpha)
+    parity.check_transform(q, s, y, yo, qo, so, label="128x256")
 
 
 def test_transform_overflow_stress_fp16():
@@ -368,7 +379,7 @@ def test_gpu_weight_prep_singular():
 
 
 # ---------------------------------------------------------------- asymmetric mode (NEXT-1, R19)
-@pytest.mark.parametrize("n1,n2", [(64, 64), (64, 128), (112, 128), (16, 32), (8, 8)])
+@pytest.mark.parametrize("n1,n2", [(64, 64), (64, 128), (112, 128), (128, 224), (16, 32), (8, 8)])
 @pytest.mark.parametrize("alpha", [1.0, 0.9])
 @pytest.mark.parametrize("tdtype", [torch.float16, torch.bfloat16])
 def test_transform_quant_asym_vs_oracle(n1, n2, alpha, tdtype):
