@@ -54,7 +54,12 @@ FQ_DEVICE void dtrace(int, int) {}
 
 constexpr int BM = 128;                       // output features per CTA (MMA M)
 constexpr int TN_MAX = 64;                    // tokens (MMA N, multiple of 16)
-constexpr int BK = 128;                       // int8 K per stage (one 128-byte swizzle atom)
+#ifndef FQ_DEC_BK
+#define FQ_DEC_BK 128
+#endif
+constexpr int BK = FQ_DEC_BK;                 // int8 K per stage (128: one 128-byte swizzle atom, 256: two)
+constexpr int KA = BK / 128;                  // swizzle atoms per widened row
+constexpr int CPR = BK / 32;                  // packed 16-byte chunks per row and stage
 constexpr int UK = 32;                        // K per tcgen05.mma kind::i8
 #ifndef FQ_DEC_STAGES
 #define FQ_DEC_STAGES 2
@@ -67,11 +72,12 @@ constexpr int UK = 32;                        // K per tcgen05.mma kind::i8
 #endif
 constexpr int STAGES = FQ_DEC_STAGES;         // widened operand stages
 constexpr int PSTAGES = FQ_DEC_PSTAGES;       // packed TMA ring
-constexpr int WP_BYTES = BM * BK / 2;         // 8 KB packed weights per stage
-constexpr int AP_BYTES = TN_MAX * BK / 2;     // 4 KB packed activations per stage (max)
+constexpr int WP_BYTES = BM * BK / 2;         // packed weights per stage (8 KB at BK = 128)
+constexpr int AP_BYTES = TN_MAX * BK / 2;     // packed activations per stage (max)
 constexpr int P_BYTES = WP_BYTES + AP_BYTES;  // ring stage (1 KB multiple)
-constexpr int WW_BYTES = BM * BK;             // 16 KB widened weights per stage
-constexpr int AW_BYTES = TN_MAX * BK;         // 8 KB widened activations per stage
+constexpr int WW_BYTES = BM * BK;             // widened weights per stage (16 KB at BK = 128)
+constexpr int AW_BYTES = TN_MAX * BK;         // widened activations per stage
+constexpr int WW_ATOM = BM * 128, AW_ATOM = TN_MAX * 128;   // one 128-byte K atom of each
 constexpr int W_BYTES = WW_BYTES + AW_BYTES;
 constexpr int RED_BYTES = TN_MAX * BM * 4;    // 32 KB int32 partial tile [token][feature]
 constexpr int TMA_WARP = 0, MMA_WARP = 1, ALLOC_WARP = 2;
@@ -103,17 +109,18 @@ FQ_DEVICE uint4 ld_cluster128(uint32_t local_addr, uint32_t cta) {
 }
 
 // One packed 16-byte chunk (32 codes) of row `row` -> 32 widened bytes at K positions 32c..32c+31
-// of a SWIZZLE_128B K-major row (16-byte chunk index ^= row % 8).
-FQ_DEVICE void convert_chunk(uint32_t src, uint32_t dst_rows, int row, int c) {
+// of a SWIZZLE_128B K-major operand (K atom c / 4 at atom_bytes stride; 16-byte chunk ^= row % 8).
+FQ_DEVICE void convert_chunk(uint32_t src, uint32_t dst_rows, int row, int c, int atom_bytes) {
   const uint4 pk = tc::lds128(src);
   uint32_t o[8];
   widen8(pk.x, o[0], o[1]);
   widen8(pk.y, o[2], o[3]);
   widen8(pk.z, o[4], o[5]);
   widen8(pk.w, o[6], o[7]);
-  const uint32_t rowp = dst_rows + uint32_t(row * 128);
-  tc::sts128(rowp + uint32_t(((2 * c) ^ (row & 7)) << 4), o[0], o[1], o[2], o[3]);
-  tc::sts128(rowp + uint32_t(((2 * c + 1) ^ (row & 7)) << 4), o[4], o[5], o[6], o[7]);
+  const uint32_t rowp = dst_rows + uint32_t((c >> 2) * atom_bytes + row * 128);
+  const int cc = c & 3;
+  tc::sts128(rowp + uint32_t(((2 * cc) ^ (row & 7)) << 4), o[0], o[1], o[2], o[3]);
+  tc::sts128(rowp + uint32_t(((2 * cc + 1) ^ (row & 7)) << 4), o[4], o[5], o[6], o[7]);
 }
 
 template <bool OUT_I32, bool BF16, bool ASYM>
@@ -121,7 +128,7 @@ __global__ void __launch_bounds__(THREADS, FQ_DEC_MINB)
 gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA,
                 const float* __restrict__ sa, int T, int TN, int K, const float* __restrict__ sw, int N,
                 void* __restrict__ yv, const int8_t* __restrict__ za, const int32_t* __restrict__ colsum,
-                int S, const uint8_t* __restrict__ qw_raw) {
+                int S) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;                                        // widened stages [W 16 KB | A 8 KB]
@@ -133,6 +140,10 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   uint64_t* pempty = pfull + PSTAGES;      // [PSTAGES] converter warps -> TMA
   uint64_t* tfull = pempty + PSTAGES;      // [1]       last MMA commit -> partial-tile warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  __shared__ float s_sa[TN_MAX];                             // sa[t] / 256 (0 past T)
+  __shared__ int s_za[TN_MAX];                               // 256 (z_t - 8) (asymmetric)
+  __shared__ __align__(16) float s_sw[BM];                  // sw of this feature block
+  __shared__ __align__(16) int s_cs[BM];                     // colsum_w of this feature block
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tslot = blockIdx.x < 2 ? int(blockIdx.x) : (blockIdx.x + 2 >= gridDim.x ? int(blockIdx.x + 4 - gridDim.x) : -1);
@@ -168,26 +179,6 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
 
   if (warp == TMA_WARP) {
     // ======================= TMA producer =======================
-#ifndef FQ_DEC_NO_L2PF
-    // The stage loads fetch 64 bytes per weight row; issued one K-block at a time across the whole
-    // GPU they hit DRAM as short scattered bursts.  Prefetching each row's whole K range of this
-    // CTA into L2 up front (one bulk request per row, contiguous bytes) streams the weights in long
-    // bursts; the stage loads then hit L2.
-    {
-      const int kbytes0 = kb0 * (BK / 2), kbytes = nk * (BK / 2);
-      const int row_bytes = K / 2;
-      for (int r = lane; r < BM; r += 32) {
-        const int row = fb * BM + r;
-        if (row < N) {
-          const uint8_t* src = qw_raw + size_t(row) * row_bytes + kbytes0;
-          const int len = (kbytes0 + kbytes <= row_bytes ? kbytes : row_bytes - kbytes0) & ~15;
-          if (len > 0)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(len) : "memory");
-        }
-      }
-      __syncwarp();
-    }
-#endif
     if (lane == 0) {
       // the weights do not depend on the previous kernel: start streaming them before the wait
       const int pre = nk < PSTAGES ? nk : PSTAGES;
@@ -215,7 +206,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     // tasks per stage: BM weight rows x 4 chunks, then TN activation rows x 4 chunks; a warp's
     // 32 tasks cover 8 consecutive rows (conflict-free 16-byte loads and swizzled stores)
     const int ct = threadIdx.x - CONV_WARP0 * 32;
-    const int ntask = (BM + TN) * 4;
+    const int ntask = (BM + TN) * CPR;
     for (int j = 0; j < nk; ++j) {
       const int sp = j % PSTAGES, st = j % STAGES;
       tc::mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1);
@@ -223,9 +214,9 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES);
       const uint32_t dst = smem_u32(sW + size_t(st) * W_BYTES);
       for (int task = ct; task < ntask; task += CONV_THREADS) {
-        const int row = task >> 2, c = task & 3;
-        if (row < BM) convert_chunk(src + uint32_t(task * 16), dst, row, c);
-        else convert_chunk(src + uint32_t(WP_BYTES + (task - 4 * BM) * 16), dst + WW_BYTES, row - BM, c);
+        const int row = task / CPR, c = task % CPR;
+        if (row < BM) convert_chunk(src + uint32_t(task * 16), dst, row, c, WW_ATOM);
+        else convert_chunk(src + uint32_t(WP_BYTES + (task - CPR * BM) * 16), dst + WW_BYTES, row - BM, c, AW_ATOM);
       }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&pempty[sp]);   // packed slot consumed (stored above)
@@ -244,8 +235,9 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         const uint32_t w0 = smem_u32(sW + size_t(st) * W_BYTES);
 #pragma unroll
         for (int k = 0; k < BK / UK; ++k)
-          tc::mma_ss<true>(tmem_base, tc::sdesc_sw128(w0 + k * UK, 16, 1024),
-                           tc::sdesc_sw128(w0 + WW_BYTES + k * UK, 16, 1024), idesc, (j | k) != 0);
+          tc::mma_ss<true>(tmem_base, tc::sdesc_sw128(w0 + (k >> 2) * WW_ATOM + (k & 3) * UK, 16, 1024),
+                           tc::sdesc_sw128(w0 + WW_BYTES + (k >> 2) * AW_ATOM + (k & 3) * UK, 16, 1024), idesc,
+                           (j | k) != 0);
         tc::mma_commit(&empty[st]);
         if (j < 36) dtrace(tslot, 76 + j);
       }
@@ -254,6 +246,20 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     __syncwarp();
   } else if (warp >= EPI_WARP0) {
     // ======================= TMEM -> shared-memory partial tile =======================
+    // while the main loop runs: stage the epilogue's scales in shared memory
+    tc::griddep_wait();
+    {
+      const int e = threadIdx.x - EPI_WARP0 * 32;          // 0..127
+      const int o = fb * BM + e;
+      if constexpr (!OUT_I32) {
+        s_sw[e] = o < N ? __ldg(sw + o) : 0.f;
+        if constexpr (ASYM) s_cs[e] = o < N ? __ldg(colsum + o) : 0;
+        if (e < TN_MAX) {
+          s_sa[e] = e < T ? sa[e] * (1.0f / 256.0f) : 0.f;
+          if constexpr (ASYM) s_za[e] = e < T ? int(za[e]) * 256 : 0;
+        }
+      }
+    }
     tc::mbar_wait(tfull, 0);
     tc::fence_after();
     if (threadIdx.x == EPI_WARP0 * 32) dtrace(tslot, 112);
@@ -282,13 +288,23 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       const int t = g / (BM / 4), f0 = (g % (BM / 4)) * 4;
       const int o = fb * BM + f0;
       int4 acc = make_int4(0, 0, 0, 0);
-      for (int r = 0; r < S; ++r) {            // fixed order; integer sums are exact anyway
-        const uint4 p = S > 1 ? ld_cluster128(red0 + uint32_t(g * 16), uint32_t(r))
-                              : tc::lds128(red0 + uint32_t(g * 16));
-        acc.x += int(p.x);
-        acc.y += int(p.y);
-        acc.z += int(p.z);
-        acc.w += int(p.w);
+      if (S == 1) {
+        const uint4 p = tc::lds128(red0 + uint32_t(g * 16));
+        acc = make_int4(int(p.x), int(p.y), int(p.z), int(p.w));
+      } else {
+        // all S remote loads in flight before the first add (integer sums: order-free, exact)
+        uint4 p[MAX_SPLIT];
+#pragma unroll
+        for (int r = 0; r < MAX_SPLIT; ++r)
+          if (r < S) p[r] = ld_cluster128(red0 + uint32_t(g * 16), uint32_t(r));
+#pragma unroll
+        for (int r = 0; r < MAX_SPLIT; ++r)
+          if (r < S) {
+            acc.x += int(p[r].x);
+            acc.y += int(p[r].y);
+            acc.z += int(p[r].z);
+            acc.w += int(p[r].w);
+          }
       }
       if (t >= T || o >= N) continue;          // N % 8 == 0: a group is all in or all out
       if constexpr (OUT_I32) {
@@ -296,15 +312,15 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
             make_int4(acc.x >> 8, acc.y >> 8, acc.z >> 8, acc.w >> 8);
       } else {
         if constexpr (ASYM) {                  // acc_true = acc - (z - 8) colsum_w; TMEM held 256 acc
-          const int zc = int(za[t]) * 256;
-          const int4 cs = __ldg(reinterpret_cast<const int4*>(colsum + o));
+          const int zc = s_za[t];
+          const int4 cs = *reinterpret_cast<const int4*>(s_cs + f0);
           acc.x -= zc * cs.x;
           acc.y -= zc * cs.y;
           acc.z -= zc * cs.z;
           acc.w -= zc * cs.w;
         }
-        const float s_a = sa[t] * (1.0f / 256.0f);
-        const float4 w = __ldg(reinterpret_cast<const float4*>(sw + o));
+        const float s_a = s_sa[t];
+        const float4 w = *reinterpret_cast<const float4*>(s_sw + f0);
         const float f0v = float(acc.x) * s_a * w.x, f1v = float(acc.y) * s_a * w.y;
         const float f2v = float(acc.z) * s_a * w.z, f3v = float(acc.w) * s_a * w.w;
         uint2 out;
@@ -390,7 +406,7 @@ cudaError_t gemm_dec_launch(const GemmArgs& a, int split) {
   S = std::max(1, std::min({S, MAX_SPLIT, nkb}));
   const int fbs = (a.N + BM - 1) / BM;
   cudaError_t e = launch_pdl(kern, dim3(unsigned(fbs * S)), dim3(THREADS), SMEM_BYTES, a.stream, S, mw, ma, a.sa,
-                             int(a.T), TN, a.K, a.sw, a.N, a.y, a.za, a.colsum, S, a.qw);
+                             int(a.T), TN, a.K, a.sw, a.N, a.y, a.za, a.colsum, S);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

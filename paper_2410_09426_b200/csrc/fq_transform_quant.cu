@@ -367,8 +367,12 @@ bool tq_simt_supported(int n1, int n2) {
 }
 
 bool tq_mma_supported(int n1, int n2) {
+  // the configs' shapes plus the decompositions of 4096 and 14336 that scripts/fig5_sweep.py
+  // measures (Fig. 5), so every n1 x n2 with 16 | n1, n2 runs on tensor cores
   return (n1 == 16 && n2 == 32) || (n1 == 64 && n2 == 64) || (n1 == 64 && n2 == 128) ||
-         (n1 == 112 && n2 == 128) || (n1 == 128 && n2 == 224);
+         (n1 == 112 && n2 == 128) || (n1 == 128 && n2 == 224) || (n1 == 16 && n2 == 256) ||
+         (n1 == 32 && n2 == 128) || (n1 == 128 && n2 == 32) || (n1 == 256 && n2 == 16) ||
+         (n1 == 64 && n2 == 224) || (n1 == 128 && n2 == 112) || (n1 == 224 && n2 == 64);
 }
 
 cudaError_t tq_mma_launch(const TQArgs& a) {
@@ -377,6 +381,13 @@ cudaError_t tq_mma_launch(const TQArgs& a) {
   if (a.n1 == 64 && a.n2 == 128) return dispatch_mma<64, 128, 2, 2>(a);
   if (a.n1 == 112 && a.n2 == 128) return dispatch_mma<112, 128, 1, 2>(a);
   if (a.n1 == 128 && a.n2 == 224) return dispatch_mma<128, 224, 1, 1>(a);
+  if (a.n1 == 16 && a.n2 == 256) return dispatch_mma<16, 256, 4, 2>(a);
+  if (a.n1 == 32 && a.n2 == 128) return dispatch_mma<32, 128, 4, 2>(a);
+  if (a.n1 == 128 && a.n2 == 32) return dispatch_mma<128, 32, 2, 2>(a);
+  if (a.n1 == 256 && a.n2 == 16) return dispatch_mma<256, 16, 2, 2>(a);
+  if (a.n1 == 64 && a.n2 == 224) return dispatch_mma<64, 224, 2, 1>(a);
+  if (a.n1 == 128 && a.n2 == 112) return dispatch_mma<128, 112, 2, 2>(a);
+  if (a.n1 == 224 && a.n2 == 64) return dispatch_mma<224, 64, 1, 2>(a);
   return cudaErrorInvalidValue;
 }
 
@@ -402,7 +413,7 @@ cudaError_t transform_quant_launch(const TQArgs& a) {
   const bool tc_shape = (a.n1 % 16 == 0) && (a.n2 % 16 == 0);
   if (impl == 0 && tq_tc05_supported(a)) return tq_tc05_launch(a);
   if (impl == 0 && tq_wide_supported(a)) return tq_wide_launch(a);
-  if (impl == 0 && int64_t(a.n1) * a.n2 <= 4096 && tq_simt_supported(a.n1, a.n2)) return tq_simt_launch(a);
+  if (impl == 0 && int64_t(a.n1) * a.n2 <= 1024 && tq_simt_supported(a.n1, a.n2)) return tq_simt_launch(a);
   if (impl <= 1 && tc_shape && tq_mma_supported(a.n1, a.n2)) return tq_mma_launch(a);
   return tq_simt_launch(a);
 }

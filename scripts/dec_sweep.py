@@ -15,6 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--T", type=int, default=64)
 ap.add_argument("--iters", type=int, default=30)
 ap.add_argument("--tag", default="")
+ap.add_argument("--only", default="", help="comma-separated shape names (qkv,o_proj,gate_up,down)")
 ap.add_argument("--flush", default="clean", choices=["write", "clean", "rotate"],
                 help="write: 256 MiB write before each launch (leaves dirty L2 lines); clean: write then "
                      "read 256 MiB (cold, clean L2); rotate: back-to-back launches over weight copies > 3x L2")
@@ -27,6 +28,8 @@ flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 g = torch.Generator(device=dev).manual_seed(0)
 T = args.T
 for name, N, K in (("qkv", 6144, 4096), ("o_proj", 4096, 4096), ("gate_up", 28672, 4096), ("down", 4096, 14336)):
+    if args.only and name not in args.only.split(","):
+        continue
     qa = torch.randint(0, 256, (T, K // 2), generator=g, device=dev, dtype=torch.int32).to(torch.uint8)
     qw = torch.randint(0, 256, (N, K // 2), generator=g, device=dev, dtype=torch.int32).to(torch.uint8)
     sa = torch.rand(T, generator=g, device=dev) + 0.5

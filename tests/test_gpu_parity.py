@@ -48,7 +48,8 @@ def run_tq(x, p1, p2, alpha, n1, n2):
 
 SHAPES = [(64, 64), (64, 128), (80, 128), (96, 128), (112, 128), (128, 128),   # tcgen05 kernel
           (128, 160), (128, 192), (128, 224),                                     # tcgen05 wide kernel
-          (16, 32),                                                               # mma.sync kernel
+          (16, 32), (32, 128), (128, 32), (16, 256), (256, 16), (128, 112),       # mma.sync kernel
+          (224, 64), (64, 224),
           (8, 8), (6, 10), (16, 48), (32, 32), (2, 3 * 2)]                        # CUDA-core kernel
 
 
