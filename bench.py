@@ -386,6 +386,38 @@ def run_ours(args):
                                 "algorithmic_bytes": int(kv_bytes)})
             del kk, vv, outs
 
+    # ---- o_proj with the paper's own online transform: P_o is a x a over
+    #      the a = 32 heads, identity inside each head of 128, i.e. n1 x n2 =
+    #      32 x 128 with P2 = I (p2 = NULL); timed beside the generic 64 x 64 transform the step uses.
+    po = None
+    L_o = next((L for L in layers if L["lin"].name == "P_o"), None)
+    if L_o is not None and L_o["lin"].K == 4096:
+        p_o = torch.linalg.qr(torch.randn((32, 32), generator=torch.Generator(device=dev).manual_seed(7),
+                                          device=dev))[0].half()
+
+        def time_tq(fn):
+            for _ in range(3):
+                fn()
+            ts = []
+            for _ in range(max(5, args.steps)):
+                flush.zero_()
+                torch.cuda._sleep(400_000)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            return sum(ts) / len(ts) * 1e3          # mean: event ticks are coarse (~2 us) on this part
+
+        lin = L_o["lin"]
+        us_paper = time_tq(lambda: fq.fq_transform_quant(L_o["x"], 32, 128, p_o, None, args.alpha, L_o["q"], L_o["s"]))
+        us_generic = time_tq(lambda: fq.fq_transform_quant(L_o["x"], lin.n1, lin.n2, L_o["p1"], L_o["p2"], args.alpha,
+                                                            L_o["q"], L_o["s"]))
+        po = {"transform": "P_o (32x32) x I_128, p2 = NULL (mma.sync, stage 2 skipped)",
+              "us": round(us_paper, 2), "gbs": round(tq_bytes(T, lin) / (us_paper * 1e-6) / 1e9, 1),
+              "generic_64x64_us": round(us_generic, 2), "note": "mean of event-timed launches, L2 flushed"}
+
     # ---- e2e: through the public C ABI with HOST buffers (H2D + hot path + D2H per step) ----
     e2e = None
     if not args.no_e2e:
@@ -476,6 +508,7 @@ def run_ours(args):
             "kernels": kernels,
             "fp16_baseline": fp16,
             "kv_cache_quant": kv,
+            "o_proj_paper_transform": po,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

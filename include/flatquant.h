@@ -65,7 +65,11 @@ typedef enum { FQ_SYM = 0, FQ_ASYM = 1 } fq_qmode;
  *
  *   x      [T, ldx] elements of x_dtype; row t holds x_t (n = n1*n2 used), ldx >= n.
  *          Viewed as V_t = reshape(x_t, n1, n2) in C order.
- *   p1     [n1, n1] row-major, x_dtype.     p2 [n2, n2] row-major, x_dtype.
+ *   p1     [n1, n1] row-major, x_dtype.     p2 [n2, n2] row-major, x_dtype, or NULL for
+ *          P2 = I_{n2}: the paper's online o_proj transform P_o (a x a) applied across the a
+ *          heads of the attention output, identity inside each head of d_head = n2
+ *          (PAPER.md:297 P_v fused, PAPER.md:726 a^2 parameters); stage 2 is skipped.  Shapes
+ *          (n1, n2) in {(32, 128), (64, 128)} and FQ_SYM only; FQ_ENOTSUP otherwise.
  *   alpha  post-sigmoid clipping ratio in (0, 1]; 1 = no clipping.
  *   qmode  FQ_SYM or FQ_ASYM.
  *   q      [T, n/2] uint8 packed codes (output).     scale [T] fp32 (output), s_t.
@@ -151,7 +155,8 @@ fq_status fq_flatquant_linear_host(const void* x_host, void* x_dev, int32_t x_dt
  *   (P1^{-T}, P2^{-T}, alpha_w) -- (P1^{-T})^T W~ P2^{-T} is the weight factor -- and, if
  *   colsum_w is not NULL, fq_weight_colsum.
  *   w       [N, n1 n2] fp16/bf16 (w_dtype), row stride ldw elements.
- *   p1, p2  [n1, n1], [n2, n2] row-major, same dtype (the activation-side transforms).
+ *   p1, p2  [n1, n1], [n2, n2] row-major, same dtype (the activation-side transforms);
+ *           p2 NULL = I_{n2} as in fq_transform_quant (then P2^{-T} = I).
  *   qw      [N, n1 n2 / 2] uint8 (output).  sw [N] fp32 (output).  colsum_w [N] int32 or NULL.
  *   workspace  device buffer of fq_prepare_weight_workspace_size(n1, n2) bytes, 256-byte
  *           aligned; scratch, contents undefined on return.

@@ -56,7 +56,8 @@ static fq_status validate_tq(const void* x, int32_t x_dtype, int64_t T, int64_t 
   if (T < 0 || n1 < 1 || n2 < 1) return FQ_EINVAL;
   if (!(alpha > 0.0f && alpha <= 1.0f)) return FQ_EINVAL;   // also rejects NaN
   if (T == 0) return FQ_OK;
-  if (!x || !p1 || !p2 || !q || !scale) return FQ_EINVAL;
+  if (!x || !p1 || !q || !scale) return FQ_EINVAL;        // p2 == NULL: P2 = I (fq_transform_quant)
+  if (!p2 && !tq_ident2_supported(n1, n2)) return FQ_ENOTSUP;
   const int64_t n = int64_t(n1) * n2;
   if (n % 2 != 0) return FQ_ESHAPE;
   if (ldx < n) return FQ_ESHAPE;
@@ -155,6 +156,7 @@ fq_status fq_transform_quant(const void* x, int32_t x_dtype, int64_t T, int64_t 
                              float* scale, int8_t* zero, void* stream) {
   if (qmode != FQ_SYM && qmode != FQ_ASYM) return FQ_EINVAL;
   if ((qmode == FQ_SYM) != (zero == nullptr)) return FQ_EINVAL;   // zero iff asymmetric
+  if (!p2 && qmode == FQ_ASYM) return FQ_ENOTSUP;                  // P2 = I: symmetric only
   fq_status s = validate_tq(x, x_dtype, T, ldx, n1, n2, p1, p2, alpha, q, scale);
   if (s != FQ_OK || T == 0) return s;
   return run_tq(x, x_dtype, T, ldx, n1, n2, p1, p2, alpha, q, scale, nullptr, zero, stream);
@@ -261,14 +263,16 @@ fq_status fq_prepare_weight(const void* w, int32_t w_dtype, int32_t N, int64_t l
   int h_status[2] = {0, 0};
   s = cuda_status(inverse_t_launch(p1, n1, bf16, aug, inv1, status, st));
   if (s != FQ_OK) return s;
-  s = cuda_status(inverse_t_launch(p2, n2, bf16, aug, inv2, status + 1, st));
-  if (s != FQ_OK) return s;
+  if (p2) {                                        // P2 = I: its inverse transpose is I as well
+    s = cuda_status(inverse_t_launch(p2, n2, bf16, aug, inv2, status + 1, st));
+    if (s != FQ_OK) return s;
+  }
   s = cuda_status(cudaMemcpyAsync(h_status, status, sizeof(h_status), cudaMemcpyDeviceToHost, st));
   if (s != FQ_OK) return s;
   s = cuda_status(cudaStreamSynchronize(st));
   if (s != FQ_OK) return s;
-  if (h_status[0] != 0 || h_status[1] != 0) return FQ_ESINGULAR;
-  s = run_tq(w, w_dtype, N, ldw, n1, n2, inv1, inv2, alpha_w, qw, sw, nullptr, nullptr, stream);
+  if (h_status[0] != 0 || (p2 && h_status[1] != 0)) return FQ_ESINGULAR;
+  s = run_tq(w, w_dtype, N, ldw, n1, n2, inv1, p2 ? inv2 : nullptr, alpha_w, qw, sw, nullptr, nullptr, stream);
   if (s != FQ_OK || !colsum_w) return s;
   return cuda_status(weight_colsum_launch(qw, N, n1 * n2, colsum_w, st));
 }

@@ -26,6 +26,7 @@
 //   warps 8-15  : converters: packed rows -> widened SWIZZLE_128B K-major operands
 //   all warps   : cluster reduction of the partial tiles + dequant epilogue (coalesced stores)
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cuda_runtime.h>
 #include "fq_device.cuh"
@@ -152,6 +153,11 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   const int fb = blockIdx.x / S;                             // feature block of this cluster
   const int NKB = (K + BK - 1) / BK;
   const int kb0 = rank * NKB / S, kb1 = (rank + 1) * NKB / S, nk = kb1 - kb0;
+  // Every CTA reads the same few KB of activation codes per K-block; walking the K-blocks in the
+  // same order would make all CTAs hit the same L2 lines at the same time.  Each CTA starts at a
+  // different K-block instead (integer accumulation: the order does not change the result).
+  const int krot = nk > 0 ? int((unsigned(fb) * 5u + unsigned(rank) * 3u) % unsigned(nk)) : 0;
+  auto kb_of = [&](int j) { const int r = j + krot; return kb0 + (r >= nk ? r - nk : r); };
   const uint32_t idesc = tc::idesc_i8(BM, TN);
   const int ap_bytes = TN * (BK / 2);
 
@@ -185,19 +191,19 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       for (int j = 0; j < pre; ++j) {
         if (j < 36) dtrace(tslot, 4 + j);
         tc::mbar_expect_tx(&pfull[j], uint32_t(WP_BYTES + ap_bytes));
-        tc::tma_load_2d(sP + size_t(j) * P_BYTES, &tmW, &pfull[j], (kb0 + j) * (BK / 2), fb * BM);
+        tc::tma_load_2d(sP + size_t(j) * P_BYTES, &tmW, &pfull[j], kb_of(j) * (BK / 2), fb * BM);
       }
       tc::griddep_wait();                        // qa written by the transform kernel is visible
       for (int j = 0; j < pre; ++j)
-        tc::tma_load_2d(sP + size_t(j) * P_BYTES + WP_BYTES, &tmA, &pfull[j], (kb0 + j) * (BK / 2), 0);
+        tc::tma_load_2d(sP + size_t(j) * P_BYTES + WP_BYTES, &tmA, &pfull[j], kb_of(j) * (BK / 2), 0);
       for (int j = pre; j < nk; ++j) {
         const int sp = j % PSTAGES;
         tc::mbar_wait(&pempty[sp], ((j / PSTAGES) & 1) ^ 1);
         if (j < 36) dtrace(tslot, 4 + j);
         tc::mbar_expect_tx(&pfull[sp], uint32_t(WP_BYTES + ap_bytes));
         uint8_t* dst = sP + size_t(sp) * P_BYTES;
-        tc::tma_load_2d(dst, &tmW, &pfull[sp], (kb0 + j) * (BK / 2), fb * BM);
-        tc::tma_load_2d(dst + WP_BYTES, &tmA, &pfull[sp], (kb0 + j) * (BK / 2), 0);
+        tc::tma_load_2d(dst, &tmW, &pfull[sp], kb_of(j) * (BK / 2), fb * BM);
+        tc::tma_load_2d(dst + WP_BYTES, &tmA, &pfull[sp], kb_of(j) * (BK / 2), 0);
       }
     }
     __syncwarp();
@@ -357,15 +363,55 @@ bool gemm_dec_supported(const GemmArgs& a) {
   return a.T >= 1 && a.T <= gd::TN_MAX && a.K % 32 == 0 && a.K <= 131072 && a.N % 8 == 0 && tmap_available();
 }
 
-// Split: the largest S <= 8 (and <= the number of K-blocks) that keeps the whole grid resident
-// at two CTAs per SM; shapes with more feature blocks than that run unsplit.
-int gemm_dec_pick_split(int N, int K) {
+static int dec_policy() {                         // FQ_DEC_POLICY: testing aid (0/1/2)
+  static const int p = [] {
+    const char* v = std::getenv("FQ_DEC_POLICY");
+    return v ? std::atoi(v) : 2;
+  }();
+  return p;
+}
+
+// How many clusters of S CTAs the hardware keeps resident at once (cluster placement is bounded
+// by the GPC structure, not only by the per-SM limits); cached per S.
+static int dec_max_clusters(const void* kern, int S) {
+  static int cache[gd::MAX_SPLIT + 1] = {0};
+  if (S <= 1) return FQ_DEC_MINB * num_sms();
+  if (cache[S] > 0) return cache[S];
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(S * 64));
+  cfg.blockDim = dim3(gd::THREADS);
+  cfg.dynamicSmemBytes = gd::SMEM_BYTES;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = unsigned(S);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  int na = 1;
+  if (dec_policy() > 0) {
+    attr[1].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+    attr[1].val.clusterSchedulingPolicyPreference =
+        dec_policy() == 1 ? cudaClusterSchedulingPolicySpread : cudaClusterSchedulingPolicyLoadBalancing;
+    na = 2;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = unsigned(na);
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = FQ_DEC_MINB * num_sms() / S;
+  }
+  cache[S] = n;
+  return n;
+}
+
+// Split: the largest S <= 8 (and <= the number of K-blocks) for which every cluster of the grid
+// is resident at once; shapes with more feature blocks than that run unsplit.
+static int dec_pick_split(const void* kern, int N, int K) {
   const int fbs = (N + gd::BM - 1) / gd::BM;
   const int nkb = (K + gd::BK - 1) / gd::BK;
-  const int slots = FQ_DEC_MINB * num_sms();
   int s = 1;
   for (int c = 2; c <= gd::MAX_SPLIT && c <= nkb; ++c)
-    if (fbs * c <= slots) s = c;
+    if (fbs * c <= FQ_DEC_MINB * num_sms() && fbs <= dec_max_clusters(kern, c)) s = c;
   return s;
 }
 
@@ -402,11 +448,15 @@ cudaError_t gemm_dec_launch(const GemmArgs& a, int split) {
     return v ? std::atoi(v) : 0;
   }();
   if (split <= 0) split = env_split;
-  int S = split > 0 ? split : gemm_dec_pick_split(a.N, a.K);
+  int S = split > 0 ? split : dec_pick_split(reinterpret_cast<const void*>(kern), a.N, a.K);
   S = std::max(1, std::min({S, MAX_SPLIT, nkb}));
   const int fbs = (a.N + BM - 1) / BM;
-  cudaError_t e = launch_pdl(kern, dim3(unsigned(fbs * S)), dim3(THREADS), SMEM_BYTES, a.stream, S, mw, ma, a.sa,
-                             int(a.T), TN, a.K, a.sw, a.N, a.y, a.za, a.colsum, S);
+  static const bool dbg = std::getenv("FQ_DEC_DEBUG") != nullptr;
+  if (dbg)
+    std::fprintf(stderr, "[fq] decode GEMM N=%d K=%d T=%lld: split %d, %d CTAs, max resident clusters %d\n", a.N,
+                 a.K, (long long)a.T, S, fbs * S, dec_max_clusters(reinterpret_cast<const void*>(kern), S));
+  cudaError_t e = launch_pdl_policy(kern, dim3(unsigned(fbs * S)), dim3(THREADS), SMEM_BYTES, a.stream, S,
+                                    dec_policy(), mw, ma, a.sa, int(a.T), TN, a.K, a.sw, a.N, a.y, a.za, a.colsum, S);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

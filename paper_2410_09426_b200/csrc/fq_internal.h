@@ -66,14 +66,25 @@ bool pdl_enabled();      // FQ_PDL=0 in the environment disables programmatic de
 // kernel of the stream finishes; it calls griddepcontrol.wait before touching global inputs) and
 // an optional cluster size.
 template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl_policy(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              int cluster_x, int cluster_policy, Args&&... args);
+
+template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                        int cluster_x, Args&&... args) {
+  return launch_pdl_policy(kern, grid, block, smem, stream, cluster_x, 0, std::forward<Args>(args)...);
+}
+
+// cluster_policy: 0 default, 1 spread, 2 load balancing (cudaClusterSchedulingPolicy)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl_policy(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              int cluster_x, int cluster_policy, Args&&... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   int na = 0;
   if (cluster_x > 1) {
     attr[na].id = cudaLaunchAttributeClusterDimension;
@@ -81,6 +92,12 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     attr[na].val.clusterDim.y = 1;
     attr[na].val.clusterDim.z = 1;
     ++na;
+    if (cluster_policy > 0) {
+      attr[na].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+      attr[na].val.clusterSchedulingPolicyPreference =
+          cluster_policy == 1 ? cudaClusterSchedulingPolicySpread : cudaClusterSchedulingPolicyLoadBalancing;
+      ++na;
+    }
   }
   if (pdl_enabled()) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -96,6 +113,8 @@ cudaError_t transform_quant_launch(const TQArgs& a);   // impl selection (fq_set
 bool tq_simt_supported(int n1, int n2);
 bool tq_mma_supported(int n1, int n2);                 // legacy mma.sync kernel instantiations
 cudaError_t tq_mma_launch(const TQArgs& a);
+bool tq_ident2_supported(int n1, int n2);             // P2 = I (p2 == nullptr), mma.sync kernel
+cudaError_t tq_ident2_launch(const TQArgs& a);
 cudaError_t tq_simt_launch(const TQArgs& a);
 bool tq_tc05_supported(const TQArgs& a);               // tcgen05 / TMA kernel
 bool tq_asym_supported(const TQArgs& a);               // FQ_ASYM available for this shape
@@ -113,7 +132,6 @@ cudaError_t gemm_pair_launch(const GemmArgs& a, int bn = 0);   // tcgen05 kind::
 int gemm_pair_pick_bn(int64_t T, int N, int clusters);
 cudaError_t gemm_dec_launch(const GemmArgs& a, int split = 0);  // decode (T <= 64): swapped operands,
 bool gemm_dec_supported(const GemmArgs& a);                     // cluster split-K; split 0 = per shape
-int gemm_dec_pick_split(int N, int K);
 bool gemm_pair_supported(const GemmArgs& a);
 size_t weight_prep_workspace(int n1, int n2);
 cudaError_t inverse_t_launch(const void* p, int n, bool bf16, void* aug, void* out, int* status,

@@ -42,7 +42,10 @@ struct TQCfg {
   static constexpr size_t SMEM = P2_BYTES + size_t(TEAMS) * TEAM_BYTES;
 };
 
-template <int N1, int N2, bool BF16, bool WRITE_Y, int TEAMS, int NBUF>
+// IDENT2: P2 = I (the online o_proj transform P_o (a x a) is applied across
+// the heads of the attention output, identity inside each head), stage 2 is skipped and the fp32
+// stage-1 accumulators are quantized directly (p2 is not read).
+template <int N1, int N2, bool BF16, bool WRITE_Y, int TEAMS, int NBUF, bool IDENT2 = false>
 __global__ void __launch_bounds__(TQCfg<N1, N2, BF16, WRITE_Y, TEAMS, NBUF>::THREADS, 1)
 tq_mma_kernel(const uint16_t* __restrict__ x, int64_t T, int64_t ldx,
               const uint16_t* __restrict__ p1, const uint16_t* __restrict__ p2, float alpha,
@@ -69,7 +72,7 @@ tq_mma_kernel(const uint16_t* __restrict__ x, int64_t T, int64_t ldx,
   // ---- P2 -> smem (whole CTA), padded rows, always as fp16: stage 2 runs in fp16 so the
   //      re-fed intermediate keeps an 11-bit mantissa (a bf16 intermediate fails the code
   //      parity bar).  bf16 -> fp16 is exact for normal-range entries. ----
-  for (int i = threadIdx.x; i < N2 * N2; i += C::THREADS) {
+  for (int i = threadIdx.x; i < (IDENT2 ? 0 : N2 * N2); i += C::THREADS) {
     const int r = i / N2, c = i % N2;
     uint16_t v = p2[i];
     if constexpr (BF16) {
@@ -136,8 +139,9 @@ tq_mma_kernel(const uint16_t* __restrict__ x, int64_t T, int64_t ldx,
         mma_16816<BF16>(acc[n + 1], a1[kt], b2, b3);
       }
     }
+    float m = 0.f, inv_pre = 1.f;
+    if constexpr (!IDENT2) {
     // ---------------- exact power-of-two prescale of the strip ----------------
-    float m = 0.f;
 #pragma unroll
     for (int n = 0; n < NT; ++n)
 #pragma unroll
@@ -145,7 +149,7 @@ tq_mma_kernel(const uint16_t* __restrict__ x, int64_t T, int64_t ldx,
     m = warp_max(m);
     // choose 2^k with m * 2^k in [2^14, 2^15): safe for fp16 (max 65504) and far from
     // its subnormals.
-    float pre = 1.f, inv_pre = 1.f;
+    float pre = 1.f;
     if (m > 0.f) {
       const int e = 14 - ilogbf(m);
       pre = ldexpf(1.f, e);
@@ -176,6 +180,7 @@ tq_mma_kernel(const uint16_t* __restrict__ x, int64_t T, int64_t ldx,
         mma_16816<false>(acc[n + 1], a2[kt], b2, b3);
       }
     }
+    }  // !IDENT2
     // ---------------- per-token absmax (clip applied after the transform) ----------------
     m = 0.f;
 #pragma unroll
@@ -316,10 +321,10 @@ tq_simt_kernel(const TIn* __restrict__ x, int64_t T, int64_t ldx, int n1, int n2
 // ============================================================================================
 // Launchers
 // ============================================================================================
-template <int N1, int N2, bool BF16, bool WRITE_Y, int TEAMS, int NBUF>
+template <int N1, int N2, bool BF16, bool WRITE_Y, int TEAMS, int NBUF, bool IDENT2 = false>
 static cudaError_t launch_mma(const TQArgs& a) {
   using C = TQCfg<N1, N2, BF16, WRITE_Y, TEAMS, NBUF>;
-  auto kern = tq_mma_kernel<N1, N2, BF16, WRITE_Y, TEAMS, NBUF>;
+  auto kern = tq_mma_kernel<N1, N2, BF16, WRITE_Y, TEAMS, NBUF, IDENT2>;
   static bool attr_set = false;  // benign race: idempotent attribute set
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
@@ -343,6 +348,23 @@ static cudaError_t dispatch_mma(const TQArgs& a) {
   if (a.bf16)
     return a.y ? launch_mma<N1, N2, true, true, TEAMS, NBUF>(a) : launch_mma<N1, N2, true, false, TEAMS, NBUF>(a);
   return a.y ? launch_mma<N1, N2, false, true, TEAMS, NBUF>(a) : launch_mma<N1, N2, false, false, TEAMS, NBUF>(a);
+}
+
+template <int N1, int N2, int TEAMS, int NBUF>
+static cudaError_t dispatch_mma_ident(const TQArgs& a) {
+  if (a.bf16)
+    return a.y ? launch_mma<N1, N2, true, true, TEAMS, NBUF, true>(a) : launch_mma<N1, N2, true, false, TEAMS, NBUF, true>(a);
+  return a.y ? launch_mma<N1, N2, false, true, TEAMS, NBUF, true>(a) : launch_mma<N1, N2, false, false, TEAMS, NBUF, true>(a);
+}
+
+bool tq_ident2_supported(int n1, int n2) { return n2 == 128 && (n1 == 32 || n1 == 64); }
+
+// P2 = I (p2 == nullptr): the paper's online o_proj transform P_o (a x a) (x) I_{d_head}
+// (PAPER.md:297, 726), a heads of d_head = 128 (LLaMA-2-7B / LLaMA-3-8B: 32, LLaMA-3-70B: 64).
+cudaError_t tq_ident2_launch(const TQArgs& a) {
+  if (a.n1 == 32 && a.n2 == 128) return dispatch_mma_ident<32, 128, 4, 2>(a);
+  if (a.n1 == 64 && a.n2 == 128) return dispatch_mma_ident<64, 128, 2, 2>(a);
+  return cudaErrorInvalidValue;
 }
 
 template <typename TIn>
@@ -405,6 +427,7 @@ bool tq_asym_supported(const TQArgs& a) {
 
 cudaError_t transform_quant_launch(const TQArgs& a) {
   const int impl = tq_impl();
+  if (a.p2 == nullptr) return tq_ident2_launch(a);     // P2 = I (validated by the ABI layer)
   if (a.zero) {                          // asymmetric: tcgen05 kernel, else the CUDA-core kernel
     if (impl == 0 && tq_tc05_supported(a)) return tq_tc05_launch(a);
     if (impl == 0 && tq_wide_supported(a)) return tq_wide_launch(a);

@@ -1,12 +1,8 @@
 cd /root/repo
 mkdir -p gpurun_out
-cp paper_2410_09426_b200/libflatquant.so /tmp/base.so
-for L in base k256a k256b k128p; do
-  if [ $L != base ]; then cp paper_2410_09426_b200/libflatquant_$L.so paper_2410_09426_b200/libflatquant.so; fi
-  echo "== $L"
-  timeout 300 python -m pytest tests -q -m gpu --timeout 240 -p no:cacheprovider -x -k "decode" 2>&1 | tail -1
-  timeout 120 python scripts/dec_sweep.py --tag $L --flush clean --iters 20
-  timeout 120 python scripts/dec_sweep.py --tag $L --flush rotate --iters 20
-  cp /tmp/base.so paper_2410_09426_b200/libflatquant.so
-done
-timeout 300 python scripts/fig5_sweep.py
+timeout 600 python -m pytest tests -q -m gpu --timeout 240 -p no:cacheprovider -k "decode or asym_linear or chain_llama3_8b" > gpurun_out/pytest_quick.log 2>&1; echo "exit $?" >> gpurun_out/pytest_quick.log
+timeout 120 python scripts/dec_sweep.py --tag rot --flush clean --iters 30
+timeout 120 python scripts/dec_sweep.py --tag rot --flush rotate --iters 30
+for S in 2 4 8; do FQ_DEC_SPLIT=$S timeout 120 python scripts/dec_sweep.py --tag rots$S --flush clean --iters 30; done
+for s in "--N 4096 --K 4096" "--N 28672 --K 4096"; do timeout 60 python scripts/trace_dec.py $s --flush; done
+timeout 300 python bench.py --config C4 --steps 20 --warmup 5 --no-cpu --no-e2e --no-kv > gpurun_out/bench_C4.json 2> gpurun_out/bench_C4.err

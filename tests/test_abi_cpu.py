@@ -75,6 +75,10 @@ def test_transform_quant_validation():
     assert tq(ldx=516) == _lib.FQ_ESHAPE                  # row stride not 16-byte multiple
     assert tq(x=MIS) == _lib.FQ_ESHAPE
     assert tq(n1=512, n2=2, ldx=1024) == _lib.FQ_ENOTSUP
+    # p2 = NULL means P2 = I (the paper's online P_o (x) I_{d_head}); only (32|64, 128), symmetric
+    assert tq(p2=None) == _lib.FQ_ENOTSUP                 # 16 x 32: no P2 = I kernel
+    assert tq(p2=None, n1=32, n2=128, ldx=4096, qmode=1, zero=A16) == _lib.FQ_ENOTSUP
+    assert tq(p2=None, n1=32, n2=128, ldx=4096, T=0) == _lib.FQ_OK
 
 
 def gemm(**kw):

@@ -128,6 +128,38 @@ def test_transform_wide_n2_256(alpha, tdtype):
     parity.check_transform(q, s, y, yo, qo, so, label="128x256")
 
 
+@pytest.mark.parametrize("n1", [32, 64])
+@pytest.mark.parametrize("alpha", [1.0, 0.9])
+@pytest.mark.parametrize("tdtype", [torch.float16, torch.bfloat16])
+def test_transform_p2_identity(n1, alpha, tdtype):
+    """p2 = NULL: the paper's online o_proj transform P_o (a x a) (x) I_{d_head} (PAPER.md:297,
+    726), a = n1 heads of 128; the oracle applies the explicit identity."""
+    n2, T = 128, 301
+    x, p1, _ = make_inputs(T, n1, n2, seed=n1 + 7, tdtype=tdtype)
+    q, s, y = fq.transform_f32(x.to(DEV), n1, n2, p1.to(DEV), None, alpha)
+    torch.cuda.synchronize()
+    qo, so, yo = O.transform_quant(x.float().numpy(), p1.float().numpy(), np.eye(n2), alpha)
+    st = parity.check_transform(np_of(q), np_of(s), np_of(y), yo, qo, so, label=f"P_o x I a={n1}")
+    assert st["mismatch_frac"] <= parity.MISMATCH_FRAC
+    q2, s2 = fq.transform_quant(x.to(DEV), n1, n2, p1.to(DEV), None, alpha)
+    torch.cuda.synchronize()
+    assert torch.equal(q2.cpu(), q.cpu()) and torch.equal(s2.cpu(), s.cpu())
+
+
+def test_gpu_weight_prep_p2_identity():
+    """fq_prepare_weight with p2 = NULL: W' = P1^{-1} W~ (P2 = I, so P2^{-T} = I); parity as in
+    test_gpu_weight_prep_matches_oracle (oracle with the fp16-rounded P1^{-T} and the identity)."""
+    n1, n2, N = 32, 128, 264
+    w = torch.from_numpy(synth.weights(N, n1 * n2, seed=3, dtype=np.float32)).half()
+    p1 = torch.from_numpy(synth.well_conditioned(n1, seed=3, tag="p1", dtype=np.float32)).half()
+    qw, sw = fq.prepare_weight(w.to(DEV), n1, n2, p1.to(DEV), None, 1.0)
+    torch.cuda.synchronize()
+    wf, p1f = w.float().numpy().astype(np.float64), p1.float().numpy().astype(np.float64)
+    p1i_t = torch.from_numpy(np.linalg.inv(p1f).T.copy()).half().float().numpy()
+    qo, so, yo = O.transform_quant(wf, p1i_t, np.eye(n2), 1.0)
+    parity.check_transform(np_of(qw), np_of(sw), None, yo, qo, so, label="weight prep P2 = I")
+
+
 def test_transform_overflow_stress_fp16():
     """A token at +-60000 in every channel: the fp16 intermediate must not overflow (exact
     power-of-two prescale), and zero / tiny tokens must not underflow."""
