@@ -17,6 +17,12 @@
  *    valid until the work queued on `stream` has completed.
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Every call
  *    is asynchronous with respect to the host unless stated otherwise.
+ *  - Parameters vs activations.  The kernels use programmatic dependent launch: a kernel may
+ *    start while the preceding kernels of the stream finish and waits for them only before it
+ *    reads its ACTIVATION inputs (x, qa, sa, za).  Its PARAMETERS (p1, p2, qw, sw, colsum_w)
+ *    are read before that wait, so they must already be written when the call is made: by
+ *    fq_prepare_weight / fq_weight_colsum followed by any synchronisation, or by a copy that
+ *    completed.  (fq_prepare_weight itself returns only after its writes are complete.)
  *  - Argument validation is synchronous: on any error nothing is launched and a non-zero
  *    fq_status is returned.  T == 0 returns FQ_OK without launching.  A failed launch
  *    returns FQ_ECUDA; fq_last_cuda_error() returns the cudaError_t value.  Device faults
@@ -38,7 +44,7 @@
 extern "C" {
 #endif
 
-#define FQ_ABI_VERSION 3   /* 2: FQ_ASYM + fq_weight_colsum; 3: fq_kv_quant, fq_prepare_weight */
+#define FQ_ABI_VERSION 4   /* 2: FQ_ASYM + fq_weight_colsum; 3: fq_kv_quant, fq_prepare_weight; 4: p2 = NULL (P2 = I) */
 
 typedef enum {
   FQ_OK = 0,

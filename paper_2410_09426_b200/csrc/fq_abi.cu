@@ -273,8 +273,14 @@ fq_status fq_prepare_weight(const void* w, int32_t w_dtype, int32_t N, int64_t l
   if (s != FQ_OK) return s;
   if (h_status[0] != 0 || (p2 && h_status[1] != 0)) return FQ_ESINGULAR;
   s = run_tq(w, w_dtype, N, ldw, n1, n2, inv1, p2 ? inv2 : nullptr, alpha_w, qw, sw, nullptr, nullptr, stream);
-  if (s != FQ_OK || !colsum_w) return s;
-  return cuda_status(weight_colsum_launch(qw, N, n1 * n2, colsum_w, st));
+  if (s != FQ_OK) return s;
+  if (colsum_w) {
+    s = cuda_status(weight_colsum_launch(qw, N, n1 * n2, colsum_w, st));
+    if (s != FQ_OK) return s;
+  }
+  // the prepared weights are parameters of the hot-path kernels, which read them before waiting
+  // for the preceding kernel (PDL): return only once they are written
+  return cuda_status(cudaStreamSynchronize(st));
 }
 
 fq_status fq_kv_quant(const void* kv, int32_t kv_dtype, int64_t R, int64_t ldkv, int32_t head_dim,

@@ -23,6 +23,7 @@
 // barrier; the leader's tcgen05.commit multicasts to both CTAs' `empty` / `tfull` barriers;
 // both CTAs' epilogues arrive on the leader's `tempty` barrier.
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 #include <cuda_runtime.h>
 #include "fq_device.cuh"
@@ -581,10 +582,17 @@ static cudaError_t launch_bn(const GemmArgs& a) {
 }
 
 cudaError_t gemm_pair_launch(const GemmArgs& a, int bn) {
+  static const int env_bn = [] {                    // FQ_PAIR_BN: testing aid (forces the width)
+    const char* v = std::getenv("FQ_PAIR_BN");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (bn == 0) bn = env_bn;
   if (bn == 0) bn = gemm_pair_pick_bn(a.T, a.N, std::max(1, num_sms() / 2));
   switch (bn) {
     case 160: return launch_bn<160>(a);
     case 128: return launch_bn<128>(a);
+    case 96: return launch_bn<96>(a);
+    case 64: return launch_bn<64>(a);
     default: return launch_bn<192>(a);
   }
 }

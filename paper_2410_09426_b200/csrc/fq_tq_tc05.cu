@@ -228,10 +228,14 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     }
     tc::fence_barrier_init();
     tc::griddep_launch();              // the next kernel may start launching (PDL)
-    tc::griddep_wait();                // inputs of this kernel are final (PDL)
+    // P1, P2 are parameters (ABI contract: not written by kernels still in flight), so they
+    // stream in while the preceding kernel finishes; X is that kernel's output
     tc::mbar_expect_tx(pfull, C::P1_BYTES + C::P2_BYTES);
     for (int a = 0; a < C::P1_ATOMS; ++a) tc::tma_load_2d(sP1 + a * N1 * 128, &tmP1, pfull, a * 64, 0);
     for (int b = 0; b < C::JB; ++b) tc::tma_load_2d(sP2 + b * N2 * 128, &tmP2, pfull, b * 64, 0);
+    trace(3);
+    tc::griddep_wait();                // inputs of this kernel are final (PDL)
+    trace(4);
     for (int k = 0; k < prefill; ++k) issue_x(k);
     trace(1);
   }

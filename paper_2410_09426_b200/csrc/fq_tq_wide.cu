@@ -147,10 +147,10 @@ tq_wide_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     tc::mbar_init(d2empty, 4);
     tc::fence_barrier_init();
     tc::griddep_launch();              // the next kernel may start launching (PDL)
-    tc::griddep_wait();                // inputs of this kernel are final (PDL)
-    tc::mbar_expect_tx(pfull, C::P1_BYTES + C::P2_BYTES);
+    tc::mbar_expect_tx(pfull, C::P1_BYTES + C::P2_BYTES);   // parameters: before the wait
     for (int a = 0; a < 2; ++a) tc::tma_load_2d(sP1 + a * N1 * 128, &tmP1, pfull, a * 64, 0);
     for (int b = 0; b < C::JB; ++b) tc::tma_load_2d(sP2 + b * N2 * 128, &tmP2, pfull, b * 64, 0);
+    tc::griddep_wait();                // X of the preceding kernel is final (PDL)
     for (int k = 0; k < prefill; ++k) issue_x(k);
   }
   if (warp == 2) tc::tmem_alloc(tmem_slot, 512);

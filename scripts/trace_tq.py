@@ -34,7 +34,7 @@ lib = fq.load()
 buf = (ctypes.c_ulonglong * (4 * 256))()
 lib.fq_debug_trace_tq(buf, 4 * 256)
 tr = np.array(buf, dtype=np.int64).reshape(4, 256)
-names = {0: "start", 1: "setup", 2: "pfull", 120: "end(t0)", 121: "end(w4)", 122: "mma_loop_done", 123: "dealloc"}
+names = {0: "start", 1: "setup", 2: "pfull", 3: "pre_wait", 4: "post_wait", 120: "end(t0)", 121: "end(w4)", 122: "mma_loop_done", 123: "dealloc"}
 for k in range(16):
     names[8 + k] = f"tma_issue[{k}]"
     names[24 + k] = f"mma1_xfull[{k}]"

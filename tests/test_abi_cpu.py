@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_status_strings():
     lib = fq.load()
-    assert fq.fq_abi_version() == 3
+    assert fq.fq_abi_version() == 4
     for s in range(5):
         assert lib.fq_status_string(s).startswith(b"FQ_")
     assert lib.fq_status_string(99) == b"unknown fq_status"
