@@ -71,7 +71,14 @@ constexpr int UK = 32;                        // K per tcgen05.mma kind::i8
 #ifndef FQ_DEC_MINB
 #define FQ_DEC_MINB 2
 #endif
-constexpr int STAGES = FQ_DEC_STAGES;         // widened operand stages
+#ifndef FQ_DEC_TMEMW
+#define FQ_DEC_TMEMW 1
+#endif
+// FQ_DEC_TMEMW: the widened weights go to TMEM (the MMA's A operand straight from tensor memory,
+// tcgen05.st by one converter thread per weight row), only the widened activations to shared
+// memory -- 6 MMA stages in flight instead of 2 within the same shared-memory budget.
+constexpr bool TMEMW = FQ_DEC_TMEMW != 0;
+constexpr int STAGES = TMEMW ? 6 : FQ_DEC_STAGES;   // widened operand stages
 constexpr int PSTAGES = FQ_DEC_PSTAGES;       // packed TMA ring
 constexpr int WP_BYTES = BM * BK / 2;         // packed weights per stage (8 KB at BK = 128)
 constexpr int AP_BYTES = TN_MAX * BK / 2;     // packed activations per stage (max)
@@ -79,18 +86,24 @@ constexpr int P_BYTES = WP_BYTES + AP_BYTES;  // ring stage (1 KB multiple)
 constexpr int WW_BYTES = BM * BK;             // widened weights per stage (16 KB at BK = 128)
 constexpr int AW_BYTES = TN_MAX * BK;         // widened activations per stage
 constexpr int WW_ATOM = BM * 128, AW_ATOM = TN_MAX * 128;   // one 128-byte K atom of each
-constexpr int W_BYTES = WW_BYTES + AW_BYTES;
+constexpr int W_BYTES = (TMEMW ? 0 : WW_BYTES) + AW_BYTES;   // shared-memory bytes per MMA stage
+constexpr int W_COL0 = 64;                    // TMEM: accumulator [0, 64), weight stages after it
+constexpr int WT_COLS = BK / 4;               // TMEM columns per weight stage (4 int8 per column)
 constexpr int RED_BYTES = TN_MAX * BM * 4;    // 32 KB int32 partial tile [token][feature]
 constexpr int TMA_WARP = 0, MMA_WARP = 1, ALLOC_WARP = 2;
 constexpr int EPI_WARP0 = 4;                  // warps 4-7 (TMEM lane quarter = warp % 4)
 constexpr int CONV_WARP0 = 8, NUM_CONV_WARPS = 8;
 constexpr int THREADS = (CONV_WARP0 + NUM_CONV_WARPS) * 32;
 constexpr int CONV_THREADS = NUM_CONV_WARPS * 32;
-constexpr int TMEM_COLS = 64;
+// TMEMW: warps 8-11 widen the weights into TMEM; the activations are widened by warps 12-15 AND
+// the epilogue warps 4-7 (idle until the last MMA), one 16-byte chunk per thread at T = 64
+constexpr int NUM_ARRIVE = TMEMW ? 12 : NUM_CONV_WARPS;   // converter warps signalling per stage
+constexpr int TMEM_COLS = TMEMW ? 256 : 64;
 constexpr int MAX_SPLIT = 8;                  // portable cluster size
 constexpr size_t SMEM_BYTES = size_t(STAGES) * W_BYTES + size_t(PSTAGES) * P_BYTES + 1024 + 256;
 static_assert(RED_BYTES <= STAGES * W_BYTES, "the partial tile reuses the widened-operand stages");
 static_assert(P_BYTES % 1024 == 0 && W_BYTES % 1024 == 0 && WW_BYTES % 1024 == 0, "1 KB alignment");
+static_assert(!TMEMW || (BK == 128 && W_COL0 + STAGES * WT_COLS <= TMEM_COLS), "TMEM budget");
 
 FQ_DEVICE void widen8(uint32_t p, uint32_t& lo, uint32_t& hi) {   // 8 nibbles -> 8 x (16 q) int8
   lo = (p << 4) & 0xF0F0F0F0u;
@@ -163,12 +176,12 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
 
   if (warp == MMA_WARP && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      tc::mbar_init(&full[s], NUM_CONV_WARPS);
+      tc::mbar_init(&full[s], NUM_ARRIVE);
       tc::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < PSTAGES; ++s) {
       tc::mbar_init(&pfull[s], 1);
-      tc::mbar_init(&pempty[s], NUM_CONV_WARPS);
+      tc::mbar_init(&pempty[s], NUM_ARRIVE);
     }
     tc::mbar_init(tfull, 1);
     tc::fence_barrier_init();
@@ -182,6 +195,25 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) tc::griddep_launch();   // the next kernel may start launching (PDL)
   if (threadIdx.x == 0) dtrace(tslot, 1);
+
+  // activation rows (TN x 4 chunks) -> widened SWIZZLE_128B K-major stage, by 256 threads
+  // (at = 0..255: epilogue warps 4-7 and converter warps 12-15)
+  auto convert_a = [&](int at) {
+    for (int j = 0; j < nk; ++j) {
+      const int sp = j % PSTAGES, st = j % STAGES;
+      tc::mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1);
+      tc::mbar_wait(&pfull[sp], (j / PSTAGES) & 1);
+      const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES + WP_BYTES);
+      const uint32_t dst = smem_u32(sW + size_t(st) * W_BYTES);
+      for (int task = at; task < TN * CPR; task += 256)
+        convert_chunk(src + uint32_t(task * 16), dst, task / CPR, task % CPR, AW_ATOM);
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&pempty[sp]);
+      tc::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&full[st]);
+    }
+  };
 
   if (warp == TMA_WARP) {
     // ======================= TMA producer =======================
@@ -213,6 +245,39 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     // 32 tasks cover 8 consecutive rows (conflict-free 16-byte loads and swizzled stores)
     const int ct = threadIdx.x - CONV_WARP0 * 32;
     const int ntask = (BM + TN) * CPR;
+    if constexpr (TMEMW) {
+      if (warp < CONV_WARP0 + 4) {
+        // weight rows: one per thread (TMEM lane), packed row from the SWIZZLE_64B ring
+        // (conflict-free) -> widened in registers -> tcgen05.st into this stage's TMEM columns
+        const int q = warp & 3, r = q * 32 + lane;
+        const uint32_t tl = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(W_COL0);
+        for (int j = 0; j < nk; ++j) {
+          const int sp = j % PSTAGES, st = j % STAGES;
+          tc::mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1);
+          tc::mbar_wait(&pfull[sp], (j / PSTAGES) & 1);
+          const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES) + uint32_t(r * 64);
+          uint32_t w[32];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint4 pk = tc::lds128(src + uint32_t((c ^ ((r >> 1) & 3)) << 4));
+            widen8(pk.x, w[8 * c + 0], w[8 * c + 1]);
+            widen8(pk.y, w[8 * c + 2], w[8 * c + 3]);
+            widen8(pk.z, w[8 * c + 4], w[8 * c + 5]);
+            widen8(pk.w, w[8 * c + 6], w[8 * c + 7]);
+          }
+          tc::tmem_st32(tl + uint32_t(st * WT_COLS), w);
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&pempty[sp]);   // the loads were consumed by the st
+          tc::tmem_st_wait();
+          tc::fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&full[st]);
+          if (threadIdx.x == CONV_WARP0 * 32 && j < 36) dtrace(tslot, 40 + j);
+        }
+      } else {
+        convert_a(threadIdx.x - (CONV_WARP0 + 4) * 32 + 128);
+      }
+    } else
     for (int j = 0; j < nk; ++j) {
       const int sp = j % PSTAGES, st = j % STAGES;
       tc::mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1);
@@ -239,11 +304,19 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         tc::mbar_wait(&full[st], (j / STAGES) & 1);
         tc::fence_after();
         const uint32_t w0 = smem_u32(sW + size_t(st) * W_BYTES);
+        if constexpr (TMEMW) {
+          const uint32_t wt = tmem_base + uint32_t(W_COL0 + st * WT_COLS);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)
+            tc::mma_ts<true>(tmem_base, wt + uint32_t(k * (UK / 4)), tc::sdesc_sw128(w0 + k * UK, 16, 1024), idesc,
+                             (j | k) != 0);
+        } else {
 #pragma unroll
         for (int k = 0; k < BK / UK; ++k)
           tc::mma_ss<true>(tmem_base, tc::sdesc_sw128(w0 + (k >> 2) * WW_ATOM + (k & 3) * UK, 16, 1024),
                            tc::sdesc_sw128(w0 + WW_BYTES + (k >> 2) * AW_ATOM + (k & 3) * UK, 16, 1024), idesc,
                            (j | k) != 0);
+        }
         tc::mma_commit(&empty[st]);
         if (j < 36) dtrace(tslot, 76 + j);
       }
@@ -266,6 +339,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         }
       }
     }
+    if constexpr (TMEMW) convert_a(threadIdx.x - EPI_WARP0 * 32);
     tc::mbar_wait(tfull, 0);
     tc::fence_after();
     if (threadIdx.x == EPI_WARP0 * 32) dtrace(tslot, 112);
@@ -434,7 +508,8 @@ cudaError_t gemm_dec_launch(const GemmArgs& a, int split) {
     const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.N)};
     const uint64_t strides[1] = {uint64_t(a.K / 2)};
     const uint32_t box[2] = {BK / 2, BM};
-    if (!tmap_encode(&mw, a.qw, 1, 2, dims, strides, box, TMAP_SW_NONE)) return cudaErrorInvalidValue;
+    if (!tmap_encode(&mw, a.qw, 1, 2, dims, strides, box, TMEMW ? TMAP_SW64 : TMAP_SW_NONE))
+      return cudaErrorInvalidValue;
   }
   {
     const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.T)};
