@@ -559,7 +559,9 @@ def run_reference(args):
     value = sample * args.steps / el
     desc = f"{sample} tokens per step through all {args.config} linears (float64 oracle)"
     print(json.dumps({
-        "impl": "reference", "metric": "prefill tokens/s, FlatQuant W4A4 layer linears (transform+quant -> W4A4 GEMM)",
+        "impl": "reference",
+        "metric": ("decode" if cfg["T"] <= 64 else "prefill")
+                  + " tokens/s, FlatQuant W4A4 layer linears (transform+quant -> W4A4 GEMM)",
         "value": round(value, 2), "unit": "tokens/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
