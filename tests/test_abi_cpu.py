@@ -108,7 +108,7 @@ def test_w4a4_linear_validation():
     lib = fq.load()
     assert lib.fq_w4a4_gemm_i32(A16, 8, 40, A16, 16, A16, None) == _lib.FQ_ESHAPE
     assert lib.fq_w4a4_gemm_i32(None, 8, 64, A16, 16, A16, None) == _lib.FQ_EINVAL
-    assert lib.fq_set_gemm_impl(7) == _lib.FQ_EINVAL and lib.fq_set_gemm_impl(-1) == _lib.FQ_EINVAL
+    assert lib.fq_set_gemm_impl(8) == _lib.FQ_EINVAL and lib.fq_set_gemm_impl(-1) == _lib.FQ_EINVAL
 
 
 def kvq(**kw):
@@ -156,7 +156,7 @@ def test_prepare_weight_validation():
 
 
 def test_gemm_impl_selector_validation():
-    assert fq.load().fq_set_gemm_impl(7) == _lib.FQ_EINVAL
+    assert fq.load().fq_set_gemm_impl(8) == _lib.FQ_EINVAL
     with pytest.raises(fq.FlatQuantError):
         fq.fq_set_gemm_impl(-1)
 
@@ -175,3 +175,11 @@ def test_product_path_does_not_import_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dp, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace("oracle's", ""), f
+
+
+def test_graft_entry_build_is_consistent():
+    """__graft_entry__.build() (the driver's build check) compiles/loads the library and its
+    ABI assertion matches the header (cached build: no recompilation when nothing changed)."""
+    import __graft_entry__ as g
+    g.build()
+    assert fq.fq_abi_version() == 4
