@@ -221,6 +221,8 @@ def run_ours(args):
     fq.load()
     if os.environ.get("FQ_GEMM_IMPL"):                     # testing aid: 0 pair (default), 1 mma.sync, 2 1-CTA
         fq.fq_set_gemm_impl(int(os.environ["FQ_GEMM_IMPL"]))
+    if os.environ.get("FQ_TQ_IMPL"):                       # testing aid: 0 default, 1 mma.sync, 2 CUDA cores
+        fq.fq_set_tq_impl(int(os.environ["FQ_TQ_IMPL"]))
 
     cfg, layers = build_workload(args.config, rank, dev, torch, fq)
     T = cfg["T"]

@@ -208,7 +208,8 @@ fq_status fq_choose_decomposition(int64_t n, int32_t* n1, int32_t* n2);
  * 0 = default (T <= 64: the decode kernel; otherwise tcgen05 kind::i8 on a CTA pair,
  * cta_group::2, tile width 192/160/128 features picked per shape to fill the last wave),
  * 1 = legacy mma.sync cross-check kernel, 2 = tcgen05 kind::i8 on a single CTA, 3 / 4 / 5 = the
- * pair kernel with the tile width forced to 192 / 160 / 128, 6 = the decode kernel forced
+ * pair kernel with the tile width forced to 192 / 160 / 128 (7: 256, one accumulator), 6 = the
+ * decode kernel forced
  * (swapped operands: 128 weight rows x T tokens per CTA, K split across a cluster and reduced
  * through distributed shared memory; T <= 64, FQ_ENOTSUP otherwise).  All bit-identical.
  * Returns FQ_EINVAL otherwise. */

@@ -133,14 +133,14 @@ static fq_status run_gemm(const uint8_t* qa, const float* sa, int64_t T, int32_t
     if (!gemm_dec_supported(a)) return FQ_ENOTSUP;
     return cuda_status(gemm_dec_launch(a));
   }
-  const bool pair = impl == 0 || (impl >= 3 && impl <= 5);
-  const int bn = impl == 3 ? 192 : impl == 4 ? 160 : impl == 5 ? 128 : 0;
+  const bool pair = impl == 0 || (impl >= 3 && impl <= 5) || impl == 7;
+  const int bn = impl == 3 ? 192 : impl == 4 ? 160 : impl == 5 ? 128 : impl == 7 ? 256 : 0;
   if (za) {                                        // asymmetric activations: pair kernel only
     if (!pair || !gemm_pair_supported(a)) return FQ_ENOTSUP;
     return cuda_status(gemm_pair_launch(a, bn));
   }
   if (pair && gemm_pair_supported(a)) return cuda_status(gemm_pair_launch(a, bn));
-  if (impl >= 3) return FQ_ENOTSUP;
+  if (impl >= 3) return FQ_ENOTSUP;   // a forced pair width the shape does not support
   if (impl == 2 && gemm_tc05_supported(a)) return cuda_status(gemm_tc05_launch(a));
   return cuda_status(gemm_mma_launch(a));
 }
@@ -328,7 +328,7 @@ fq_status fq_set_tq_impl(int32_t impl) {
 }
 
 fq_status fq_set_gemm_impl(int32_t impl) {
-  if (impl < 0 || impl > 6) return FQ_EINVAL;
+  if (impl < 0 || impl > 7) return FQ_EINVAL;
   g_gemm_impl.store(impl);
   return FQ_OK;
 }

@@ -78,12 +78,15 @@ constexpr int B_CHUNKS = BK / 32;                          // 16-byte packed chu
 // fill the last wave (fewer, narrower waves when N / 192 tiles would leave most clusters idle).
 template <int BN>
 struct Geo {
-  static_assert(BN % 32 == 0 && BN >= 64 && BN <= 192, "BN: multiple of 32 in [64, 192]");
+  static_assert(BN % 32 == 0 && BN >= 64 && BN <= 256, "BN: multiple of 32 in [64, 256]");
+  // up to 192 columns two accumulators fit beside the A stages (epilogue of tile i overlaps the
+  // main loop of tile i+1); a 256-wide tile has one, and its epilogue is not overlapped
+  static constexpr int NACC = BN <= 192 ? 2 : 1;
   static constexpr int BN_CTA = BN / 2;                    // B rows per CTA
   static constexpr int B_BYTES = BN_CTA * BK;              // widened B per stage per CTA
   static constexpr int BP_BYTES = BN_CTA * BK / 2;         // packed B per ring stage
   static constexpr int P_BYTES = AP_BYTES + BP_BYTES;
-  static constexpr int TMEM_A0 = 2 * BN;                   // A stages after the two accumulators
+  static constexpr int TMEM_A0 = NACC * BN;                // A stages after the accumulator(s)
   static constexpr int B_ATOM = BN_CTA * 128;              // one 128-byte K atom of the widened B stage
   static constexpr int B_TOTAL = BN_CTA * B_CHUNKS;        // B conversion tasks per stage
   static constexpr int B_TASKS = (B_TOTAL + NUM_B_WARPS * 32 - 1) / (NUM_B_WARPS * 32);
@@ -350,8 +353,8 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       uint32_t phase = 0;
       int it = 0;
       for (int tile = sc.cluster; tile < sc.num_tiles; tile += sc.num_clusters, ++it) {
-        const int buf = it & 1;
-        tc::mbar_wait_cluster(&tempty[buf], ((it >> 1) & 1) ^ 1);
+        const int buf = GE::NACC == 2 ? (it & 1) : 0;
+        tc::mbar_wait_cluster(&tempty[buf], ((GE::NACC == 2 ? (it >> 1) : it) & 1) ^ 1);
         tc::fence_after();
         const uint32_t tmem_d = tmem_base + uint32_t(TMEM_ACC0 + buf * BN);
         for (int kb = 0; kb < sc.num_kb; ++kb) {
@@ -383,8 +386,8 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     for (int tile = sc.cluster; tile < sc.num_tiles; tile += sc.num_clusters, ++it) {
       int mb, nb;
       sc.tile(tile, mb, nb);
-      const int buf = it & 1;
-      tc::mbar_wait(&tfull[buf], (it >> 1) & 1);
+      const int buf = GE::NACC == 2 ? (it & 1) : 0;
+      tc::mbar_wait(&tfull[buf], (GE::NACC == 2 ? (it >> 1) : it) & 1);
       tc::fence_after();
       if (threadIdx.x == 0 && it < 8) trace(136 + it);
       const int row = mb * BM + int(rank) * BM_CTA + r_local;
@@ -516,18 +519,23 @@ bool gemm_pair_supported(const GemmArgs& a) {
   return a.K % 32 == 0 && a.K <= 131072 && a.N % 8 == 0 && a.T <= int64_t(1) << 30 && tmap_available();
 }
 
-// Tile width per shape: the candidates cost waves * BN MMA-cycles per cluster (a pair tile's
-// main loop is proportional to BN at fixed K); a narrower tile wins only if it saves >= 4%.
-int gemm_pair_pick_bn(int64_t T, int N, int clusters) {
+// Tile width per shape.  A pair tile's main loop is bound by the A conversion (256 activation
+// rows per K-block, independent of the width), so the time of one wave grows much slower than
+// the width.  Measured per-wave costs relative to 128 columns (scripts/gemm_bn_sweep.py, C3
+// shapes): 1.16 at 160, 1.23 at 192; 256 columns has one accumulator, its epilogue is not
+// overlapped, which costs more at short K: 1.6 + 0.3 * 4096 / K (1.9 at K = 4096, where it never
+// wins; 1.69 at K = 14336, where it saves a wave on down_proj).  cost = waves x per-wave cost.
+int gemm_pair_pick_bn(int64_t T, int N, int K, int clusters) {
   using g3::BM;
-  const int cands[3] = {192, 160, 128};
+  const int cands[4] = {192, 160, 128, 256};
+  const double rel[4] = {1.23, 1.16, 1.0, 1.6 + 0.3 * 4096.0 / double(K > 0 ? K : 1)};
   int best = 192;
   double best_cost = 0;
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < 4; ++i) {
     const int bn = cands[i];
     const int64_t tiles = ((T + BM - 1) / BM) * ((N + bn - 1) / bn);
-    const double cost = double((tiles + clusters - 1) / clusters) * bn * (i == 0 ? 1.0 : 1.04);
-    if (i == 0 || cost < best_cost) {
+    const double cost = double((tiles + clusters - 1) / clusters) * rel[i];
+    if (i == 0 || cost < best_cost - 1e-9) {
       best = bn;
       best_cost = cost;
     }
@@ -587,8 +595,9 @@ cudaError_t gemm_pair_launch(const GemmArgs& a, int bn) {
     return v ? std::atoi(v) : 0;
   }();
   if (bn == 0) bn = env_bn;
-  if (bn == 0) bn = gemm_pair_pick_bn(a.T, a.N, std::max(1, num_sms() / 2));
+  if (bn == 0) bn = gemm_pair_pick_bn(a.T, a.N, a.K, std::max(1, num_sms() / 2));
   switch (bn) {
+    case 256: return launch_bn<256>(a);
     case 160: return launch_bn<160>(a);
     case 128: return launch_bn<128>(a);
     case 96: return launch_bn<96>(a);

@@ -129,7 +129,7 @@ cudaError_t gemm_tc05_launch(const GemmArgs& a);     // tcgen05 kind::i8, single
 bool gemm_tc05_supported(const GemmArgs& a);
 cudaError_t gemm_pair_launch(const GemmArgs& a, int bn = 0);   // tcgen05 kind::i8, CTA pair (cta_group::2);
                                                           // bn: tile width 192/160/128, 0 = per shape
-int gemm_pair_pick_bn(int64_t T, int N, int clusters);
+int gemm_pair_pick_bn(int64_t T, int N, int K, int clusters);
 cudaError_t gemm_dec_launch(const GemmArgs& a, int split = 0);  // decode (T <= 64): swapped operands,
 bool gemm_dec_supported(const GemmArgs& a);                     // cluster split-K; split 0 = per shape
 bool gemm_pair_supported(const GemmArgs& a);

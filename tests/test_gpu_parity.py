@@ -190,8 +190,8 @@ def test_transform_strided_rows_and_empty():
 
 
 # GEMM implementations (fq_set_gemm_impl): 0 pair kernel, tile width per shape; 1 legacy mma.sync;
-# 2 single-CTA tcgen05; 3 / 4 / 5 pair kernel with the tile width forced to 192 / 160 / 128.
-GEMM_IMPLS = [0, 1, 2, 3, 4, 5]
+# 2 single-CTA tcgen05; 3 / 4 / 5 / 7 pair kernel with the tile width forced to 192 / 160 / 128 / 256.
+GEMM_IMPLS = [0, 1, 2, 3, 4, 5, 7]
 
 
 @pytest.mark.parametrize("impl", GEMM_IMPLS)
@@ -435,7 +435,7 @@ def test_weight_colsum_exact():
     assert np.array_equal(np_of(cs).astype(np.int64), qw.astype(np.int64).sum(1))
 
 
-@pytest.mark.parametrize("impl,T", [(0, 1037), (4, 1037), (0, 64), (6, 23)])
+@pytest.mark.parametrize("impl,T", [(0, 1037), (4, 1037), (7, 1037), (0, 64), (6, 23)])
 @pytest.mark.parametrize("out_dtype", [torch.float16, torch.bfloat16])
 def test_asym_linear_vs_oracle(out_dtype, impl, T):
     """Asymmetric activations through the GEMM: Y = s_a s_w (acc - (z - 8) colsum_w) equals the
