@@ -67,8 +67,14 @@ constexpr int A_COLS = BK / 4;            // TMEM columns per A stage
 constexpr int TMEM_ACC0 = 0;              // two accumulators [0, 2*BN)
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_EPI_WARPS = 4, MMA_WARP = 4;
-constexpr int A_WARP0 = 5, NUM_A_WARPS = 8;     // 2 warps per TMEM lane quarter (each half of K)
-constexpr int B_WARP0 = 13, NUM_B_WARPS = FQ_GEMM_BWARPS;
+#ifndef FQ_GEMM_AWARPS
+#define FQ_GEMM_AWARPS 8
+#endif
+constexpr int A_WARP0 = 5, NUM_A_WARPS = FQ_GEMM_AWARPS;   // 4 warps per K part (one per TMEM lane quarter)
+constexpr int A_PARTS = NUM_A_WARPS / 4;                   // K parts of a row: 2 (halves) or 4 (quarters)
+constexpr int A_CH = 8 / A_PARTS;                          // packed 16-byte chunks per thread and K-block
+static_assert(NUM_A_WARPS == 8 || NUM_A_WARPS == 16, "A converter warps: 8 or 16");
+constexpr int B_WARP0 = A_WARP0 + NUM_A_WARPS, NUM_B_WARPS = FQ_GEMM_BWARPS;
 constexpr int NUM_CONV_WARPS = NUM_A_WARPS + NUM_B_WARPS;
 constexpr int TMA_WARP = B_WARP0 + NUM_B_WARPS;
 constexpr int THREADS = (TMA_WARP + 1) * 32;
@@ -247,12 +253,12 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     cv.init(sc);
     int job = 0;
     if (is_a) {
-      // row r_local of the CTA's 128 activation rows, K-half khalf of the 256-element K-block:
-      // 64 packed bytes = chunks 4 khalf .. 4 khalf + 3 of the SWIZZLE_128B row
+      // row r_local of the CTA's 128 activation rows, K part kpart of the 256-element K-block:
+      // 128 / A_PARTS packed bytes = chunks A_CH kpart .. A_CH kpart + A_CH - 1 of the SWIZZLE_128B row
       const int aw = warp - A_WARP0;
-      const int quarter = warp & 3, khalf = aw >> 2;
+      const int quarter = warp & 3, kpart = aw >> 2;
       const int r_local = quarter * 32 + lane;                   // == TMEM lane of this row
-      const uint32_t tl = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(TMEM_A0 + khalf * (A_COLS / 2));
+      const uint32_t tl = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(TMEM_A0 + kpart * (A_COLS / A_PARTS));
       const uint32_t sw = uint32_t(r_local & 7);
       const uint32_t roff = uint32_t(r_local * 128);
       // Two K-blocks per iteration: both are converted and their tcgen05.st issued before one
@@ -263,16 +269,17 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         tc::mbar_wait(&empty[st], ph ^ 1);
         tc::mbar_wait(&pfull[sp], (jb / PSTAGES) & 1);
         const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES) + roff;
-        uint32_t w[32];
+        uint32_t w[8 * A_CH];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const uint4 pk = tc::lds128(src + ((uint32_t(4 * khalf + c) ^ sw) << 4));
+        for (int c = 0; c < A_CH; ++c) {
+          const uint4 pk = tc::lds128(src + ((uint32_t(A_CH * kpart + c) ^ sw) << 4));
           widen8(pk.x, w[8 * c + 0], w[8 * c + 1]);
           widen8(pk.y, w[8 * c + 2], w[8 * c + 3]);
           widen8(pk.z, w[8 * c + 4], w[8 * c + 5]);
           widen8(pk.w, w[8 * c + 6], w[8 * c + 7]);
         }
-        tc::tmem_st32(tl + uint32_t(st * A_COLS), w);
+        if constexpr (A_CH == 4) tc::tmem_st32(tl + uint32_t(st * A_COLS), *reinterpret_cast<uint32_t(*)[32]>(w));
+        else tmem_st16(tl + uint32_t(st * A_COLS), *reinterpret_cast<uint32_t(*)[16]>(w));
         // release the ring slot only after the loaded values were consumed (the tcgen05.st reads
         // them): mbarrier.arrive does not wait for an outstanding ld.shared, so an arrive right
         // after the loads lets the TMA overwrite the slot before a delayed load has read it
