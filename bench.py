@@ -427,11 +427,25 @@ def run_ours(args):
         hy = [torch.empty(L["y"].shape, dtype=L["y"].dtype).pin_memory() for L in layers]
         dx = [torch.empty_like(L["x"]) for L in layers]
 
+        # two streams: the linears of a step alternate between them, so one linear's D2H copy
+        # overlaps the next one's H2D copy (PCIe is full duplex) and compute; every linear has
+        # its own staging buffers.  The step ends when both streams are done.  (Splitting each
+        # linear into 4 token chunks was measured slower: 0.47 vs 0.51 M tokens/s on C3.)
+        e2e_streams = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+
         def e2e_step():
-            for L, x_h, y_h, x_d in zip(layers, hx, hy, dx):
+            start = torch.cuda.Event()
+            start.record(stream)
+            for st in e2e_streams:
+                st.wait_event(start)
+            for i, (L, x_h, y_h, x_d) in enumerate(zip(layers, hx, hy, dx)):
                 lin = L["lin"]
                 fq.fq_flatquant_linear_host(x_h, x_d, lin.n1, lin.n2, L["p1"], L["p2"], args.alpha, L["qw"], L["sw"],
-                                            y_h, L["y"], L["q"], L["s"])
+                                            y_h, L["y"], L["q"], L["s"], stream=e2e_streams[i % 2], sync=False)
+            for st in e2e_streams:
+                done = torch.cuda.Event()
+                done.record(st)
+                stream.wait_event(done)
 
         for _ in range(2):
             e2e_step()

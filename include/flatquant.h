@@ -151,6 +151,17 @@ fq_status fq_flatquant_linear_host(const void* x_host, void* x_dev, int32_t x_dt
                                    const float* sw, int32_t N, void* y_host, void* y_dev,
                                    int32_t y_dtype, uint8_t* q_ws, float* s_ws, void* stream);
 
+/* fq_flatquant_linear_host_async -- fq_flatquant_linear_host WITHOUT the final
+ * synchronisation: the H2D copy, the hot path and the D2H copy are only enqueued on `stream`;
+ * y_host is valid once the caller has synchronised the stream.  With page-locked buffers the
+ * copies are asynchronous, so linears issued on different streams overlap their transfers
+ * (PCIe is full duplex) with each other's compute. */
+fq_status fq_flatquant_linear_host_async(const void* x_host, void* x_dev, int32_t x_dtype,
+                                         int64_t T, int32_t n1, int32_t n2, const void* p1,
+                                         const void* p2, float alpha, const uint8_t* qw,
+                                         const float* sw, int32_t N, void* y_host, void* y_dev,
+                                         int32_t y_dtype, uint8_t* q_ws, float* s_ws, void* stream);
+
 /* ---------------------------------------------------------------------------------------
  * fq_prepare_weight -- offline weight side of Eq. 3 on the GPU:
  *   W'_o = P1^{-1} W~_o P2^{-T}     (W~_o = row o of W reshaped n1 x n2)

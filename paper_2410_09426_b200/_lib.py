@@ -34,6 +34,8 @@ SIGNATURES = {
                                    _vp, _vp, _vp]),
     "fq_flatquant_linear_host": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp, _vp, _f32, _vp, _vp, _i32, _vp,
                                         _vp, _i32, _vp, _vp, _vp]),
+    "fq_flatquant_linear_host_async": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp, _vp, _f32, _vp, _vp, _i32, _vp,
+                                        _vp, _i32, _vp, _vp, _vp]),
     "fq_prepare_weight": (_i32, [_vp, _i32, _i32, _i64, _i32, _i32, _vp, _vp, _f32, _vp, _vp, _vp, _vp, _u64,
                                  _vp]),
     "fq_prepare_weight_workspace_size": (_u64, [_i32, _i32]),

@@ -112,16 +112,19 @@ def fq_flatquant_linear(x, n1, n2, p1, p2, alpha, qw, sw, y, q_ws, s_ws, stream=
     check("fq_flatquant_linear", st)
 
 
-def fq_flatquant_linear_host(x_host, x_dev, n1, n2, p1, p2, alpha, qw, sw, y_host, y_dev, q_ws, s_ws, stream=None):
-    """x_host / y_host are CPU tensors (pinned recommended); synchronises the stream."""
+def fq_flatquant_linear_host(x_host, x_dev, n1, n2, p1, p2, alpha, qw, sw, y_host, y_dev, q_ws, s_ws, stream=None,
+                             sync=True):
+    """x_host / y_host are CPU tensors (pinned recommended).  sync=True synchronises the stream
+    (fq_flatquant_linear_host); sync=False only enqueues (fq_flatquant_linear_host_async)."""
     _cuda(x_dev, p1, p2, qw, sw, y_dev, q_ws, s_ws)
     if x_host.is_cuda or y_host.is_cuda:
         raise ValueError("x_host and y_host must be host tensors")
-    st = load().fq_flatquant_linear_host(_ptr(x_host), _ptr(x_dev), _fq_dtype(x_dev.dtype), x_dev.shape[0], n1, n2,
-                                         _ptr(p1), _ptr(p2), float(alpha), _ptr(qw), _ptr(sw), qw.shape[0],
-                                         _ptr(y_host), _ptr(y_dev), _fq_dtype(y_dev.dtype), _ptr(q_ws), _ptr(s_ws),
-                                         _stream(stream))
-    check("fq_flatquant_linear_host", st)
+    name = "fq_flatquant_linear_host" if sync else "fq_flatquant_linear_host_async"
+    st = getattr(load(), name)(_ptr(x_host), _ptr(x_dev), _fq_dtype(x_dev.dtype), x_dev.shape[0], n1, n2,
+                               _ptr(p1), _ptr(p2), float(alpha), _ptr(qw), _ptr(sw), qw.shape[0],
+                               _ptr(y_host), _ptr(y_dev), _fq_dtype(y_dev.dtype), _ptr(q_ws), _ptr(s_ws),
+                               _stream(stream))
+    check(name, st)
 
 
 def fq_choose_decomposition(n: int) -> tuple[int, int]:

@@ -212,6 +212,16 @@ fq_status fq_flatquant_linear_host(const void* x_host, void* x_dev, int32_t x_dt
                                    int32_t n2, const void* p1, const void* p2, float alpha, const uint8_t* qw,
                                    const float* sw, int32_t N, void* y_host, void* y_dev, int32_t y_dtype,
                                    uint8_t* q_ws, float* s_ws, void* stream) {
+  fq_status s = fq_flatquant_linear_host_async(x_host, x_dev, x_dtype, T, n1, n2, p1, p2, alpha, qw, sw, N, y_host,
+                                               y_dev, y_dtype, q_ws, s_ws, stream);
+  if (s != FQ_OK || T == 0) return s;
+  return cuda_status(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+}
+
+fq_status fq_flatquant_linear_host_async(const void* x_host, void* x_dev, int32_t x_dtype, int64_t T, int32_t n1,
+                                         int32_t n2, const void* p1, const void* p2, float alpha, const uint8_t* qw,
+                                         const float* sw, int32_t N, void* y_host, void* y_dev, int32_t y_dtype,
+                                         uint8_t* q_ws, float* s_ws, void* stream) {
   if (T < 0) return FQ_EINVAL;
   if (T == 0) return FQ_OK;
   if (!x_host || !x_dev || !y_host || !y_dev) return FQ_EINVAL;
@@ -222,9 +232,7 @@ fq_status fq_flatquant_linear_host(const void* x_host, void* x_dev, int32_t x_dt
   if (s != FQ_OK) return s;
   s = fq_flatquant_linear(x_dev, x_dtype, T, n1, n2, p1, p2, alpha, qw, sw, N, y_dev, y_dtype, q_ws, s_ws, stream);
   if (s != FQ_OK) return s;
-  s = cuda_status(cudaMemcpyAsync(y_host, y_dev, ybytes, cudaMemcpyDeviceToHost, st));
-  if (s != FQ_OK) return s;
-  return cuda_status(cudaStreamSynchronize(st));
+  return cuda_status(cudaMemcpyAsync(y_host, y_dev, ybytes, cudaMemcpyDeviceToHost, st));
 }
 
 fq_status fq_weight_colsum(const uint8_t* qw, int32_t N, int32_t K, int32_t* colsum, void* stream) {

@@ -463,3 +463,27 @@ def test_asym_linear_vs_oracle(out_dtype, impl, T):
     qo, so, zo, _ = O.transform_quant_asym(x.float().numpy(), p1.float().numpy(), p2.float().numpy(), 0.9)
     ref = O.w4a4_linear_asym(qo, so, zo, qw, sw32.astype(np.float64))
     parity.check_output(np_of(y), ref, same, label="asym linear")
+
+
+def test_host_buffer_entry_points_match_device_path():
+    """fq_flatquant_linear_host (synchronous) and fq_flatquant_linear_host_async (two streams,
+    caller synchronises) give bit-identical outputs to the device-buffer entry point."""
+    T, n1, n2, N = 300, 64, 64, 520
+    x, p1, p2 = make_inputs(T, n1, n2, seed=41)
+    qw = synth.random_codes(N, n1 * n2, seed=41, tag="qw")
+    sw = to_dev(synth.random_scales(N, seed=41, tag="sw"))
+    qwd, p1d, p2d = to_dev(O.pack_int4(qw)), p1.to(DEV), p2.to(DEV)
+    ref = fq.flatquant_linear(x.to(DEV), n1, n2, p1d, p2d, 0.9, qwd, sw)
+    torch.cuda.synchronize()
+    xh = x.contiguous().pin_memory()
+    outs = []
+    for sync, stream in ((True, None), (False, torch.cuda.Stream()), (False, torch.cuda.Stream())):
+        yh = torch.empty((T, N), dtype=torch.float16).pin_memory()
+        xd, yd = torch.empty_like(x, device=DEV), torch.empty((T, N), dtype=torch.float16, device=DEV)
+        qws = torch.empty((T, n1 * n2 // 2), dtype=torch.uint8, device=DEV)
+        sws = torch.empty((T,), dtype=torch.float32, device=DEV)
+        fq.fq_flatquant_linear_host(xh, xd, n1, n2, p1d, p2d, 0.9, qwd, sw, yh, yd, qws, sws, stream=stream, sync=sync)
+        outs.append((yh, stream, (xd, yd, qws, sws)))
+    torch.cuda.synchronize()
+    for yh, _, _ in outs:
+        assert torch.equal(yh, ref.cpu())
