@@ -228,9 +228,11 @@ fq_status fq_set_gemm_impl(int32_t impl);
 
 /* Selects the transform+quant implementation for subsequent calls in this process (testing
  * aid): 0 = default (tcgen05/TMEM/TMA kernel for n2 in {64,128} with n1 = 64, or n2 = 128 with
- * n1 in {80,96,112,128}; otherwise the legacy mma.sync kernel where instantiated, else the
- * CUDA-core kernel), 1 = legacy mma.sync kernel (else CUDA cores), 2 = CUDA-core kernel.
- * Returns FQ_EINVAL otherwise.  All implementations compute the same function. */
+ * n1 in {80,96,112,128}; the wide tcgen05 kernel for n1 = 128, n2 in {160,192,224,256}; the
+ * CUDA-core kernel for n1 n2 <= 1024; otherwise the legacy mma.sync kernel where instantiated,
+ * else the CUDA-core kernel), 1 = legacy mma.sync kernel (else CUDA cores), 2 = CUDA-core
+ * kernel.  p2 = NULL (P2 = I) always runs its mma.sync variant.  Returns FQ_EINVAL otherwise.
+ * All implementations compute the same function. */
 fq_status fq_set_tq_impl(int32_t impl);
 
 /* Number of kernel launches issued by this library since process start (bench accounting). */
