@@ -28,6 +28,7 @@
 //               stage-1 epilogue (prescale, fp16, smem) and stage-2 epilogue (absmax, quantize,
 //               pack, store) of its own tiles; TMEM/smem buffers are indexed by the group.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include "fq_device.cuh"
@@ -69,7 +70,10 @@ constexpr int MAX_GROUPS = 4;
 constexpr int SMEM_LIMIT = 232448;       // max dynamic smem per block on sm_100
 constexpr int SMEM_OVERHEAD = 1024 + 512;  // 1024-B alignment slack + barriers/scratch
 
-template <int N1, int N2>
+// SMALL (decode-size launches, T <= 64): one epilogue group and two X stages, so a 64 x 64 CTA
+// needs ~66 KB of shared memory and 128 TMEM columns and can become resident beside a decode-GEMM CTA
+// of the preceding kernel (PDL): its setup and parameter loads then overlap that kernel's tail.
+template <int N1, int N2, bool SMALL = false>
 struct Cfg {
   static_assert(N2 == 64 || N2 == 128, "n2 in {64, 128}");
   static_assert(N1 % 16 == 0 && N1 >= 16 && N1 <= 128, "n1 multiple of 16, <= 128");
@@ -84,13 +88,14 @@ struct Cfg {
   static constexpr int A2_BYTES = 2 * N2 * 128;        // 2 M-atoms x N2 K-rows x 128 B
   static constexpr int D1C = G1 * N1;                  // TMEM columns of one stage-1 result
   // epilogue groups = tiles in flight (each owns a D1, D2 and A2 slot), as many as TMEM allows
-  static constexpr int GROUPS = (512 / (D1C + N2)) > MAX_GROUPS ? MAX_GROUPS : (512 / (D1C + N2));
+  static constexpr int GROUPS_FIT = (512 / (D1C + N2)) > MAX_GROUPS ? MAX_GROUPS : (512 / (D1C + N2));
+  static constexpr int GROUPS = SMALL ? 1 : GROUPS_FIT;
   static constexpr int THREADS = (4 + 4 * GROUPS) * 32;
   static constexpr int TMEM_USED = GROUPS * (D1C + N2);
-  static constexpr int TMEM_COLS = TMEM_USED <= 256 ? 256 : 512;
+  static constexpr int TMEM_COLS = TMEM_USED <= 128 ? 128 : (TMEM_USED <= 256 ? 256 : 512);
   static constexpr int FIXED = P1_BYTES + P2_BYTES + GROUPS * A2_BYTES;
   static constexpr int STAGES_FIT = (SMEM_LIMIT - SMEM_OVERHEAD - FIXED) / X_BYTES;
-  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static constexpr int STAGES = SMALL ? 2 : (STAGES_FIT > 8 ? 8 : STAGES_FIT);
   static constexpr size_t SMEM = size_t(FIXED) + size_t(STAGES) * X_BYTES + SMEM_OVERHEAD;
   static_assert(TMEM_USED <= 512, "TMEM budget");
   static_assert(STAGES >= 2, "shared-memory budget");
@@ -166,12 +171,12 @@ FQ_DEVICE uint32_t pack8(const float (&v)[8]) {
   return (e & 0x0F0F0F0Fu) | ((o << 4) & 0xF0F0F0F0u);
 }
 
-template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM>
-__global__ void __launch_bounds__(Cfg<N1, N2>::THREADS, 1)
+template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM, bool SMALL = false>
+__global__ void __launch_bounds__(Cfg<N1, N2, SMALL>::THREADS, 1)
 tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmP1,
                const __grid_constant__ CUtensorMap tmP2, int64_t T, float alpha, uint8_t* __restrict__ q,
                float* __restrict__ scale, float* __restrict__ y_out, int8_t* __restrict__ zero) {
-  using C = Cfg<N1, N2>;
+  using C = Cfg<N1, N2, SMALL>;
   constexpr int S = C::STAGES, TOK = C::TOK, G = C::GROUPS, THREADS = C::THREADS;
   constexpr uint32_t IDESC1 = tc::idesc_f16(128, N1, BF16 ? 1 : 0, 1, 1);
   constexpr uint32_t IDESC2 = tc::idesc_f16(128, N2, 0, 1, 1);
@@ -504,10 +509,18 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
 }
 
 // ------------------------------------------------------------------------------ host side
-template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM = false>
+static bool small_enabled() {                      // FQ_TQ_SMALL=0: testing aid (large config)
+  static const bool on = [] {
+    const char* v = std::getenv("FQ_TQ_SMALL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM = false, bool SMALL = false>
 static cudaError_t launch(const TQArgs& a) {
-  using C = Cfg<N1, N2>;
-  auto kern = tq_tc05_kernel<N1, N2, BF16, WRITE_Y, ASYM>;
+  using C = Cfg<N1, N2, SMALL>;
+  auto kern = tq_tc05_kernel<N1, N2, BF16, WRITE_Y, ASYM, SMALL>;
   static bool attr_set = false;   // benign race: idempotent attribute set
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
@@ -544,6 +557,10 @@ static cudaError_t launch(const TQArgs& a) {
 template <int N1, int N2>
 static cudaError_t dispatch(const TQArgs& a) {
   if (a.zero) return a.bf16 ? launch<N1, N2, true, false, true>(a) : launch<N1, N2, false, false, true>(a);
+  if constexpr (N1 == 64 && N2 == 64) {           // decode (C4) launches of the 64 x 64 transforms
+    if (a.T <= 64 && !a.y && small_enabled())
+      return a.bf16 ? launch<N1, N2, true, false, false, true>(a) : launch<N1, N2, false, false, false, true>(a);
+  }
   if (a.bf16) return a.y ? launch<N1, N2, true, true>(a) : launch<N1, N2, true, false>(a);
   return a.y ? launch<N1, N2, false, true>(a) : launch<N1, N2, false, false>(a);
 }
