@@ -7,9 +7,17 @@ quantize/pack) followed by fq_w4a4_linear (tcgen05 W4A4 GEMM + dequant epilogue)
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
 
-N > 1 is launched by torchrun (one process per GPU, NCCL); every rank processes its own T
-tokens (weak scaling, no collective in the timed path), the time is the max over ranks.
-Prints ONE JSON line on rank 0.
+N > 1 runs one process per GPU under torchrun (NCCL).  Launched without torchrun, `--gpus N`
+re-executes itself under `python -m torch.distributed.run --nproc-per-node N`; launched by
+torchrun, WORLD_SIZE must equal N (anything else is an error, never a silent 1-GPU run).
+Sharding: tokens are independent, so every rank owns a contiguous block of
+the global batch (paper_2410_09426_b200.sharding.shard_range), weights and transforms are
+replicated, and the timed path has no collective.  C1-C4 scale weakly (every rank processes the
+configuration's T tokens, rows [r T, (r+1) T) of an N T-token batch); C5, whose BASELINE config
+is a 16 x 2048-token batch sharded across the GPUs, scales strongly (T / N tokens per rank).
+The step time is the max over ranks.  After the timed region (untimed), an NCCL all-gather of
+the first linear's output is checked bit for bit against rank 0's own recompute of the last
+rank's shard.  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -68,8 +76,30 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp16", action="store_true")
     ap.add_argument("--no-kv", action="store_true", help="skip the KV-cache quantization measurement")
-    ap.add_argument("--verify", action="store_true", help="all-gather outputs (untimed) and check shards")
+    ap.add_argument("--no-verify", action="store_true", help="N > 1: skip the untimed all-gather check")
+    ap.add_argument("--no-fig6", action="store_true", help="skip the per-transform in-step overhead steps")
     return ap.parse_args()
+
+
+def launch_or_check_world(args):
+    """--gpus N: re-exec under torchrun if not already a torchrun rank; else WORLD_SIZE must be N."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None:
+        if args.gpus > 1 and args.impl == "ours":
+            import socket
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                port = so.getsockname()[1]
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+                   "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+            sys.stderr.write("[bench] --gpus %d without torchrun: launching %s\n" % (args.gpus, " ".join(cmd)))
+            sys.stderr.flush()
+            os.execv(sys.executable, cmd)
+        return
+    if int(ws) != args.gpus:
+        sys.stderr.write(f"[bench] error: --gpus {args.gpus} but WORLD_SIZE={ws}: refusing to report a "
+                         f"{ws}-process run as {args.gpus} GPUs\n")
+        sys.exit(2)
 
 
 # ------------------------------------------------------------------------ clocks sampler
@@ -137,13 +167,26 @@ class Clocks:
 
 
 # ------------------------------------------------------------------------ workload
-def build_workload(cfg_name, rank, dev, torch, fq):
+STRONG = {"C5"}        # configs whose global batch is split across the ranks (BASELINE config 5)
+
+
+def token_block(cfg_name, rank, world):
+    """(lo, hi, global_T): the rows of the global batch that `rank` owns."""
+    from paper_2410_09426_b200.sharding import shard_range
+    T = synth.config(cfg_name)["T"]
+    total = T if cfg_name in STRONG else T * world
+    lo, hi = shard_range(total, rank, world)
+    return lo, hi, total
+
+
+def build_workload(cfg_name, rank, world, dev, torch, fq):
     cfg = synth.config(cfg_name)
-    T = cfg["T"]
+    lo, hi, _ = token_block(cfg_name, rank, world)
+    T = hi - lo
     layers = []
     for lin in cfg["linears"]:
         n1, n2, N, K = lin.n1, lin.n2, lin.N, lin.K
-        x = torch.from_numpy(synth.activations(T, K, seed=1000 + rank, tag=lin.name)).to(dev)
+        x = torch.from_numpy(synth.activations(hi, K, seed=1000, tag=lin.name, rows=range(lo, hi))).to(dev)
         p1 = torch.from_numpy(synth.well_conditioned(n1, seed=0, tag=lin.name + "/p1")).to(dev)
         p2 = torch.from_numpy(synth.well_conditioned(n2, seed=0, tag=lin.name + "/p2")).to(dev)
         w = torch.from_numpy(synth.weights(N, K, seed=0, tag=lin.name)).to(dev)
@@ -152,7 +195,7 @@ def build_workload(cfg_name, rank, dev, torch, fq):
                            q=torch.empty((T, K // 2), dtype=torch.uint8, device=dev),
                            s=torch.empty((T,), dtype=torch.float32, device=dev),
                            y=torch.empty((T, N), dtype=torch.float16, device=dev)))
-    return cfg, layers
+    return cfg, layers, T
 
 
 def tq_bytes(T, lin):
@@ -173,14 +216,35 @@ def gemm_min_bytes(T, lin):
 
 
 # ------------------------------------------------------------------------ oracle (CPU) timing
-def cpu_oracle_rate(cfg_name, sample_tokens, alpha, budget_s=20.0):
-    """The float64 oracle as it stands, on a bounded token sample of the same workload."""
-    import oracle as O
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def blas_threads():
     try:
         from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
-        cores = os.cpu_count()
+        return os.cpu_count()
+
+
+def cpu_oracle_rate(cfg_name, sample_tokens, alpha, budget_s=12.0, threads=None):
+    """The float64 oracle as it stands, on a bounded token sample of the same workload; with
+    `threads`, its BLAS pool is limited to that many threads (threadpoolctl)."""
+    import contextlib
+
+    import oracle as O
+    ctx = contextlib.nullcontext()
+    if threads is not None:
+        from threadpoolctl import threadpool_limits
+        ctx = threadpool_limits(limits=threads)
     cfg = synth.config(cfg_name)
     prepared = []
     for lin in cfg["linears"]:
@@ -190,17 +254,28 @@ def cpu_oracle_rate(cfg_name, sample_tokens, alpha, budget_s=20.0):
         w = synth.weights(lin.N, lin.K, seed=0, tag=lin.name)
         qw, sw, _ = O.prepare_weight(w, p1, p2, 1.0)                 # offline, untimed
         prepared.append((x, p1, p2, qw, sw))
-    done, t0 = 0, time.perf_counter()
-    while True:
-        for x, p1, p2, qw, sw in prepared:
-            qa, sa, _ = O.transform_quant(x, p1, p2, alpha)
-            O.dequant(O.int_gemm(qa, qw), sa, sw)
-        done += sample_tokens
-        el = time.perf_counter() - t0
-        if el >= budget_s or done >= 4 * sample_tokens:
-            break
+    with ctx:
+        cores = threads if threads is not None else blas_threads()
+        done, t0 = 0, time.perf_counter()
+        while True:
+            for x, p1, p2, qw, sw in prepared:
+                qa, sa, _ = O.transform_quant(x, p1, p2, alpha)
+                O.dequant(O.int_gemm(qa, qw), sa, sw)
+            done += sample_tokens
+            el = time.perf_counter() - t0
+            if el >= budget_s or done >= 4 * sample_tokens:
+                break
     return done / el, cores, f"{sample_tokens} tokens x {done // sample_tokens} passes of all {cfg_name} linears " \
                              f"(transform+quant, int GEMM, dequant; weight prep untimed), {el:.1f} s"
+
+
+def cpu_baseline(cfg_name, alpha):
+    """all-core and 1-thread rates of the oracle, with the host's core count and CPU model"""
+    rate, cores, sample = cpu_oracle_rate(cfg_name, 128, alpha)
+    r1, _, s1 = cpu_oracle_rate(cfg_name, 32, alpha, threads=1)
+    return {"value": round(rate, 2), "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample,
+            "nproc": os.cpu_count(), "cpu_model": cpu_model(),
+            "one_thread": {"value": round(r1, 2), "unit": "tokens/s", "cores": 1, "sample": s1}}
 
 
 # ------------------------------------------------------------------------ our implementation
@@ -224,23 +299,38 @@ def run_ours(args):
     if os.environ.get("FQ_TQ_IMPL"):                       # testing aid: 0 default, 1 mma.sync, 2 CUDA cores
         fq.fq_set_tq_impl(int(os.environ["FQ_TQ_IMPL"]))
 
-    cfg, layers = build_workload(args.config, rank, dev, torch, fq)
-    T = cfg["T"]
+    cfg, layers, T = build_workload(args.config, rank, world, dev, torch, fq)
+    lo, hi, total_T = token_block(args.config, rank, world)
+    scaling = "strong" if args.config in STRONG else "weak"
     stream = torch.cuda.current_stream()
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > L2 (126 MB)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 2x L2 (126 MB)
+    flush_sum = torch.empty((), dtype=torch.float32, device=dev)
 
-    def step(evs=None):
+    def flush_l2():
+        # write then read 256 MiB: the dirty lines of the write are evicted by the read, so the
+        # next kernel finds the L2 full of clean lines it does not need (no write-back charged to it)
+        flush.zero_()
+        torch.sum(flush, dim=0, out=flush_sum)
+        torch.cuda._sleep(400_000)    # lets the host enqueue the whole step before the GPU reaches it
+
+    def step(evs=None, tq_mask=None, gemm=True, po_paper=None):
         for i, L in enumerate(layers):
             lin = L["lin"]
-            if evs is not None:
-                evs[2 * i][0].record(stream)
-            fq.fq_transform_quant(L["x"], lin.n1, lin.n2, L["p1"], L["p2"], args.alpha, L["q"], L["s"])
-            if evs is not None:
-                evs[2 * i][1].record(stream)
-                evs[2 * i + 1][0].record(stream)
-            fq.fq_w4a4_linear(L["q"], L["s"], L["qw"], L["sw"], L["y"])
-            if evs is not None:
-                evs[2 * i + 1][1].record(stream)
+            if tq_mask is None or tq_mask[i]:
+                if evs is not None:
+                    evs[2 * i][0].record(stream)
+                if po_paper is not None and lin.name == "P_o":
+                    fq.fq_transform_quant(L["x"], 32, 128, po_paper, None, args.alpha, L["q"], L["s"])
+                else:
+                    fq.fq_transform_quant(L["x"], lin.n1, lin.n2, L["p1"], L["p2"], args.alpha, L["q"], L["s"])
+                if evs is not None:
+                    evs[2 * i][1].record(stream)
+            if gemm:
+                if evs is not None:
+                    evs[2 * i + 1][0].record(stream)
+                fq.fq_w4a4_linear(L["q"], L["s"], L["qw"], L["sw"], L["y"])
+                if evs is not None:
+                    evs[2 * i + 1][1].record(stream)
 
     def barrier():
         torch.cuda.synchronize()
@@ -248,41 +338,52 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed_steps(n, **kw):
+        """n steps, L2 flushed before each (flush untimed); returns the summed step time (ms)."""
+        tot = 0.0
+        for _ in range(n):
+            flush_l2()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step(**kw)
+            b.record(stream)
+            torch.cuda.synchronize()
+            tot += a.elapsed_time(b)
+        return tot
+
     clk = Clocks(local).start()
     t_w = time.time()
     w = 0
     while w < max(args.warmup, 3) or time.time() - t_w < 1.0:      # >= 1 s soak so clocks settle
-        flush.zero_()
-        torch.cuda._sleep(400_000)
+        flush_l2()
         step()
         w += 1
         if w % 50 == 0:
             torch.cuda.synchronize()
     barrier()
 
-    # ---- timed region: K steps, L2 flushed before each step (flush itself untimed).  A device
-    #      sleep after the flush lets the host enqueue the whole step before the GPU reaches it,
-    #      so no host launch overhead is timed.  Pass 1 times the step alone (first kernel start ->
-    #      last kernel end, kernels back to back so programmatic dependent launch can overlap
-    #      their launches); pass 2 re-runs the K steps with events around every kernel for the
-    #      per-kernel roofline numbers (events between kernels serialise them).
+    # ---- timed region: K steps between barriers.  Pass 1 times the step alone (first kernel start
+    #      -> last kernel end, kernels back to back so programmatic dependent launch overlaps their
+    #      launches); pass 2 re-runs the K steps with events around every kernel for the per-kernel
+    #      roofline numbers (events between kernels serialise them and add ~5 us each, see
+    #      `event_overhead`).
     per_kernel = [[0.0, 0.0] for _ in range(2 * len(layers))]
-    step_ms = []
     launches0 = fq.fq_launch_count()
     clk.mark_start()
-    for _ in range(args.steps):
-        flush.zero_()
-        torch.cuda._sleep(400_000)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        step()
-        b.record(stream)
-        torch.cuda.synchronize()
-        step_ms.append(a.elapsed_time(b))
+    t_start = time.time()
+    total_ms = timed_steps(args.steps)
+    barrier()
+    wall_s = time.time() - t_start
     launches = fq.fq_launch_count() - launches0
     for _ in range(args.steps):
-        flush.zero_()
-        torch.cuda._sleep(400_000)
+        flush_l2()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(2 * len(layers))]
         step(evs)
@@ -293,13 +394,25 @@ def run_ours(args):
     barrier()
     clk.mark_end()
     clk.stop()
-    total_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    my_ms = total_ms / args.steps
+    total_ms = max_over_ranks(total_ms)
     ms_per_step = total_ms / args.steps
-    value = world * T / (ms_per_step * 1e-3)
+    value = total_T / (ms_per_step * 1e-3)          # all tokens of all ranks / max-over-ranks step time
+    rank_lines = None
+    if world > 1:
+        props = torch.cuda.get_device_properties(dev)
+        bus = float(getattr(props, "pci_bus_id", -1)) * 1000.0 + float(getattr(props, "pci_device_id", 0))
+        mine = torch.tensor([float(rank), float(T), my_ms, float(props.multi_processor_count), bus],
+                            dtype=torch.float64, device=dev)
+        allr = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        rank_lines = [{"rank": int(r[0]), "tokens": int(r[1]), "ms_per_step": round(float(r[2]), 4),
+                       "tokens_per_s": round(float(r[1]) / (float(r[2]) * 1e-3), 1), "sms": int(r[3]),
+                       "pci": int(r[4])}
+                      for r in (t.tolist() for t in allr)]
+    sys.stderr.write(f"[bench] rank {rank}/{world} cuda:{local} {torch.cuda.get_device_name(dev)} "
+                     f"backend={'nccl' if world > 1 else 'none'} tokens [{lo},{hi}) of {total_T}: "
+                     f"{my_ms:.4f} ms/step\n")
 
     # ---- kernel-level rooflines ----
     pk, peak_src = peaks()
@@ -308,7 +421,7 @@ def run_ours(args):
     g_ops = sum(gemm_ops(T, L["lin"]) for L in layers)
     t_bytes = sum(tq_bytes(T, L["lin"]) for L in layers)
     t_flops = sum(tq_flops(T, L["lin"]) for L in layers)
-    int8_peak = pk["bf16_tflops"] * INT8_PER_BF16
+    int8_peak, int8_src = int8_peak_tops(pk, peak_src)
     gemm_tops = g_ops / (gemm_ms * 1e-3) / 1e12
     tq_gbs = t_bytes / (tq_ms * 1e-3) / 1e9
     kernels = {}
@@ -324,27 +437,64 @@ def run_ours(args):
             "gemm_gbs": round(gemm_min_bytes(T, lin) / (gm_i * 1e-3) / 1e9, 1),
         }
 
+    # ---- event overhead and a same-byte copy (what an event-timed launch of this size can show) ----
+    one = torch.zeros(1, device=dev)
+    ev_empty = timed_ms(torch, stream, flush_l2, lambda: one.add_(1), max(5, args.steps))
+    cp_bytes = tq_bytes(T, layers[0]["lin"])
+    cp_src = torch.empty(cp_bytes // 4, dtype=torch.float16, device=dev)
+    cp_dst = torch.empty_like(cp_src)
+    ev_copy = timed_ms(torch, stream, flush_l2, lambda: cp_dst.copy_(cp_src), max(5, args.steps))
+    del cp_src, cp_dst
+
+    # ---- Fig. 6 analogue and the transforms' in-step cost: the same step
+    #      without any transform kernel (GEMMs on the codes already in place: "plain INT4"), and
+    #      with exactly one transform kernel added back; the difference is that transform's
+    #      marginal cost inside the step (PDL overlap included).  Also the step with the paper's
+    #      own o_proj transform P_o (32 x 32) x I_128 in place of the generic 64 x 64.
+    fig6 = None
+    if not args.no_fig6:
+        nl = len(layers)
+        reps = max(5, args.steps)
+        t_gemm_only = timed_steps(reps, tq_mask=[False] * nl) / reps
+        t_full = timed_steps(reps) / reps
+        per = {}
+        marg_sum = 0.0
+        for i, L in enumerate(layers):
+            mask = [j == i for j in range(nl)]
+            t_i = timed_steps(reps, tq_mask=mask) / reps
+            m_i = t_i - t_gemm_only
+            marg_sum += m_i
+            per[L["lin"].name] = {"transform": f"{L['lin'].n1}x{L['lin'].n2}", "step_ms": round(t_i, 4),
+                                  "marginal_us": round(m_i * 1e3, 2),
+                                  "slowdown_vs_int4": round(m_i / t_gemm_only, 4),
+                                  "marginal_gbs": round(tq_bytes(T, L["lin"]) / max(m_i * 1e-3, 1e-12) / 1e9, 1)}
+        fig6 = {"int4_gemm_only_step_ms": round(t_gemm_only, 4), "full_step_ms": round(t_full, 4),
+                "total_slowdown_vs_int4": round((t_full - t_gemm_only) / t_gemm_only, 4), "per_transform": per,
+                "paper_rtx3090": {"total": 0.07, "P_d": 0.04, "P_o": 0.01,
+                                  "source": "PAPER.md:510 (Fig. 6), 529-531; context only"},
+                "note": "INT4 = the same W4A4 GEMMs on codes already in HBM (no transform/quantize kernel); "
+                        "marginal = step with that one transform+quantize kernel minus the INT4 step"}
+        L_o = next((L for L in layers if L["lin"].name == "P_o"), None)
+        if L_o is not None and L_o["lin"].K == 4096:
+            p_o = torch.linalg.qr(torch.randn((32, 32), generator=torch.Generator(device=dev).manual_seed(7),
+                                              device=dev))[0].half()
+            mask = [L["lin"].name == "P_o" for L in layers]
+            t_po = timed_steps(reps, tq_mask=mask, po_paper=p_o) / reps
+            fig6["per_transform"]["P_o_paper"] = {
+                "transform": "P_o (32x32) x I_128 (p2 = NULL), the paper's online o_proj form (PAPER.md:297, 726)",
+                "step_ms": round(t_po, 4), "marginal_us": round((t_po - t_gemm_only) * 1e3, 2),
+                "slowdown_vs_int4": round((t_po - t_gemm_only) / t_gemm_only, 4)}
+        fig6["in_step_tq_gbs"] = round(t_bytes / max(marg_sum * 1e-3, 1e-12) / 1e9, 1)
+
     # ---- FP16 baseline (torch.matmul / cuBLAS on the same shapes), context for "vs FP16" ----
     fp16 = None
     if not args.no_fp16:
         xs = [L["x"] for L in layers]
         ws = [L["w"] for L in layers]
-        for _ in range(3):
-            for x, w in zip(xs, ws):
-                torch.matmul(x, w.t())
-        f_ms = []
-        for _ in range(max(5, args.steps // 2)):
-            flush.zero_()
-            torch.cuda._sleep(400_000)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            for x, w in zip(xs, ws):
-                torch.matmul(x, w.t())
-            b.record(stream)
-            torch.cuda.synchronize()
-            f_ms.append(a.elapsed_time(b))
-        fp16_ms = sum(f_ms) / len(f_ms)
-        fp16 = {"ms_per_step": round(fp16_ms, 4), "tokens_per_s": round(world * T / (fp16_ms * 1e-3), 1),
+        f_ms = timed_ms(torch, stream, flush_l2, lambda: [torch.matmul(x, w.t()) for x, w in zip(xs, ws)],
+                        max(5, args.steps // 2))
+        fp16_ms = max_over_ranks(f_ms)
+        fp16 = {"ms_per_step": round(fp16_ms, 4), "tokens_per_s": round(total_T / (fp16_ms * 1e-3), 1),
                 "speedup_ours_vs_fp16": round(fp16_ms / ms_per_step, 3)}
 
     # ---- KV-cache quantization, measured beside the step (not part of it).
@@ -357,7 +507,8 @@ def run_ours(args):
         ph = torch.linalg.qr(torch.randn((D, D), generator=gk, device=dev))[0].half()
         eye = torch.eye(D, device=dev).half()
         kv = {"kernel": "fq_kv_quant (tcgen05 kind::f16, K with P_h + V with P = I)", "head_dim": D, "bound": "hbm",
-              "peak": pk["hbm_gbs"], "unit": "GB/s", "l2": "flushed before every timed K+V pair", "sizes": []}
+              "peak": pk["hbm_gbs"], "unit": "GB/s", "l2": "flushed (write + read) before every timed K+V pair",
+              "sizes": []}
         for label, R in ((f"step: {T} tokens x {H} heads", T * H), (f"batch 64 x 2048 tokens x {H} heads", 64 * 2048 * H)):
             kk = torch.randn((R, D), generator=gk, device=dev).half()
             vv = torch.randn((R, D), generator=gk, device=dev).half()
@@ -368,57 +519,13 @@ def run_ours(args):
                 fq.fq_kv_quant(kk, ph, 0.95, *outs[0])
                 fq.fq_kv_quant(vv, eye, 0.95, *outs[1])
 
-            for _ in range(3):
-                kv_step()
-            k_ms = []
-            for _ in range(max(5, args.steps)):
-                flush.zero_()
-                torch.cuda._sleep(400_000)
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                kv_step()
-                b.record(stream)
-                torch.cuda.synchronize()
-                k_ms.append(a.elapsed_time(b))
-            kv_ms = sum(k_ms) / len(k_ms)
+            kv_ms = timed_ms(torch, stream, flush_l2, kv_step, max(5, args.steps))
             kv_bytes = 2 * R * (2 * D + D // 2 + 4 + 1)
             kv_gbs = kv_bytes / (kv_ms * 1e-3) / 1e9
             kv["sizes"].append({"workload": label, "head_vectors": 2 * R, "us": round(kv_ms * 1e3, 2),
                                 "achieved": round(kv_gbs, 1), "frac": round(kv_gbs / pk["hbm_gbs"], 4),
                                 "algorithmic_bytes": int(kv_bytes)})
             del kk, vv, outs
-
-    # ---- o_proj with the paper's own online transform: P_o is a x a over
-    #      the a = 32 heads, identity inside each head of 128, i.e. n1 x n2 =
-    #      32 x 128 with P2 = I (p2 = NULL); timed beside the generic 64 x 64 transform the step uses.
-    po = None
-    L_o = next((L for L in layers if L["lin"].name == "P_o"), None)
-    if L_o is not None and L_o["lin"].K == 4096:
-        p_o = torch.linalg.qr(torch.randn((32, 32), generator=torch.Generator(device=dev).manual_seed(7),
-                                          device=dev))[0].half()
-
-        def time_tq(fn):
-            for _ in range(3):
-                fn()
-            ts = []
-            for _ in range(max(5, args.steps)):
-                flush.zero_()
-                torch.cuda._sleep(400_000)
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                fn()
-                b.record(stream)
-                torch.cuda.synchronize()
-                ts.append(a.elapsed_time(b))
-            return sum(ts) / len(ts) * 1e3          # mean: event ticks are coarse (~2 us) on this part
-
-        lin = L_o["lin"]
-        us_paper = time_tq(lambda: fq.fq_transform_quant(L_o["x"], 32, 128, p_o, None, args.alpha, L_o["q"], L_o["s"]))
-        us_generic = time_tq(lambda: fq.fq_transform_quant(L_o["x"], lin.n1, lin.n2, L_o["p1"], L_o["p2"], args.alpha,
-                                                            L_o["q"], L_o["s"]))
-        po = {"transform": "P_o (32x32) x I_128, p2 = NULL (mma.sync, stage 2 skipped)",
-              "us": round(us_paper, 2), "gbs": round(tq_bytes(T, lin) / (us_paper * 1e-6) / 1e9, 1),
-              "generic_64x64_us": round(us_generic, 2), "note": "mean of event-timed launches, L2 flushed"}
 
     # ---- e2e: through the public C ABI with HOST buffers (H2D + hot path + D2H per step) ----
     e2e = None
@@ -458,29 +565,37 @@ def run_ours(args):
             b.record(stream)
             torch.cuda.synchronize()
             e_ms.append(a.elapsed_time(b))
-        e_tot = sum(e_ms)
-        if world > 1:
-            t = torch.tensor([e_tot], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_tot = float(t.item())
-        e2e_step_ms = e_tot / len(e_ms)
-        e2e = {"value": round(world * T / (e2e_step_ms * 1e-3), 1), "unit": "tokens/s",
+        e2e_step_ms = max_over_ranks(sum(e_ms)) / len(e_ms)
+        e2e = {"value": round(total_T / (e2e_step_ms * 1e-3), 1), "unit": "tokens/s",
                "ms_per_step": round(e2e_step_ms, 4),
                "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in hx)),
                "d2h_bytes_per_step": int(sum(y.numel() * y.element_size() for y in hy))}
 
-    # ---- verification (untimed): shards are independent, gather and compare with local ----
+    # ---- verification (untimed, N > 1): all-gather the first linear's output over NCCL; rank 0
+    #      recomputes the LAST rank's shard itself (same inputs regenerated from the seeded
+    #      streams, same kernels) and compares bit for bit; every rank checks its own block.
     verify = None
-    if args.verify and world > 1:
-        from paper_2410_09426_b200.sharding import gather_rows
-        y0 = layers[0]["y"]
-        full = gather_rows(y0, world * T)
-        verify = bool(torch.equal(full[rank * T:(rank + 1) * T], y0))
+    if world > 1 and not args.no_verify:
+        from paper_2410_09426_b200.sharding import gather_rows, shard_range
+        L0 = layers[0]
+        lin = L0["lin"]
+        step()
+        torch.cuda.synchronize()
+        full = gather_rows(L0["y"], total_T if scaling == "strong" else world * T)
+        own = bool(torch.equal(full[lo:hi], L0["y"]))
+        ok = torch.tensor([1 if own else 0], device=dev)
+        if rank == 0:
+            rlo, rhi = shard_range(full.shape[0], world - 1, world)
+            xr = torch.from_numpy(synth.activations(rhi, lin.K, seed=1000, tag=lin.name, rows=range(rlo, rhi))).to(dev)
+            yr = fq.flatquant_linear(xr, lin.n1, lin.n2, L0["p1"], L0["p2"], args.alpha, L0["qw"], L0["sw"])
+            torch.cuda.synchronize()
+            ok &= torch.tensor([1 if torch.equal(full[rlo:rhi], yr) else 0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        verify = bool(ok.item() == 1)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        rate, cores, sample = cpu_oracle_rate(args.config, 128, args.alpha)
-        cpu = {"value": round(rate, 2), "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample}
+        cpu = cpu_baseline(args.config, args.alpha)
 
     gemm_traffic = ncu_traffic(args.config, [L["lin"] for L in layers], "gemm")
     tq_traffic = ncu_traffic(args.config, [L["lin"] for L in layers], "tq")
@@ -499,42 +614,85 @@ def run_ours(args):
                 "achieved": round(gemm_tops, 1), "peak": round(int8_peak, 1), "unit": "TOPS",
                 "frac": round(gemm_tops / int8_peak, 4), "traffic": gemm_traffic,
                 "per": "aggregate of the step's GEMM launches (sum of 2TNK / sum of their durations)",
-                "algorithmic_bytes_per_step": int(g_bytes),
-                "peak_source": f"{peak_src}: bf16 {pk['bf16_tflops']} TF/s x nominal int8/bf16 ratio 2"}
+                "algorithmic_bytes_per_step": int(g_bytes), "peak_source": int8_src}
+    tq_roof = {"bound": "hbm", "kernel": "fq_transform_quant", "achieved": round(tq_gbs, 1),
+               "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(tq_gbs / pk["hbm_gbs"], 4),
+               "traffic": tq_traffic, "algorithmic_bytes_per_step": int(t_bytes),
+               "tflops": round(t_flops / (tq_ms * 1e-3) / 1e12, 1),
+               "per": "sum of algorithmic bytes / sum of event-timed launch durations (pass 2)",
+               "event_overhead": {"empty_kernel_us": round(ev_empty * 1e3, 2),
+                                  "same_bytes_copy_us": round(ev_copy * 1e3, 2),
+                                  "same_bytes_copy_gbs": round(cp_bytes / (ev_copy * 1e-3) / 1e9, 1),
+                                  "note": "an event-bracketed empty kernel and a torch copy moving one 64x64 "
+                                          "launch's algorithmic bytes, timed the same way (L2 flushed): the "
+                                          "ceiling an event-timed launch of this size can show"}}
+    if fig6 is not None:
+        tq_roof["in_step"] = {"achieved": fig6["in_step_tq_gbs"],
+                              "frac": round(fig6["in_step_tq_gbs"] / pk["hbm_gbs"], 4),
+                              "per": "sum of algorithmic bytes / sum of the transforms' in-step marginal costs "
+                                     "(fig6_transform_overhead)"}
     if rank == 0:
         out = {
             "metric": ("decode" if decode else "prefill")
                       + " tokens/s, FlatQuant W4A4 layer linears (transform+quant -> W4A4 GEMM)",
             "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "fp16 in / int4 x int4 -> int32 / fp16 out",
+            "scaling": scaling, "vs_baseline": None, "dtype": "fp16 in / int4 x int4 -> int32 / fp16 out",
             "data": "synthetic (seeded Gaussian + channel outliers + pivot token; random-init weights)",
-            "config": {"workload": f"{args.config}: {cfg['desc']}", "tokens_per_gpu": T,
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "tokens_per_gpu": T, "tokens_total": total_T,
                        "linears": [f"{L['lin'].name} {L['lin'].K}({L['lin'].n1}x{L['lin'].n2})->{L['lin'].N}"
                                    for L in layers],
-                       "alpha": args.alpha, "parallelism": f"token-shard x{world}",
-                       "l2": "flushed (256 MiB write) before every timed step; flush untimed"},
+                       "alpha": args.alpha, "parallelism": f"token-shard x{world} ({scaling} scaling)",
+                       "l2": "flushed (256 MiB write then read) before every timed step; flush untimed"},
+            "per_gpu": {"value": round(value / world, 1), "unit": "tokens/s"},
+            "gpus_active": 1 if rank_lines is None else len({r["pci"] for r in rank_lines}),
             "roofline": roof,
-            "tq_roofline": {"bound": "hbm", "kernel": "fq_transform_quant", "achieved": round(tq_gbs, 1),
-                            "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(tq_gbs / pk["hbm_gbs"], 4),
-                            "traffic": tq_traffic, "algorithmic_bytes_per_step": int(t_bytes),
-                            "tflops": round(t_flops / (tq_ms * 1e-3) / 1e12, 1)},
+            "tq_roofline": tq_roof,
             "time_share": {"transform_quant": round(tq_ms / ms_per_step, 4), "gemm": round(gemm_ms / ms_per_step, 4),
                            "note": "shares of the serialised per-kernel times (pass 2) relative to the step span (pass 1)"},
             "kernels": kernels,
+            "fig6_transform_overhead": fig6,
             "fp16_baseline": fp16,
             "kv_cache_quant": kv,
-            "o_proj_paper_transform": po,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "host_wall_s_timed_pass": round(wall_s, 3),
         }
+        if rank_lines is not None:
+            out["ranks"] = rank_lines
         if verify is not None:
             out["verify_allgather"] = verify
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def timed_ms(torch, stream, flush_l2, fn, reps):
+    """mean event-timed duration (ms) of fn over reps runs, L2 flushed before each"""
+    for _ in range(3):
+        fn()
+    tot = 0.0
+    for _ in range(reps):
+        flush_l2()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        tot += a.elapsed_time(b)
+    return tot / reps
+
+
+def int8_peak_tops(pk, peak_src):
+    """INT8 dense denominator: the committed own measurement (profiles/int8_peak.json: a
+    tcgen05 kind::i8 issue loop and cuBLASLt int8) if present, else 2 x the measured bf16 peak."""
+    path = os.path.join(ROOT, "profiles", "int8_peak.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["int8_tops"]), f"profiles/int8_peak.json: {d.get('how', 'measured')}"
+    return pk["bf16_tflops"] * INT8_PER_BF16, f"{peak_src}: bf16 {pk['bf16_tflops']} TF/s x nominal int8/bf16 ratio 2"
 
 
 # ------------------------------------------------------------------------ reference arm
@@ -578,17 +736,20 @@ def run_reference(args):
         "impl": "reference",
         "metric": ("decode" if cfg["T"] <= 64 else "prefill")
                   + " tokens/s, FlatQuant W4A4 layer linears (transform+quant -> W4A4 GEMM)",
-        "value": round(value, 2), "unit": "tokens/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "value": round(value, 2), "unit": "tokens/s", "n_gpus": int(os.environ.get("WORLD_SIZE", str(args.gpus))),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if args.config in STRONG else "weak", "vs_baseline": None,
+        "dtype": "f64",
         "data": "synthetic", "config": {"workload": f"{args.config}: {cfg['desc']}", "sample_tokens_per_step": sample},
-        "cpu_baseline": {"value": round(value, 2), "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": round(value, 2), "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": desc,
+                         "nproc": os.cpu_count(), "cpu_model": cpu_model()},
         "e2e": {"value": round(value, 2), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
 if __name__ == "__main__":
     a = parse()
+    launch_or_check_world(a)
     if a.impl == "reference":
         run_reference(a)
     else:

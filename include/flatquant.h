@@ -17,12 +17,18 @@
  *    valid until the work queued on `stream` has completed.
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Every call
  *    is asynchronous with respect to the host unless stated otherwise.
- *  - Parameters vs activations.  The kernels use programmatic dependent launch: a kernel may
- *    start while the preceding kernels of the stream finish and waits for them only before it
- *    reads its ACTIVATION inputs (x, qa, sa, za).  Its PARAMETERS (p1, p2, qw, sw, colsum_w)
- *    are read before that wait, so they must already be written when the call is made: by
- *    fq_prepare_weight / fq_weight_colsum followed by any synchronisation, or by a copy that
- *    completed.  (fq_prepare_weight itself returns only after its writes are complete.)
+ *  - Stream order.  Every call is ordered after the work already enqueued on `stream`, as
+ *    with any CUDA library.  The kernels use programmatic dependent launch (PDL) to overlap
+ *    their start with the tail of the preceding kernel: ACTIVATION inputs (x, qa, sa, za) are
+ *    always read after griddepcontrol.wait; PARAMETERS (p1, p2, qw, sw, colsum_w) are read
+ *    before it only when the library can tell that the preceding kernel does not write them --
+ *    it records the outputs of the last kernel it enqueued on each stream and, if a parameter
+ *    buffer overlaps them, the kernel reads its parameters after the wait instead.  Work of
+ *    other origin between two calls (copies, kernels that do not trigger PDL early) completes
+ *    before a PDL kernel may start, so the check is complete for this library's own kernels.
+ *    The one case it cannot see: a kernel of ANOTHER library that triggers its dependents early
+ *    (griddepcontrol.launch_dependents) and writes this library's parameters immediately before
+ *    the call; synchronise or record an event between them in that case.
  *  - Argument validation is synchronous: on any error nothing is launched and a non-zero
  *    fq_status is returned.  T == 0 returns FQ_OK without launching.  A failed launch
  *    returns FQ_ECUDA; fq_last_cuda_error() returns the cudaError_t value.  Device faults
@@ -32,7 +38,9 @@
  *    is aligned to its element size; in addition the tensor-core paths (the GEMM, and the
  *    transform when n1 % 16 == 0 and n2 % 16 == 0) need x, q, qa, qw, y and sw 16-byte
  *    aligned and row strides that are multiples of 16 bytes (FQ_ESHAPE otherwise).
- *  - Stateless and re-entrant; per-device kernel attributes are set once, thread-safely.
+ *  - Re-entrant.  Per-device kernel attributes are set once per (kernel, device), thread-safely;
+ *    the only state is the per-stream record of the last launch's outputs (see Stream order),
+ *    guarded by a mutex.
  *  - Non-finite inputs give unspecified codes (the oracle's precondition is finite x).
  */
 #ifndef FLATQUANT_H_
@@ -44,7 +52,8 @@
 extern "C" {
 #endif
 
-#define FQ_ABI_VERSION 4   /* 2: FQ_ASYM + fq_weight_colsum; 3: fq_kv_quant, fq_prepare_weight; 4: p2 = NULL (P2 = I) */
+#define FQ_ABI_VERSION 5   /* 2: FQ_ASYM + fq_weight_colsum; 3: fq_kv_quant, fq_prepare_weight; 4: p2 = NULL (P2 = I);
+                              5: K < 131072, PDL parameter hazard check, bf16 P2 scaled into fp16 range */
 
 typedef enum {
   FQ_OK = 0,
@@ -82,8 +91,14 @@ typedef enum { FQ_SYM = 0, FQ_ASYM = 1 } fq_qmode;
  *   zero   FQ_SYM: must be NULL.  FQ_ASYM: [T] int8 (output), z_t - 8.
  *   FQ_ASYM runs on the tcgen05 kernel shapes and the CUDA-core kernel (n1 n2 <= 25600);
  *   other shapes return FQ_ENOTSUP.
- *   Supported: n1, n2 >= 1, n even, n1, n2 <= 256 (tensor-core kernel when n1 % 16 == 0
- *   and n2 % 16 == 0; a CUDA-core kernel otherwise).
+ *   Supported (FQ_ENOTSUP otherwise): n even, 1 <= n1, n2 <= 256, and a kernel for the shape:
+ *   tcgen05 for (64, 64), (64, 128), ({80, 96, 112, 128}, 128), (128, {160, 192, 224, 256});
+ *   mma.sync for the other multiples of 16 listed in DESIGN.md (Fig. 5 decompositions); the
+ *   CUDA-core fp32 kernel for any shape with n1 n2 <= 25600.
+ *   Precision: X and P in x_dtype; stage 1 (P1^T V) accumulates in fp32; the intermediate is
+ *   re-fed to the second stage as fp16 after an exact per-token power-of-two prescale (never
+ *   bf16, R9).  A bf16 P2 is likewise scaled by a power of two into fp16 range (its
+ *   largest entry to [2^14, 2^15)), so no entry overflows; 2^-e is divided out exactly.
  * ------------------------------------------------------------------------------------- */
 fq_status fq_transform_quant(const void* x, int32_t x_dtype, int64_t T, int64_t ldx,
                              int32_t n1, int32_t n2, const void* p1, const void* p2,
@@ -114,7 +129,10 @@ fq_status fq_transform_f32(const void* x, int32_t x_dtype, int64_t T, int64_t ld
  *      implementation (fq_set_gemm_impl 0) or a tcgen05 pair / decode one (3-6); FQ_ENOTSUP
  *      otherwise.
  *   y  [T, N] of y_dtype (FQ_F16 or FQ_BF16), row-major.
- *   Requires K % 32 == 0 and N % 8 == 0.  Exact integer accumulation (|acc| <= 64 K < 2^31).
+ *   Requires K % 32 == 0, K < 131072 and N % 8 == 0 (FQ_ESHAPE / FQ_ENOTSUP otherwise).
+ *   Exact integer accumulation: the tensor core accumulates 256 acc (operands widened to 16 q),
+ *   |256 acc| <= 2^14 K < 2^31; the asymmetric correction is applied after the exact division
+ *   by 256, |acc - za colsum_w| <= 120 K.
  * ------------------------------------------------------------------------------------- */
 fq_status fq_w4a4_linear(const uint8_t* qa, const float* sa, const int8_t* za, int64_t T,
                          int32_t K, const uint8_t* qw, const float* sw,

@@ -46,10 +46,40 @@ def _cuda(*ts):
             raise ValueError("all tensors must be CUDA tensors (there is no CPU path)")
 
 
+def _need(cond, msg):
+    if not cond:
+        raise ValueError(msg)
+
+
+def _buf(t, name, shape, dtype):
+    """An output/parameter buffer the C ABI addresses as a dense row-major array of `shape`."""
+    if t is None:
+        return
+    _need(tuple(t.shape) == tuple(shape), f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    _need(t.dtype == dtype, f"{name}: dtype {t.dtype}, expected {dtype}")
+    _need(t.is_contiguous(), f"{name} must be contiguous")
+
+
+def _rows(x, name, min_cols):
+    """A [rows, >= min_cols] matrix with unit column stride (the row stride is passed)."""
+    _need(x.dim() == 2 and x.stride(1) == 1, f"{name} must be 2-D with unit column stride")
+    _need(x.shape[1] >= min_cols, f"{name}: {x.shape[1]} columns < {min_cols}")
+
+
 # ------------------------------------------------------------------ raw entry points
+def _tq_args(x, n1, n2, p1, p2, q, scale, zero=None):
+    _rows(x, "x", n1 * n2)
+    T = x.shape[0]
+    _buf(p1, "p1", (n1, n1), x.dtype)
+    _buf(p2, "p2", (n2, n2), x.dtype)
+    _buf(q, "q", (T, n1 * n2 // 2), torch.uint8)
+    _buf(scale, "scale", (T,), torch.float32)
+    _buf(zero, "zero", (T,), torch.int8)
+
+
 def fq_transform_quant(x, n1, n2, p1, p2, alpha, q, scale, zero=None, qmode=FQ_SYM, stream=None):
     _cuda(x, p1, p2, q, scale, zero)
-    assert x.dim() == 2 and x.stride(1) == 1
+    _tq_args(x, n1, n2, p1, p2, q, scale, zero)
     st = load().fq_transform_quant(_ptr(x), _fq_dtype(x.dtype), x.shape[0], x.stride(0), n1, n2, _ptr(p1),
                                    _ptr(p2), float(alpha), qmode, _ptr(q), _ptr(scale), _ptr(zero), _stream(stream))
     check("fq_transform_quant", st)
@@ -57,15 +87,31 @@ def fq_transform_quant(x, n1, n2, p1, p2, alpha, q, scale, zero=None, qmode=FQ_S
 
 def fq_transform_f32(x, n1, n2, p1, p2, alpha, q, scale, y, stream=None):
     _cuda(x, p1, p2, q, scale, y)
-    assert x.dim() == 2 and x.stride(1) == 1
+    _tq_args(x, n1, n2, p1, p2, q, scale)
+    _buf(y, "y", (x.shape[0], n1 * n2), torch.float32)
     st = load().fq_transform_f32(_ptr(x), _fq_dtype(x.dtype), x.shape[0], x.stride(0), n1, n2, _ptr(p1), _ptr(p2),
                                  float(alpha), _ptr(q), _ptr(scale), _ptr(y), _stream(stream))
     check("fq_transform_f32", st)
 
 
+def _gemm_args(qa, qw, K):
+    _need(qa.dim() == 2 and qw.dim() == 2, "qa and qw must be 2-D")
+    K = qa.shape[1] * 2 if K is None else K
+    _buf(qa, "qa", (qa.shape[0], K // 2), torch.uint8)
+    _buf(qw, "qw", (qw.shape[0], K // 2), torch.uint8)
+    return K
+
+
 def fq_w4a4_linear(qa, sa, qw, sw, y, K=None, za=None, colsum_w=None, stream=None):
     _cuda(qa, sa, qw, sw, y, za, colsum_w)
-    K = qa.shape[1] * 2 if K is None else K
+    K = _gemm_args(qa, qw, K)
+    T, N = qa.shape[0], qw.shape[0]
+    _buf(sa, "sa", (T,), torch.float32)
+    _buf(sw, "sw", (N,), torch.float32)
+    _buf(za, "za", (T,), torch.int8)
+    _buf(colsum_w, "colsum_w", (N,), torch.int32)
+    _need(y.dtype in (torch.float16, torch.bfloat16), "y must be fp16 or bf16")
+    _buf(y, "y", (T, N), y.dtype)
     st = load().fq_w4a4_linear(_ptr(qa), _ptr(sa), _ptr(za), qa.shape[0], K, _ptr(qw), _ptr(sw), _ptr(colsum_w),
                                qw.shape[0], _ptr(y), _fq_dtype(y.dtype), _stream(stream))
     check("fq_w4a4_linear", st)
@@ -73,21 +119,30 @@ def fq_w4a4_linear(qa, sa, qw, sw, y, K=None, za=None, colsum_w=None, stream=Non
 
 def fq_w4a4_gemm_i32(qa, qw, acc, K=None, stream=None):
     _cuda(qa, qw, acc)
-    K = qa.shape[1] * 2 if K is None else K
+    K = _gemm_args(qa, qw, K)
+    _buf(acc, "acc", (qa.shape[0], qw.shape[0]), torch.int32)
     st = load().fq_w4a4_gemm_i32(_ptr(qa), qa.shape[0], K, _ptr(qw), qw.shape[0], _ptr(acc), _stream(stream))
     check("fq_w4a4_gemm_i32", st)
 
 
 def fq_weight_colsum(qw, colsum, K=None, stream=None):
     _cuda(qw, colsum)
+    _need(qw.dim() == 2, "qw must be 2-D")
     K = qw.shape[1] * 2 if K is None else K
+    _buf(qw, "qw", (qw.shape[0], K // 2), torch.uint8)
+    _buf(colsum, "colsum", (qw.shape[0],), torch.int32)
     check("fq_weight_colsum", load().fq_weight_colsum(_ptr(qw), qw.shape[0], K, _ptr(colsum), _stream(stream)))
 
 
 def fq_kv_quant(kv, p_h, alpha, q, scale, zero, stream=None):
     """kv [R, D] (row stride kv.stride(0)), p_h [D, D]; outputs q [R, D/2], scale [R], zero [R]."""
     _cuda(kv, p_h, q, scale, zero)
-    assert kv.dim() == 2 and kv.stride(1) == 1
+    _need(kv.dim() == 2 and kv.stride(1) == 1, "kv must be 2-D with unit column stride")
+    R, D = kv.shape
+    _buf(p_h, "p_h", (D, D), kv.dtype)
+    _buf(q, "q", (R, D // 2), torch.uint8)
+    _buf(scale, "scale", (R,), torch.float32)
+    _buf(zero, "zero", (R,), torch.int8)
     st = load().fq_kv_quant(_ptr(kv), _fq_dtype(kv.dtype), kv.shape[0], kv.stride(0), kv.shape[1], _ptr(p_h),
                             float(alpha), _ptr(q), _ptr(scale), _ptr(zero), _stream(stream))
     check("fq_kv_quant", st)
@@ -104,8 +159,20 @@ def kv_quant(kv, p_h, alpha=1.0, stream=None):
     return q, s, z
 
 
+def _linear_args(x, n1, n2, p1, p2, qw, sw, y, q_ws, s_ws):
+    # the C entry point takes x as a dense [T, n1 n2] matrix (row stride n1 n2)
+    _need(x.dim() == 2 and x.shape[1] == n1 * n2 and x.is_contiguous(), "x must be a contiguous [T, n1*n2] matrix")
+    _tq_args(x, n1, n2, p1, p2, q_ws, s_ws)
+    _need(qw.dim() == 2, "qw must be 2-D")
+    _buf(qw, "qw", (qw.shape[0], n1 * n2 // 2), torch.uint8)
+    _buf(sw, "sw", (qw.shape[0],), torch.float32)
+    _need(y.dtype in (torch.float16, torch.bfloat16), "y must be fp16 or bf16")
+    _buf(y, "y", (x.shape[0], qw.shape[0]), y.dtype)
+
+
 def fq_flatquant_linear(x, n1, n2, p1, p2, alpha, qw, sw, y, q_ws, s_ws, stream=None):
     _cuda(x, p1, p2, qw, sw, y, q_ws, s_ws)
+    _linear_args(x, n1, n2, p1, p2, qw, sw, y, q_ws, s_ws)
     st = load().fq_flatquant_linear(_ptr(x), _fq_dtype(x.dtype), x.shape[0], n1, n2, _ptr(p1), _ptr(p2),
                                     float(alpha), _ptr(qw), _ptr(sw), qw.shape[0], _ptr(y), _fq_dtype(y.dtype),
                                     _ptr(q_ws), _ptr(s_ws), _stream(stream))
@@ -119,6 +186,9 @@ def fq_flatquant_linear_host(x_host, x_dev, n1, n2, p1, p2, alpha, qw, sw, y_hos
     _cuda(x_dev, p1, p2, qw, sw, y_dev, q_ws, s_ws)
     if x_host.is_cuda or y_host.is_cuda:
         raise ValueError("x_host and y_host must be host tensors")
+    _linear_args(x_dev, n1, n2, p1, p2, qw, sw, y_dev, q_ws, s_ws)
+    _buf(x_host, "x_host", tuple(x_dev.shape), x_dev.dtype)
+    _buf(y_host, "y_host", tuple(y_dev.shape), y_dev.dtype)
     name = "fq_flatquant_linear_host" if sync else "fq_flatquant_linear_host_async"
     st = getattr(load(), name)(_ptr(x_host), _ptr(x_dev), _fq_dtype(x_dev.dtype), x_dev.shape[0], n1, n2,
                                _ptr(p1), _ptr(p2), float(alpha), _ptr(qw), _ptr(sw), qw.shape[0],
@@ -199,7 +269,8 @@ def w4a4_gemm_i32(qa, qw, stream=None):
 def fq_prepare_weight(w, n1, n2, p1, p2, alpha_w, qw, sw, colsum_w=None, workspace=None, stream=None):
     """Raw entry point (synchronous, see include/flatquant.h); allocates the workspace if not given."""
     _cuda(w, p1, p2, qw, sw, colsum_w)
-    assert w.dim() == 2 and w.stride(1) == 1
+    _tq_args(w, n1, n2, p1, p2, qw, sw)
+    _buf(colsum_w, "colsum_w", (w.shape[0],), torch.int32)
     lib = load()
     need = int(lib.fq_prepare_weight_workspace_size(n1, n2))
     if workspace is None:

@@ -1,6 +1,10 @@
 """Build libflatquant.so (all CUDA sources, sm_100a) in-tree with nvcc.
 
-Usage: python -m paper_2410_09426_b200.build [-v]
+Every .cu is compiled to an object in parallel (objects are cached under build/ by a digest of
+the source, the shared headers and the flags, so an edit recompiles only what it touches), then
+the objects are linked into one shared library.
+
+Usage: python -m paper_2410_09426_b200.build [-v] [-f] [--trace]
 """
 from __future__ import annotations
 
@@ -9,17 +13,20 @@ import hashlib
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libflatquant.so")
+TRACE_LIB = os.path.join(HERE, "libflatquant_trace.so")
+OBJ_DIR = os.path.join(ROOT, "build", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
-    "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v", "-shared",
+    "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v",
     "-I", os.path.join(ROOT, "include"),
 ]
 
@@ -28,34 +35,73 @@ def sources() -> list[str]:
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
-def _digest() -> str:
+def _headers() -> list[str]:
+    return sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))) \
+        + [os.path.join(ROOT, "include", "flatquant.h")]
+
+
+def _hash(paths, extra: str) -> str:
+    """content digest, independent of where the repo lives (the snapshot runs from another path)"""
     h = hashlib.sha256()
-    for f in sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))) \
-            + [os.path.join(ROOT, "include", "flatquant.h")]:
+    for f in paths:
         h.update(open(f, "rb").read())
-    h.update(" ".join(NVCC_FLAGS).encode())
+    h.update(extra.replace(ROOT, "<root>").encode())
     return h.hexdigest()
 
 
-TRACE_LIB = os.path.join(HERE, "libflatquant_trace.so")
+def _digest() -> str:
+    return _hash(sources() + _headers(), " ".join(NVCC_FLAGS))
+
+
+def _compile(src: str, defs: list[str]) -> tuple[str, str]:
+    key = _hash([src] + _headers(), " ".join(NVCC_FLAGS + defs))[:16]
+    obj = os.path.join(OBJ_DIR, f"{os.path.basename(src)[:-3]}-{key}.o")
+    if os.path.exists(obj):
+        return obj, ""
+    tmp = obj + f".tmp{os.getpid()}"
+    r = subprocess.run([NVCC] + NVCC_FLAGS + defs + ["-c", "-o", tmp, src], capture_output=True, text=True)
+    log = f"$ nvcc -c {os.path.basename(src)}\n" + r.stdout + r.stderr
+    if r.returncode != 0:
+        raise RuntimeError(log)
+    os.replace(tmp, obj)
+    return obj, log
 
 
 def build(verbose: bool = False, force: bool = False, trace: bool = False) -> str:
     """Build libflatquant.so; trace=True builds the instrumented libflatquant_trace.so instead
-    (-DFQ_TRACE: device timelines for scripts/trace_tq.py; never loaded by the product)."""
+    (-DFQ_TRACE: device timelines for scripts/trace_*.py; never loaded by the product)."""
     lib = TRACE_LIB if trace else LIB
     stamp = lib + ".sha256"
     dig = _digest() + ("-trace" if trace else "")
     if not force and os.path.exists(lib) and os.path.exists(stamp) and open(stamp).read() == dig:
         return lib
-    cmd = [NVCC] + NVCC_FLAGS + (["-DFQ_TRACE"] if trace else []) + ["-o", lib] + sources()
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    defs = ["-DFQ_TRACE"] if trace else []
+    if force:
+        for src in sources():
+            key = _hash([src] + _headers(), " ".join(NVCC_FLAGS + defs))[:16]
+            p = os.path.join(OBJ_DIR, f"{os.path.basename(src)[:-3]}-{key}.o")
+            if os.path.exists(p):
+                os.remove(p)
+    logs = []
+    try:
+        with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 4)) as ex:
+            results = list(ex.map(lambda s: _compile(s, defs), sources()))
+    except RuntimeError as e:
+        with open(os.path.join(HERE, "build_trace.log" if trace else "build.log"), "w") as f:
+            f.write(str(e))
+        sys.stderr.write(str(e))
+        raise RuntimeError(f"nvcc failed building {os.path.basename(lib)} (see paper_2410_09426_b200/build*.log)")
+    objs = [o for o, _ in results]
+    logs = [lg for _, lg in results]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib] + objs
     r = subprocess.run(cmd, capture_output=True, text=True)
-    log = r.stdout + r.stderr
+    log = "\n".join(logs) + " ".join(cmd) + "\n" + r.stdout + r.stderr
     with open(os.path.join(HERE, "build_trace.log" if trace else "build.log"), "w") as f:
-        f.write(" ".join(cmd) + "\n" + log)
+        f.write(log)
     if r.returncode != 0:
         sys.stderr.write(log)
-        raise RuntimeError(f"nvcc failed building {os.path.basename(lib)} (see paper_2410_09426_b200/build*.log)")
+        raise RuntimeError(f"nvcc failed linking {os.path.basename(lib)} (see paper_2410_09426_b200/build*.log)")
     if verbose:
         sys.stderr.write(log)
     with open(stamp, "w") as f:

@@ -5,6 +5,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
+#include <vector>
 #include <cuda_runtime.h>
 #include "../../include/flatquant.h"
 #include "fq_internal.h"
@@ -42,6 +44,45 @@ int num_sms() {
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---- programmatic dependent launch: parameter hazard check ----------------------------------
+// The tensor-core kernels trigger their dependents early (griddepcontrol.launch_dependents at
+// their start), so the next kernel of the stream may begin while they still write.  A kernel
+// launched with PDL may therefore read a buffer before its griddepcontrol.wait only if the
+// immediately preceding kernel does not write it.  Activations are always read after the wait.
+// Parameters (p1, p2, qw, sw, colsum_w) are read before it -- overlapping their loads with the
+// tail of the preceding kernel -- unless they overlap the outputs of the last kernel this library
+// enqueued on the same stream, in which case the kernel reads them after the wait.  Work enqueued
+// in between by anyone else (copies, kernels without early triggers) completes before a PDL
+// kernel may start, so tracking this library's own last launch per stream is sufficient.
+struct Span {
+  uintptr_t lo, hi;
+};
+static Span span(const void* p, size_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  return Span{a, p ? a + bytes : a};
+}
+static std::mutex g_pdl_mu;
+static std::unordered_map<void*, std::vector<Span>> g_pdl_out;   // stream -> outputs of our last launch
+
+static bool params_early(cudaStream_t st, std::initializer_list<Span> params) {
+  std::lock_guard<std::mutex> lk(g_pdl_mu);
+  auto it = g_pdl_out.find(static_cast<void*>(st));
+  if (it == g_pdl_out.end()) return true;
+  for (const Span& o : it->second)
+    for (const Span& p : params)
+      if (p.lo < p.hi && o.lo < o.hi && p.lo < o.hi && o.lo < p.hi) return false;
+  return true;
+}
+static void record_outputs(cudaStream_t st, std::initializer_list<Span> outs) {
+  std::lock_guard<std::mutex> lk(g_pdl_mu);
+  auto& v = g_pdl_out[static_cast<void*>(st)];
+  v.assign(outs.begin(), outs.end());
+}
+static void clear_outputs(cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_pdl_mu);
+  g_pdl_out.erase(static_cast<void*>(st));
+}
 
 static fq_status cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return FQ_OK;
@@ -91,10 +132,15 @@ static fq_status run_tq(const void* x, int32_t x_dtype, int64_t T, int64_t ldx, 
   a.zero = zero;
   a.bf16 = (x_dtype == FQ_BF16);
   a.stream = static_cast<cudaStream_t>(stream);
-  const bool tc = (n1 % 16 == 0) && (n2 % 16 == 0);
-  if (!tc && !tq_simt_supported(n1, n2)) return FQ_ENOTSUP;
+  if (!tq_kernel_available(a)) return FQ_ENOTSUP;
   if (zero && !tq_asym_supported(a)) return FQ_ENOTSUP;
-  return cuda_status(transform_quant_launch(a));
+  const int64_t n = int64_t(n1) * n2;
+  a.params_early = params_early(a.stream, {span(p1, size_t(n1) * n1 * 2), span(p2, size_t(n2) * n2 * 2)});
+  const fq_status s = cuda_status(transform_quant_launch(a));
+  if (s == FQ_OK)
+    record_outputs(a.stream, {span(q, size_t(T) * size_t(n / 2)), span(scale, size_t(T) * 4),
+                              span(zero, size_t(T)), span(y, y ? size_t(T) * size_t(n) * 4 : 0)});
+  return s;
 }
 
 static fq_status validate_gemm(const uint8_t* qa, int64_t T, int32_t K, const uint8_t* qw, int32_t N,
@@ -104,10 +150,12 @@ static fq_status validate_gemm(const uint8_t* qa, int64_t T, int32_t K, const ui
   if (!qa || !qw || !y) return FQ_EINVAL;
   if (K == 0 || K % 32 != 0 || N % 8 != 0) return FQ_ESHAPE;
   if (!aligned16(qa) || !aligned16(qw) || !aligned16(y)) return FQ_ESHAPE;
-  if (K > 131072) return FQ_ENOTSUP;
+  if (K >= 131072) return FQ_ENOTSUP;   // 256 |acc| <= 2^14 K must stay < 2^31 (widened x16 operands)
   if (T > (int64_t(1) << 30)) return FQ_ENOTSUP;
   return FQ_OK;
 }
+
+static fq_status launch_gemm(GemmArgs& a);
 
 static fq_status run_gemm(const uint8_t* qa, const float* sa, int64_t T, int32_t K, const uint8_t* qw,
                           const float* sw, int32_t N, void* y, bool y_bf16, bool out_i32, void* stream,
@@ -126,7 +174,16 @@ static fq_status run_gemm(const uint8_t* qa, const float* sa, int64_t T, int32_t
   a.za = za;
   a.colsum = colsum;
   a.stream = static_cast<cudaStream_t>(stream);
+  a.params_early = params_early(a.stream, {span(qw, size_t(N) * size_t(K / 2)), span(sw, sw ? size_t(N) * 4 : 0),
+                                           span(colsum, colsum ? size_t(N) * 4 : 0)});
+  const fq_status s = launch_gemm(a);
+  if (s == FQ_OK) record_outputs(a.stream, {span(y, size_t(T) * size_t(N) * (out_i32 ? 4 : 2))});
+  return s;
+}
+
+static fq_status launch_gemm(GemmArgs& a) {
   const int impl = g_gemm_impl.load();
+  const bool za = a.za != nullptr;
   // impl 0: decode kernel for T <= 64, else the pair kernel with the tile width picked per shape;
   // 3 / 4 / 5: pair kernel with the width forced to 192 / 160 / 128; 6: decode kernel forced
   if (impl == 6 || (impl == 0 && gemm_dec_supported(a))) {
@@ -135,7 +192,7 @@ static fq_status run_gemm(const uint8_t* qa, const float* sa, int64_t T, int32_t
   }
   const bool pair = impl == 0 || (impl >= 3 && impl <= 5) || impl == 7;
   const int bn = impl == 3 ? 192 : impl == 4 ? 160 : impl == 5 ? 128 : impl == 7 ? 256 : 0;
-  if (za) {                                        // asymmetric activations: pair kernel only
+  if (za) {                                        // asymmetric activations: pair or decode kernel
     if (!pair || !gemm_pair_supported(a)) return FQ_ENOTSUP;
     return cuda_status(gemm_pair_launch(a, bn));
   }
@@ -191,9 +248,16 @@ fq_status fq_w4a4_gemm_i32(const uint8_t* qa, int64_t T, int32_t K, const uint8_
   return run_gemm(qa, nullptr, T, K, qw, nullptr, N, acc, false, true, stream);
 }
 
-fq_status fq_flatquant_linear(const void* x, int32_t x_dtype, int64_t T, int32_t n1, int32_t n2,
-                              const void* p1, const void* p2, float alpha, const uint8_t* qw, const float* sw,
-                              int32_t N, void* y, int32_t y_dtype, uint8_t* q_ws, float* s_ws, void* stream) {
+}  // extern "C"
+
+namespace fq {
+// every check fq_flatquant_linear makes, before anything is enqueued (also for the host-buffer
+// entry points, which must not start a copy for a call that is then rejected)
+static fq_status validate_linear(const void* x, int32_t x_dtype, int64_t T, int32_t n1, int32_t n2,
+                                 const void* p1, const void* p2, float alpha, const uint8_t* qw,
+                                 const float* sw, int32_t N, const void* y, int32_t y_dtype,
+                                 const uint8_t* q_ws, const float* s_ws) {
+  if (T < 0 || n1 < 1 || n2 < 1 || N < 0) return FQ_EINVAL;
   const int64_t n = int64_t(n1) * n2;
   if (n > INT32_MAX) return FQ_ESHAPE;
   if (y_dtype != FQ_F16 && y_dtype != FQ_BF16) return FQ_EINVAL;
@@ -203,6 +267,18 @@ fq_status fq_flatquant_linear(const void* x, int32_t x_dtype, int64_t T, int32_t
   if (s != FQ_OK || N == 0) return s;
   if (!sw) return FQ_EINVAL;
   if (!aligned16(sw)) return FQ_ESHAPE;
+  return FQ_OK;
+}
+}  // namespace fq
+
+extern "C" {
+
+fq_status fq_flatquant_linear(const void* x, int32_t x_dtype, int64_t T, int32_t n1, int32_t n2,
+                              const void* p1, const void* p2, float alpha, const uint8_t* qw, const float* sw,
+                              int32_t N, void* y, int32_t y_dtype, uint8_t* q_ws, float* s_ws, void* stream) {
+  fq_status s = validate_linear(x, x_dtype, T, n1, n2, p1, p2, alpha, qw, sw, N, y, y_dtype, q_ws, s_ws);
+  if (s != FQ_OK || T == 0 || N == 0) return s;
+  const int64_t n = int64_t(n1) * n2;
   s = run_tq(x, x_dtype, T, n, n1, n2, p1, p2, alpha, q_ws, s_ws, nullptr, nullptr, stream);
   if (s != FQ_OK) return s;
   return run_gemm(q_ws, s_ws, T, int32_t(n), qw, sw, N, y, y_dtype == FQ_BF16, false, stream);
@@ -222,17 +298,22 @@ fq_status fq_flatquant_linear_host_async(const void* x_host, void* x_dev, int32_
                                          int32_t n2, const void* p1, const void* p2, float alpha, const uint8_t* qw,
                                          const float* sw, int32_t N, void* y_host, void* y_dev, int32_t y_dtype,
                                          uint8_t* q_ws, float* s_ws, void* stream) {
-  if (T < 0) return FQ_EINVAL;
-  if (T == 0) return FQ_OK;
+  fq_status s = validate_linear(x_dev, x_dtype, T, n1, n2, p1, p2, alpha, qw, sw, N, y_dev, y_dtype, q_ws, s_ws);
+  if (s != FQ_OK || T == 0) return s;
   if (!x_host || !x_dev || !y_host || !y_dev) return FQ_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t xbytes = size_t(T) * size_t(n1) * size_t(n2) * 2;
   const size_t ybytes = size_t(T) * size_t(N) * 2;
-  fq_status s = cuda_status(cudaMemcpyAsync(x_dev, x_host, xbytes, cudaMemcpyHostToDevice, st));
+  s = cuda_status(cudaMemcpyAsync(x_dev, x_host, xbytes, cudaMemcpyHostToDevice, st));
   if (s != FQ_OK) return s;
-  s = fq_flatquant_linear(x_dev, x_dtype, T, n1, n2, p1, p2, alpha, qw, sw, N, y_dev, y_dtype, q_ws, s_ws, stream);
-  if (s != FQ_OK) return s;
-  return cuda_status(cudaMemcpyAsync(y_host, y_dev, ybytes, cudaMemcpyDeviceToHost, st));
+  clear_outputs(st);               // the copy completes before any later kernel starts
+  if (N > 0) {
+    s = fq_flatquant_linear(x_dev, x_dtype, T, n1, n2, p1, p2, alpha, qw, sw, N, y_dev, y_dtype, q_ws, s_ws, stream);
+    if (s != FQ_OK) return s;
+  }
+  s = cuda_status(cudaMemcpyAsync(y_host, y_dev, ybytes, cudaMemcpyDeviceToHost, st));
+  if (s == FQ_OK) clear_outputs(st);
+  return s;
 }
 
 fq_status fq_weight_colsum(const uint8_t* qw, int32_t N, int32_t K, int32_t* colsum, void* stream) {
@@ -241,7 +322,9 @@ fq_status fq_weight_colsum(const uint8_t* qw, int32_t N, int32_t K, int32_t* col
   if (!qw || !colsum) return FQ_EINVAL;
   if (K % 2 != 0) return FQ_ESHAPE;
   if ((reinterpret_cast<uintptr_t>(colsum) & 3u) != 0) return FQ_ESHAPE;
-  return cuda_status(weight_colsum_launch(qw, N, K, colsum, static_cast<cudaStream_t>(stream)));
+  const fq_status s = cuda_status(weight_colsum_launch(qw, N, K, colsum, static_cast<cudaStream_t>(stream)));
+  if (s == FQ_OK) record_outputs(static_cast<cudaStream_t>(stream), {span(colsum, size_t(N) * 4)});
+  return s;
 }
 
 uint64_t fq_prepare_weight_workspace_size(int32_t n1, int32_t n2) {
@@ -286,9 +369,10 @@ fq_status fq_prepare_weight(const void* w, int32_t w_dtype, int32_t N, int64_t l
     s = cuda_status(weight_colsum_launch(qw, N, n1 * n2, colsum_w, st));
     if (s != FQ_OK) return s;
   }
-  // the prepared weights are parameters of the hot-path kernels, which read them before waiting
-  // for the preceding kernel (PDL): return only once they are written
-  return cuda_status(cudaStreamSynchronize(st));
+  // return once the prepared weights are written (the caller may hand them to another stream)
+  s = cuda_status(cudaStreamSynchronize(st));
+  if (s == FQ_OK) clear_outputs(st);
+  return s;
 }
 
 fq_status fq_kv_quant(const void* kv, int32_t kv_dtype, int64_t R, int64_t ldkv, int32_t head_dim,
@@ -312,7 +396,10 @@ fq_status fq_kv_quant(const void* kv, int32_t kv_dtype, int64_t R, int64_t ldkv,
   a.bf16 = kv_dtype == FQ_BF16;
   a.stream = static_cast<cudaStream_t>(stream);
   if (!kv_quant_supported(a)) return FQ_ESHAPE;
-  return cuda_status(kv_quant_launch(a));
+  const fq_status s = cuda_status(kv_quant_launch(a));
+  if (s == FQ_OK)
+    record_outputs(a.stream, {span(q, size_t(R) * size_t(head_dim / 2)), span(scale, size_t(R) * 4), span(zero, size_t(R))});
+  return s;
 }
 
 fq_status fq_choose_decomposition(int64_t n, int32_t* n1, int32_t* n2) {

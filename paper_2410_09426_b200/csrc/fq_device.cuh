@@ -105,4 +105,50 @@ FQ_DEVICE float warp_max(float v) {
   return v;
 }
 
+// Exponent e with max * 2^e in [2^14, 2^15) for a finite max >= 0 (biased-exponent arithmetic,
+// exact); 0 for max == 0; clamped to [-126, 126].
+FQ_DEVICE int p2_scale_exp(uint32_t max_bits) {
+  const int be = int(max_bits >> 23);
+  if (max_bits == 0) return 0;
+  const int e = 14 - ((be == 0 ? 1 : be) - 127);
+  return e < -126 ? -126 : (e > 126 ? 126 : e);
+}
+
+// A bf16 matrix P (row-major, `elems` entries at p, 16-byte aligned, in shared memory) becomes
+// fp16 P * 2^e IN PLACE, with e from p2_scale_exp(max |P|) so that the largest entry lands in
+// [2^14, 2^15): every bf16 entry >= 2^-17 of that range is exact in fp16 (8-bit bf16 mantissa),
+// none can overflow, and the caller divides 2^e out of the result exactly (DESIGN.md reading
+// R9: the second Kronecker stage runs in fp16 with its fp16 intermediate).  Whole block; `red`
+// is one shared word; returns e.  Ends with the smem writes visible to the async proxy and
+// the block synchronised.
+FQ_DEVICE int bf16_to_f16_pow2(uint8_t* p, int elems, uint32_t* red) {
+  uint4* v4 = reinterpret_cast<uint4*>(p);
+  const int n4 = elems / 8;
+  if (threadIdx.x == 0) *red = 0u;
+  __syncthreads();
+  uint32_t m = 0;
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+    const uint4 v = v4[i];
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) m = max(m, max((w[h] << 16) & 0x7FFFFFFFu, w[h] & 0x7FFF0000u));
+  }
+  m = __reduce_max_sync(0xffffffffu, m);        // |x| bit patterns order like the values
+  if ((threadIdx.x & 31) == 0) atomicMax(red, m);
+  __syncthreads();
+  const int e = p2_scale_exp(*red);
+  const float sc = __int_as_float((127 + e) << 23);
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+    uint4 v = v4[i];
+    uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+    for (int h = 0; h < 4; ++h)
+      w[h] = pack_half2(__uint_as_float(w[h] << 16) * sc, __uint_as_float(w[h] & 0xFFFF0000u) * sc);
+    v4[i] = v;
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncthreads();
+  return e;
+}
+
 }  // namespace fq

@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(THREADS, FQ_DEC_MINB)
 gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA,
                 const float* __restrict__ sa, int T, int TN, int K, const float* __restrict__ sw, int N,
                 void* __restrict__ yv, const int8_t* __restrict__ za, const int32_t* __restrict__ colsum,
-                int S) {
+                int S, int params_early) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;                                        // widened stages [W 16 KB | A 8 KB]
@@ -218,14 +218,16 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   if (warp == TMA_WARP) {
     // ======================= TMA producer =======================
     if (lane == 0) {
-      // the weights do not depend on the previous kernel: start streaming them before the wait
+      // the weights are parameters: unless the preceding kernel of the stream writes them
+      // (host-side hazard check, fq_abi.cu), start streaming them before the wait
+      if (!params_early) tc::griddep_wait();
       const int pre = nk < PSTAGES ? nk : PSTAGES;
       for (int j = 0; j < pre; ++j) {
         if (j < 36) dtrace(tslot, 4 + j);
         tc::mbar_expect_tx(&pfull[j], uint32_t(WP_BYTES + ap_bytes));
         tc::tma_load_2d(sP + size_t(j) * P_BYTES, &tmW, &pfull[j], kb_of(j) * (BK / 2), fb * BM);
       }
-      tc::griddep_wait();                        // qa written by the transform kernel is visible
+      if (params_early) tc::griddep_wait();      // qa written by the transform kernel is visible
       for (int j = 0; j < pre; ++j)
         tc::tma_load_2d(sP + size_t(j) * P_BYTES + WP_BYTES, &tmA, &pfull[j], kb_of(j) * (BK / 2), 0);
       for (int j = pre; j < nk; ++j) {
@@ -334,8 +336,8 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         s_sw[e] = o < N ? __ldg(sw + o) : 0.f;
         if constexpr (ASYM) s_cs[e] = o < N ? __ldg(colsum + o) : 0;
         if (e < TN_MAX) {
-          s_sa[e] = e < T ? sa[e] * (1.0f / 256.0f) : 0.f;
-          if constexpr (ASYM) s_za[e] = e < T ? int(za[e]) * 256 : 0;
+          s_sa[e] = e < T ? sa[e] * (ASYM ? 1.0f : 1.0f / 256.0f) : 0.f;
+          if constexpr (ASYM) s_za[e] = e < T ? int(za[e]) : 0;
         }
       }
     }
@@ -391,13 +393,13 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         *reinterpret_cast<int4*>(static_cast<int32_t*>(yv) + size_t(t) * N + o) =
             make_int4(acc.x >> 8, acc.y >> 8, acc.z >> 8, acc.w >> 8);
       } else {
-        if constexpr (ASYM) {                  // acc_true = acc - (z - 8) colsum_w; TMEM held 256 acc
-          const int zc = s_za[t];
+        if constexpr (ASYM) {                  // acc_true = acc - (z - 8) colsum_w after the exact >> 8
+          const int zc = s_za[t];              // (TMEM held 256 acc), so no int32 wrap for K < 131072
           const int4 cs = *reinterpret_cast<const int4*>(s_cs + f0);
-          acc.x -= zc * cs.x;
-          acc.y -= zc * cs.y;
-          acc.z -= zc * cs.z;
-          acc.w -= zc * cs.w;
+          acc.x = (acc.x >> 8) - zc * cs.x;
+          acc.y = (acc.y >> 8) - zc * cs.y;
+          acc.z = (acc.z >> 8) - zc * cs.z;
+          acc.w = (acc.w >> 8) - zc * cs.w;
         }
         const float s_a = s_sa[t];
         const float4 w = *reinterpret_cast<const float4*>(s_sw + f0);
@@ -434,7 +436,7 @@ extern "C" int fq_debug_trace_dec(unsigned long long* out) {
 #endif
 
 bool gemm_dec_supported(const GemmArgs& a) {
-  return a.T >= 1 && a.T <= gd::TN_MAX && a.K % 32 == 0 && a.K <= 131072 && a.N % 8 == 0 && tmap_available();
+  return a.T >= 1 && a.T <= gd::TN_MAX && a.K % 32 == 0 && a.K < 131072 && a.N % 8 == 0 && tmap_available();
 }
 
 static int dec_policy() {                         // FQ_DEC_POLICY: testing aid (0/1/2)
@@ -495,13 +497,9 @@ cudaError_t gemm_dec_launch(const GemmArgs& a, int split) {
   auto kern = a.out_i32 ? gemm_dec_kernel<true, false, false>
               : asym    ? (a.y_bf16 ? gemm_dec_kernel<false, true, true> : gemm_dec_kernel<false, false, true>)
                         : (a.y_bf16 ? gemm_dec_kernel<false, true, false> : gemm_dec_kernel<false, false, false>);
-  static bool attr_done[5] = {false, false, false, false, false};
+  static std::atomic<uint64_t> attr_done[5];   // per kernel variant: devices configured
   const int which = a.out_i32 ? 0 : (a.y_bf16 ? 1 : 2) + (asym ? 2 : 0);
-  if (!attr_done[which]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    if (e != cudaSuccess) return e;
-    attr_done[which] = true;
-  }
+  if (cudaError_t e = ensure_smem_attr(kern, int(SMEM_BYTES), attr_done[which]); e != cudaSuccess) return e;
   const int TN = int((a.T + 15) / 16) * 16;
   CUtensorMap mw{}, ma{};
   {
@@ -531,7 +529,8 @@ cudaError_t gemm_dec_launch(const GemmArgs& a, int split) {
     std::fprintf(stderr, "[fq] decode GEMM N=%d K=%d T=%lld: split %d, %d CTAs, max resident clusters %d\n", a.N,
                  a.K, (long long)a.T, S, fbs * S, dec_max_clusters(reinterpret_cast<const void*>(kern), S));
   cudaError_t e = launch_pdl_policy(kern, dim3(unsigned(fbs * S)), dim3(THREADS), SMEM_BYTES, a.stream, S,
-                                    dec_policy(), mw, ma, a.sa, int(a.T), TN, a.K, a.sw, a.N, a.y, a.za, a.colsum, S);
+                                    dec_policy(), mw, ma, a.sa, int(a.T), TN, a.K, a.sw, a.N, a.y, a.za, a.colsum, S,
+                                    int(a.params_early));
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

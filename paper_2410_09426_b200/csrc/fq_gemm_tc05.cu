@@ -8,7 +8,7 @@
 // HIGH half of a byte whose low half is zero IS 16*q as a signed int8 (q in [-8,7] -> 16q in
 // [-128,112]); one AND (odd elements) or SHL+AND (even elements) per 4 bytes.  Both operands are
 // widened that way, so the tensor core accumulates 256*acc exactly (|256 acc| <= 256*64*K < 2^31
-// for K <= 131072) and the epilogue divides by 256 exactly.  Inside each 32-element group the
+// for K < 131072) and the epilogue divides by 256 exactly.  Inside each 32-element group the
 // int8 K order is a fixed permutation of the packed order, identical for A and B, so every dot
 // product is unchanged.
 //
@@ -47,7 +47,7 @@ constexpr int A_WARP0 = 5, NUM_A_WARPS = 4;   // warps 5..8 (TMEM lane quarter =
 constexpr int B_WARP0 = 9, NUM_B_WARPS = 4;   // warps 9..12 (one B row per thread)
 constexpr int THREADS = (B_WARP0 + NUM_B_WARPS) * 32;
 constexpr size_t SMEM_BYTES = size_t(STAGES) * B_BYTES + 1024 + 256;
-constexpr int MAX_K = 131072;
+constexpr int MAX_K = 131040;   // largest K % 32 == 0 with 256 * 64 * K < 2^31
 constexpr uint32_t IDESC = tc::idesc_i8(BM, BN);
 
 static_assert(TMEM_A0 + STAGES * A_COLS <= TMEM_COLS, "TMEM budget");
@@ -295,13 +295,9 @@ cudaError_t gemm_tc05_launch(const GemmArgs& a) {
   using namespace g2;
   auto kern = a.out_i32 ? gemm_tc05_kernel<true, false>
                         : (a.y_bf16 ? gemm_tc05_kernel<false, true> : gemm_tc05_kernel<false, false>);
-  static bool attr_done[3] = {false, false, false};
+  static std::atomic<uint64_t> attr_done[3];   // per kernel variant: devices configured
   const int which = a.out_i32 ? 0 : (a.y_bf16 ? 1 : 2);
-  if (!attr_done[which]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    if (e != cudaSuccess) return e;
-    attr_done[which] = true;
-  }
+  if (cudaError_t e = ensure_smem_attr(kern, int(SMEM_BYTES), attr_done[which]); e != cudaSuccess) return e;
   const int num_tiles = int((a.T + BM - 1) / BM) * ((a.N + BN - 1) / BN);
   const int grid = std::min(num_tiles, num_sms());
   kern<<<grid, THREADS, SMEM_BYTES, a.stream>>>(a.qa, a.sa, int(a.T), a.K, a.qw, a.sw, a.N, a.y);

@@ -421,9 +421,12 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           }
         }
       } else {
-        const float s_a = row_ok ? sa[row] * (1.0f / 256.0f) : 0.f;
-        // asymmetric activations: acc_true = acc - (z - 8) colsum_w; the TMEM holds 256 acc
-        const int zc256 = (ASYM && row_ok) ? int(za[row]) * 256 : 0;
+        // the TMEM holds 256 acc exactly (|256 acc| <= 2^14 K < 2^31 for K < 131072).  Symmetric:
+        // float(256 acc) * (s_a / 256) is exactly float(acc) * s_a (power-of-two scaling).
+        // Asymmetric: acc_true = acc - (z - 8) colsum_w is formed after the exact >> 8, in int32
+        // (|acc_true| <= 120 K), so it cannot wrap for any supported K.
+        const float s_a = row_ok ? sa[row] * (ASYM ? 1.0f : 1.0f / 256.0f) : 0.f;
+        const int zc = (ASYM && row_ok) ? int(za[row]) : 0;
         // one chunk of NC (64 or 32) columns: TMEM -> dequant -> swizzled staging -> TMA store
         auto emit = [&](auto nc_tag, int c0off) {
           constexpr int NC = decltype(nc_tag)::value;
@@ -450,14 +453,14 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 c0 = __ldg(reinterpret_cast<const int4*>(colsum + col));
                 c1 = __ldg(reinterpret_cast<const int4*>(colsum + col + 4));
               }
-              vv[0] -= uint32_t(zc256 * c0.x);
-              vv[1] -= uint32_t(zc256 * c0.y);
-              vv[2] -= uint32_t(zc256 * c0.z);
-              vv[3] -= uint32_t(zc256 * c0.w);
-              vv[4] -= uint32_t(zc256 * c1.x);
-              vv[5] -= uint32_t(zc256 * c1.y);
-              vv[6] -= uint32_t(zc256 * c1.z);
-              vv[7] -= uint32_t(zc256 * c1.w);
+              vv[0] = uint32_t((int(vv[0]) >> 8) - zc * c0.x);
+              vv[1] = uint32_t((int(vv[1]) >> 8) - zc * c0.y);
+              vv[2] = uint32_t((int(vv[2]) >> 8) - zc * c0.z);
+              vv[3] = uint32_t((int(vv[3]) >> 8) - zc * c0.w);
+              vv[4] = uint32_t((int(vv[4]) >> 8) - zc * c1.x);
+              vv[5] = uint32_t((int(vv[5]) >> 8) - zc * c1.y);
+              vv[6] = uint32_t((int(vv[6]) >> 8) - zc * c1.z);
+              vv[7] = uint32_t((int(vv[7]) >> 8) - zc * c1.w);
             }
             const float f0 = float(int(vv[0])) * s_a * w0.x, f1 = float(int(vv[1])) * s_a * w0.y;
             const float f2 = float(int(vv[2])) * s_a * w0.z, f3 = float(int(vv[3])) * s_a * w0.w;
@@ -523,7 +526,7 @@ extern "C" int fq_debug_trace_gemm(unsigned long long* out) {
 #endif
 
 bool gemm_pair_supported(const GemmArgs& a) {
-  return a.K % 32 == 0 && a.K <= 131072 && a.N % 8 == 0 && a.T <= int64_t(1) << 30 && tmap_available();
+  return a.K % 32 == 0 && a.K < 131072 && a.N % 8 == 0 && a.T <= int64_t(1) << 30 && tmap_available();
 }
 
 // Tile width per shape.  A pair tile's main loop is bound by the A conversion (256 activation
@@ -559,13 +562,9 @@ static cudaError_t launch_bn(const GemmArgs& a) {
               : asym    ? (a.y_bf16 ? gemm_pair_kernel<BN, false, true, true> : gemm_pair_kernel<BN, false, false, true>)
                         : (a.y_bf16 ? gemm_pair_kernel<BN, false, true, false>
                                     : gemm_pair_kernel<BN, false, false, false>);
-  static bool attr_done[5] = {false, false, false, false, false};
+  static std::atomic<uint64_t> attr_done[5];   // per kernel variant: devices configured
   const int which = a.out_i32 ? 0 : (a.y_bf16 ? 1 : 2) + (asym ? 2 : 0);
-  if (!attr_done[which]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(GE::SMEM_BYTES));
-    if (e != cudaSuccess) return e;
-    attr_done[which] = true;
-  }
+  if (cudaError_t e = ensure_smem_attr(kern, int(GE::SMEM_BYTES), attr_done[which]); e != cudaSuccess) return e;
   CUtensorMap ma{}, mb{}, my{}, my32{};
   {
     const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.T)};

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstdint>
 #include <algorithm>
+#include <atomic>
 #include <utility>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -26,6 +27,7 @@ struct TQArgs {
   float* y;         // optional fp32 export of the transformed activations (debug / parity)
   int8_t* zero;     // FQ_ASYM: per-token zero point - 8 (output); nullptr for FQ_SYM
   bool bf16;
+  bool params_early;  // PDL: p1 / p2 may be read before griddepcontrol.wait (fq_abi.cu hazard check)
   cudaStream_t stream;
 };
 
@@ -42,6 +44,7 @@ struct GemmArgs {
   const int32_t* colsum;    // asymmetric activations: sum_k qw[o,k] per output channel
   bool y_bf16;
   bool out_i32;
+  bool params_early;  // PDL: qw / sw / colsum may be read before griddepcontrol.wait (fq_abi.cu)
   cudaStream_t stream;
 };
 
@@ -60,6 +63,21 @@ struct KVArgs {     // KV-cache quantization (fq_kv_quant)
 
 int num_sms();
 void count_launch();
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies per device context: set it once per
+// device for one kernel; `done` (a static at the launch site, one per kernel variant) holds a bit
+// per device id < 64 already configured (larger ids are configured on every launch).
+template <typename K>
+cudaError_t ensure_smem_attr(K kern, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = dev < 64 ? uint64_t(1) << dev : 0;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_release);
+  return e;
+}
 bool pdl_enabled();      // FQ_PDL=0 in the environment disables programmatic dependent launch
 
 // Launch with programmatic stream serialization (PDL: the kernel may start while the previous
@@ -110,6 +128,7 @@ cudaError_t launch_pdl_policy(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 }
 
 cudaError_t transform_quant_launch(const TQArgs& a);   // impl selection (fq_set_tq_impl)
+bool tq_kernel_available(const TQArgs& a);             // some kernel serves this call
 bool tq_simt_supported(int n1, int n2);
 bool tq_mma_supported(int n1, int n2);                 // legacy mma.sync kernel instantiations
 cudaError_t tq_mma_launch(const TQArgs& a);

@@ -205,12 +205,8 @@ template <int D, bool BF16>
 static cudaError_t launch(const KVArgs& a) {
   using C = Cfg<D>;
   auto kern = kv_quant_kernel<D, BF16>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};   // devices configured for this kernel
+  if (cudaError_t e = ensure_smem_attr(kern, int(C::SMEM), attr_done); e != cudaSuccess) return e;
   CUtensorMap mx, mp;
   {
     const uint64_t dims[2] = {uint64_t(D), uint64_t(a.R)};

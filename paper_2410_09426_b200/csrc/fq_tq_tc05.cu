@@ -175,7 +175,8 @@ template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM, bool SMALL = false
 __global__ void __launch_bounds__(Cfg<N1, N2, SMALL>::THREADS, 1)
 tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmP1,
                const __grid_constant__ CUtensorMap tmP2, int64_t T, float alpha, uint8_t* __restrict__ q,
-               float* __restrict__ scale, float* __restrict__ y_out, int8_t* __restrict__ zero) {
+               float* __restrict__ scale, float* __restrict__ y_out, int8_t* __restrict__ zero,
+               int params_early) {
   using C = Cfg<N1, N2, SMALL>;
   constexpr int S = C::STAGES, TOK = C::TOK, G = C::GROUPS, THREADS = C::THREADS;
   constexpr uint32_t IDESC1 = tc::idesc_f16(128, N1, BF16 ? 1 : 0, 1, 1);
@@ -233,13 +234,17 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     }
     tc::fence_barrier_init();
     tc::griddep_launch();              // the next kernel may start launching (PDL)
-    // P1, P2 are parameters (ABI contract: not written by kernels still in flight), so they
-    // stream in while the preceding kernel finishes; X is that kernel's output
-    tc::mbar_expect_tx(pfull, C::P1_BYTES + C::P2_BYTES);
-    for (int a = 0; a < C::P1_ATOMS; ++a) tc::tma_load_2d(sP1 + a * N1 * 128, &tmP1, pfull, a * 64, 0);
-    for (int b = 0; b < C::JB; ++b) tc::tma_load_2d(sP2 + b * N2 * 128, &tmP2, pfull, b * 64, 0);
+    // P1, P2 are parameters: unless the preceding kernel of the stream writes them (host-side
+    // hazard check, fq_abi.cu), they stream in while that kernel finishes; X is its output
+    auto load_p = [&] {
+      tc::mbar_expect_tx(pfull, C::P1_BYTES + C::P2_BYTES);
+      for (int a = 0; a < C::P1_ATOMS; ++a) tc::tma_load_2d(sP1 + a * N1 * 128, &tmP1, pfull, a * 64, 0);
+      for (int b = 0; b < C::JB; ++b) tc::tma_load_2d(sP2 + b * N2 * 128, &tmP2, pfull, b * 64, 0);
+    };
+    if (params_early) load_p();
     trace(3);
     tc::griddep_wait();                // inputs of this kernel are final (PDL)
+    if (!params_early) load_p();
     trace(4);
     for (int k = 0; k < prefill; ++k) issue_x(k);
     trace(1);
@@ -252,20 +257,15 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
 
   tc::mbar_wait(pfull, 0);
   if (threadIdx.x == 0) trace(2);
+  // stage 2 runs in fp16 (R9): a bf16 P2 becomes fp16 P2 * 2^e2 in place (power-of-two scaled
+  // into fp16 range, so no entry overflows); 2^-e2 is applied to the statistics below, exactly
+  float inv_p2 = 1.0f;
   if constexpr (BF16) {
-    // stage 2 runs in fp16 (R9): convert P2 in place (bf16 -> fp16 is exact in normal range)
-    for (int i = threadIdx.x; i < C::P2_BYTES / 16; i += THREADS) {
-      uint4* p = reinterpret_cast<uint4*>(sP2) + i;
-      uint4 v = *p;
-      uint32_t* w = reinterpret_cast<uint32_t*>(&v);
-#pragma unroll
-      for (int h = 0; h < 4; ++h)
-        w[h] = pack_half2(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xFFFF0000u));
-      *p = v;
-    }
-    tc::fence_proxy_async_smem();
+    __shared__ uint32_t p2max;
+    inv_p2 = exp2i(-bf16_to_f16_pow2(sP2, C::P2_BYTES / 2, &p2max));
+  } else {
+    __syncthreads();
   }
-  __syncthreads();
 
   if (warp == 0) {
     // ================================ TMA producer ================================
@@ -477,17 +477,18 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
             float2* yd = reinterpret_cast<float2*>(y_out + t * (N1 * N2) + i * N2 + col);   // 8-B aligned (ABI)
 #pragma unroll
             for (int e = 0; e < 16; ++e)
-              yd[e] = make_float2(__uint_as_float(v[2 * e]) * inv_pre, __uint_as_float(v[2 * e + 1]) * inv_pre);
+              yd[e] = make_float2(__uint_as_float(v[2 * e]) * inv_pre * inv_p2,
+                                  __uint_as_float(v[2 * e + 1]) * inv_pre * inv_p2);
           }
         }
       });
       tc::fence_before();
       if (store && i == 0) {
         if constexpr (ASYM) {
-          scale[t] = mp > 0.f ? alpha * (mp * inv_pre) / 15.0f : 1.0f;
+          scale[t] = mp > 0.f ? alpha * (mp * inv_pre * inv_p2) / 15.0f : 1.0f;
           zero[t] = int8_t(int(zq) - 8);
         } else {
-          scale[t] = mp > 0.f ? alpha * (mp * inv_pre) / 7.0f : 1.0f;
+          scale[t] = mp > 0.f ? alpha * (mp * inv_pre * inv_p2) / 7.0f : 1.0f;
         }
       }
       if (L == 0 && k < 16) trace(104 + k);
@@ -521,12 +522,8 @@ template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM = false, bool SMALL
 static cudaError_t launch(const TQArgs& a) {
   using C = Cfg<N1, N2, SMALL>;
   auto kern = tq_tc05_kernel<N1, N2, BF16, WRITE_Y, ASYM, SMALL>;
-  static bool attr_set = false;   // benign race: idempotent attribute set
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};   // devices configured for this kernel
+  if (cudaError_t e = ensure_smem_attr(kern, int(C::SMEM), attr_done); e != cudaSuccess) return e;
   CUtensorMap mx, m1, m2;
   {
     const uint64_t dims[3] = {uint64_t(N2), uint64_t(N1), uint64_t(a.T)};
@@ -549,7 +546,7 @@ static cudaError_t launch(const TQArgs& a) {
   const int64_t tiles = (a.T + C::TOK - 1) / C::TOK;
   const int grid = int(std::min<int64_t>(tiles, num_sms()));
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(C::THREADS), C::SMEM, a.stream, 1, mx, m1, m2, a.T, a.alpha,
-                             a.q, a.scale, a.y, a.zero);
+                             a.q, a.scale, a.y, a.zero, int(a.params_early));
   count_launch();
   return e;
 }

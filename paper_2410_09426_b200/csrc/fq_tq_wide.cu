@@ -98,7 +98,8 @@ template <int N2, bool BF16, bool WRITE_Y, bool ASYM>
 __global__ void __launch_bounds__(THREADS, 1)
 tq_wide_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmP1,
                const __grid_constant__ CUtensorMap tmP2, int64_t T, float alpha, uint8_t* __restrict__ q,
-               float* __restrict__ scale, float* __restrict__ y_out, int8_t* __restrict__ zero) {
+               float* __restrict__ scale, float* __restrict__ y_out, int8_t* __restrict__ zero,
+               int params_early) {
   using C = Cfg<N2>;
   constexpr int S = C::STAGES;
   constexpr uint32_t IDESC1 = tc::idesc_f16(128, N2, BF16 ? 1 : 0, 1, 1);
@@ -147,10 +148,14 @@ tq_wide_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     tc::mbar_init(d2empty, 4);
     tc::fence_barrier_init();
     tc::griddep_launch();              // the next kernel may start launching (PDL)
-    tc::mbar_expect_tx(pfull, C::P1_BYTES + C::P2_BYTES);   // parameters: before the wait
-    for (int a = 0; a < 2; ++a) tc::tma_load_2d(sP1 + a * N1 * 128, &tmP1, pfull, a * 64, 0);
-    for (int b = 0; b < C::JB; ++b) tc::tma_load_2d(sP2 + b * N2 * 128, &tmP2, pfull, b * 64, 0);
+    auto load_p = [&] {                // parameters: before the wait unless the preceding kernel writes them
+      tc::mbar_expect_tx(pfull, C::P1_BYTES + C::P2_BYTES);
+      for (int a = 0; a < 2; ++a) tc::tma_load_2d(sP1 + a * N1 * 128, &tmP1, pfull, a * 64, 0);
+      for (int b = 0; b < C::JB; ++b) tc::tma_load_2d(sP2 + b * N2 * 128, &tmP2, pfull, b * 64, 0);
+    };
+    if (params_early) load_p();
     tc::griddep_wait();                // X of the preceding kernel is final (PDL)
+    if (!params_early) load_p();
     for (int k = 0; k < prefill; ++k) issue_x(k);
   }
   if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
@@ -160,18 +165,12 @@ tq_wide_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
   const uint32_t tmem = *tmem_slot;
 
   tc::mbar_wait(pfull, 0);
+  // stage 2 runs in fp16 (R9): a bf16 P2 becomes fp16 P2 * 2^e2 in place (no overflow); the
+  // statistics divide 2^e2 out exactly
+  float inv_p2 = 1.0f;
   if constexpr (BF16) {
-    // stage 2 runs in fp16 (R9): convert P2 in place (bf16 -> fp16 is exact in normal range)
-    for (int i = threadIdx.x; i < C::P2_BYTES / 16; i += THREADS) {
-      uint4* p = reinterpret_cast<uint4*>(sP2) + i;
-      uint4 v = *p;
-      uint32_t* w = reinterpret_cast<uint32_t*>(&v);
-#pragma unroll
-      for (int h = 0; h < 4; ++h)
-        w[h] = pack_half2(__uint_as_float(w[h] << 16), __uint_as_float(w[h] & 0xFFFF0000u));
-      *p = v;
-    }
-    tc::fence_proxy_async_smem();
+    __shared__ uint32_t p2max;
+    inv_p2 = exp2i(-bf16_to_f16_pow2(sP2, C::P2_BYTES / 2, &p2max));
   }
   __syncthreads();
 
@@ -314,7 +313,8 @@ tq_wide_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
           float2* yd = reinterpret_cast<float2*>(y_out + t * (N1 * N2) + i * N2 + c);
 #pragma unroll
           for (int e = 0; e < 16; ++e)
-            yd[e] = make_float2(__uint_as_float(v[2 * e]) * inv_pre, __uint_as_float(v[2 * e + 1]) * inv_pre);
+            yd[e] = make_float2(__uint_as_float(v[2 * e]) * inv_pre * inv_p2,
+                                __uint_as_float(v[2 * e + 1]) * inv_pre * inv_p2);
         }
       }
       tc::fence_before();
@@ -322,10 +322,10 @@ tq_wide_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
       if (lane == 0) tc::mbar_arrive(d2empty);
       if (i == 0) {
         if constexpr (ASYM) {
-          scale[t] = mp > 0.f ? alpha * (mp * inv_pre) / 15.0f : 1.0f;
+          scale[t] = mp > 0.f ? alpha * (mp * inv_pre * inv_p2) / 15.0f : 1.0f;
           zero[t] = int8_t(int(zq) - 8);
         } else {
-          scale[t] = mp > 0.f ? alpha * (mp * inv_pre) / 7.0f : 1.0f;
+          scale[t] = mp > 0.f ? alpha * (mp * inv_pre * inv_p2) / 7.0f : 1.0f;
         }
       }
     }
@@ -343,12 +343,8 @@ template <int N2, bool BF16, bool WRITE_Y, bool ASYM>
 static cudaError_t launch(const TQArgs& a) {
   using C = Cfg<N2>;
   auto kern = tq_wide_kernel<N2, BF16, WRITE_Y, ASYM>;
-  static bool attr_set = false;   // benign race: idempotent attribute set
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};   // devices configured for this kernel
+  if (cudaError_t e = ensure_smem_attr(kern, int(C::SMEM), attr_done); e != cudaSuccess) return e;
   CUtensorMap mx, m1, m2;
   {
     const uint64_t dims[3] = {uint64_t(N2), uint64_t(N1), uint64_t(a.T)};
@@ -370,7 +366,7 @@ static cudaError_t launch(const TQArgs& a) {
   }
   const int grid = int(std::min<int64_t>(a.T, num_sms()));
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(THREADS), C::SMEM, a.stream, 1, mx, m1, m2, a.T, a.alpha, a.q,
-                             a.scale, a.y, a.zero);
+                             a.scale, a.y, a.zero, int(a.params_early));
   count_launch();
   return e;
 }

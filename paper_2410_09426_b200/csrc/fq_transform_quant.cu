@@ -72,11 +72,27 @@ tq_mma_kernel(const uint16_t* __restrict__ x, int64_t T, int64_t ldx,
   // ---- P2 -> smem (whole CTA), padded rows, always as fp16: stage 2 runs in fp16 so the
   //      re-fed intermediate keeps an 11-bit mantissa (a bf16 intermediate fails the code
   //      parity bar).  bf16 -> fp16 is exact for normal-range entries. ----
+  //      A bf16 P2 is scaled by 2^e2 into fp16 range first (no entry overflows; 2^-e2 is
+  //      applied to the result exactly). ----
+  float p2_sc = 1.f, p2_inv = 1.f;
+  if constexpr (BF16 && !IDENT2) {
+    __shared__ uint32_t p2max;
+    if (threadIdx.x == 0) p2max = 0u;
+    __syncthreads();
+    uint32_t m = 0;
+    for (int i = threadIdx.x; i < N2 * N2; i += C::THREADS) m = max(m, (uint32_t(p2[i]) << 16) & 0x7FFFFFFFu);
+    m = __reduce_max_sync(0xffffffffu, m);
+    if (lane == 0) atomicMax(&p2max, m);
+    __syncthreads();
+    const int e2 = p2_scale_exp(p2max);
+    p2_sc = __int_as_float((127 + e2) << 23);
+    p2_inv = __int_as_float((127 - e2) << 23);
+  }
   for (int i = threadIdx.x; i < (IDENT2 ? 0 : N2 * N2); i += C::THREADS) {
     const int r = i / N2, c = i % N2;
     uint16_t v = p2[i];
     if constexpr (BF16) {
-      __half h = __float2half_rn(__uint_as_float(uint32_t(v) << 16));
+      __half h = __float2half_rn(__uint_as_float(uint32_t(v) << 16) * p2_sc);
       v = *reinterpret_cast<uint16_t*>(&h);
     }
     sP2[r * C::XPITCH + c] = v;
@@ -187,7 +203,7 @@ tq_mma_kernel(const uint16_t* __restrict__ x, int64_t T, int64_t ldx,
     for (int n = 0; n < NT; ++n)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        acc[n][e] *= inv_pre;
+        acc[n][e] = acc[n][e] * inv_pre * p2_inv;
         m = fmaxf(m, fabsf(acc[n][e]));
       }
     m = warp_max(m);
@@ -325,12 +341,8 @@ template <int N1, int N2, bool BF16, bool WRITE_Y, int TEAMS, int NBUF, bool IDE
 static cudaError_t launch_mma(const TQArgs& a) {
   using C = TQCfg<N1, N2, BF16, WRITE_Y, TEAMS, NBUF>;
   auto kern = tq_mma_kernel<N1, N2, BF16, WRITE_Y, TEAMS, NBUF, IDENT2>;
-  static bool attr_set = false;  // benign race: idempotent attribute set
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};   // devices configured for this kernel
+  if (cudaError_t e = ensure_smem_attr(kern, int(C::SMEM), attr_done); e != cudaSuccess) return e;
   const int64_t teams_needed = (a.T + TEAMS - 1) / TEAMS;
   int blocks_per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, C::THREADS, C::SMEM);
@@ -423,6 +435,18 @@ cudaError_t tq_simt_launch(const TQArgs& a) {
 // impl 1: mma.sync where instantiated, else CUDA cores;  impl 2: CUDA cores.
 bool tq_asym_supported(const TQArgs& a) {
   return (tq_impl() == 0 && (tq_tc05_supported(a) || tq_wide_supported(a))) || tq_simt_supported(a.n1, a.n2);
+}
+
+// true when transform_quant_launch has a kernel for this call (else the ABI returns FQ_ENOTSUP
+// instead of a launch that cannot fit its shared memory)
+bool tq_kernel_available(const TQArgs& a) {
+  const int impl = tq_impl();
+  if (a.p2 == nullptr) return tq_ident2_supported(a.n1, a.n2);
+  if (impl == 0 && (tq_tc05_supported(a) || tq_wide_supported(a))) return true;
+  if (impl == 0 && int64_t(a.n1) * a.n2 <= 1024 && tq_simt_supported(a.n1, a.n2)) return true;
+  const bool tc_shape = (a.n1 % 16 == 0) && (a.n2 % 16 == 0);
+  if (!a.zero && impl <= 1 && tc_shape && tq_mma_supported(a.n1, a.n2)) return true;
+  return tq_simt_supported(a.n1, a.n2);
 }
 
 cudaError_t transform_quant_launch(const TQArgs& a) {

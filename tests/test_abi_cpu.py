@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_status_strings():
     lib = fq.load()
-    assert fq.fq_abi_version() == 4
+    assert fq.fq_abi_version() == 5
     for s in range(5):
         assert lib.fq_status_string(s).startswith(b"FQ_")
     assert lib.fq_status_string(99) == b"unknown fq_status"
@@ -75,6 +75,10 @@ def test_transform_quant_validation():
     assert tq(ldx=516) == _lib.FQ_ESHAPE                  # row stride not 16-byte multiple
     assert tq(x=MIS) == _lib.FQ_ESHAPE
     assert tq(n1=512, n2=2, ldx=1024) == _lib.FQ_ENOTSUP
+    # multiples of 16 with no tensor-core kernel and too large for the CUDA-core kernel's shared
+    # memory: rejected up front, not launched
+    assert tq(n1=256, n2=256, ldx=65536) == _lib.FQ_ENOTSUP
+    assert tq(n1=192, n2=192, ldx=36864) == _lib.FQ_ENOTSUP
     # p2 = NULL means P2 = I (the paper's online P_o (x) I_{d_head}); only (32|64, 128), symmetric
     assert tq(p2=None) == _lib.FQ_ENOTSUP                 # 16 x 32: no P2 = I kernel
     assert tq(p2=None, n1=32, n2=128, ldx=4096, qmode=1, zero=A16) == _lib.FQ_ENOTSUP
@@ -105,6 +109,9 @@ def test_w4a4_linear_validation():
     assert lib0.fq_weight_colsum(A16, 0, 64, A16, None) == _lib.FQ_OK
     assert gemm(y=MIS) == _lib.FQ_ESHAPE
     assert gemm(K=262144) == _lib.FQ_ENOTSUP
+    # 256 |acc| <= 2^14 K must stay below 2^31 in the widened (16 q) accumulator: K < 131072
+    assert gemm(K=131072) == _lib.FQ_ENOTSUP
+    assert gemm(K=131072, za=A16, cs=A16) == _lib.FQ_ENOTSUP
     lib = fq.load()
     assert lib.fq_w4a4_gemm_i32(A16, 8, 40, A16, 16, A16, None) == _lib.FQ_ESHAPE
     assert lib.fq_w4a4_gemm_i32(None, 8, 64, A16, 16, A16, None) == _lib.FQ_EINVAL
@@ -182,4 +189,23 @@ def test_graft_entry_build_is_consistent():
     ABI assertion matches the header (cached build: no recompilation when nothing changed)."""
     import __graft_entry__ as g
     g.build()
-    assert fq.fq_abi_version() == 4
+    assert fq.fq_abi_version() == 5
+
+
+def test_linear_host_async_validates_before_copying():
+    """Every argument check of the hot path runs before the host-buffer entry point enqueues its
+    H2D copy (nothing is enqueued on error): bad alpha, N % 8, misaligned scales, negative n1."""
+    lib = fq.load()
+
+    def call(**kw):
+        a = dict(xh=A16, xd=A16, dt=0, T=4, n1=16, n2=32, p1=A16, p2=A16, alpha=0.9, qw=A16, sw=A16, N=16,
+                 yh=A16, yd=A16, ydt=0, q=A16, s=A16)
+        a.update(kw)
+        return lib.fq_flatquant_linear_host_async(a["xh"], a["xd"], a["dt"], a["T"], a["n1"], a["n2"], a["p1"],
+                                                  a["p2"], a["alpha"], a["qw"], a["sw"], a["N"], a["yh"], a["yd"],
+                                                  a["ydt"], a["q"], a["s"], None)
+    assert call(alpha=1.5) == _lib.FQ_EINVAL
+    assert call(N=12) == _lib.FQ_ESHAPE
+    assert call(sw=MIS) == _lib.FQ_ESHAPE
+    assert call(n1=-3) == _lib.FQ_EINVAL
+    assert call(T=0) == _lib.FQ_OK
