@@ -19,16 +19,20 @@
  *    is asynchronous with respect to the host unless stated otherwise.
  *  - Stream order.  Every call is ordered after the work already enqueued on `stream`, as
  *    with any CUDA library.  The kernels use programmatic dependent launch (PDL) to overlap
- *    their start with the tail of the preceding kernel: ACTIVATION inputs (x, qa, sa, za) are
- *    always read after griddepcontrol.wait; PARAMETERS (p1, p2, qw, sw, colsum_w) are read
- *    before it only when the library can tell that the preceding kernel does not write them --
- *    it records the outputs of the last kernel it enqueued on each stream and, if a parameter
- *    buffer overlaps them, the kernel reads its parameters after the wait instead.  Work of
- *    other origin between two calls (copies, kernels that do not trigger PDL early) completes
- *    before a PDL kernel may start, so the check is complete for this library's own kernels.
- *    The one case it cannot see: a kernel of ANOTHER library that triggers its dependents early
- *    (griddepcontrol.launch_dependents) and writes this library's parameters immediately before
- *    the call; synchronise or record an event between them in that case.
+ *    with the kernel before them: each kernel lets its dependents launch only after its own
+ *    griddepcontrol.wait has returned, so a kernel that has not yet waited can overlap only its
+ *    immediate predecessor on the stream.  The library records, per stream, the buffers its last
+ *    kernel reads and writes; the next kernel reads its parameters (p1, p2, qw, sw, colsum_w)
+ *    or its activations (x, qa, sa, za) before the wait only if the predecessor does not write
+ *    them, and writes its outputs before the wait only if the predecessor neither reads nor
+ *    writes them -- otherwise it waits first.  So weights and transforms stream in while the
+ *    previous kernel finishes, and a call whose buffers are disjoint from the previous call's
+ *    (e.g. the next layer linear's transform after a GEMM) runs concurrently with it, while
+ *    any real dependency (read-after-write, write-after-read, write-after-write) is ordered.
+ *    Work of other origin between two calls (copies, kernels without an early PDL trigger)
+ *    completes before a PDL kernel may start.  The one case the library cannot see: a kernel
+ *    of ANOTHER library that triggers its dependents early and touches this library's buffers
+ *    immediately before a call; synchronise or record an event between them in that case.
  *  - Argument validation is synchronous: on any error nothing is launched and a non-zero
  *    fq_status is returned.  T == 0 returns FQ_OK without launching.  A failed launch
  *    returns FQ_ECUDA; fq_last_cuda_error() returns the cudaError_t value.  Device faults
@@ -39,7 +43,7 @@
  *    transform when n1 % 16 == 0 and n2 % 16 == 0) need x, q, qa, qw, y and sw 16-byte
  *    aligned and row strides that are multiples of 16 bytes (FQ_ESHAPE otherwise).
  *  - Re-entrant.  Per-device kernel attributes are set once per (kernel, device), thread-safely;
- *    the only state is the per-stream record of the last launch's outputs (see Stream order),
+ *    the only state is the per-stream record of the last launch's buffers (see Stream order),
  *    guarded by a mutex.
  *  - Non-finite inputs give unspecified codes (the oracle's precondition is finite x).
  */
@@ -53,7 +57,7 @@ extern "C" {
 #endif
 
 #define FQ_ABI_VERSION 5   /* 2: FQ_ASYM + fq_weight_colsum; 3: fq_kv_quant, fq_prepare_weight; 4: p2 = NULL (P2 = I);
-                              5: K < 131072, PDL parameter hazard check, bf16 P2 scaled into fp16 range */
+                              5: K < 131072, PDL hazard check on inputs/outputs, bf16 P2 scaled into fp16 range */
 
 typedef enum {
   FQ_OK = 0,

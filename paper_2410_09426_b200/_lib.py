@@ -15,6 +15,9 @@ LIB_PATH = os.path.join(HERE, "libflatquant.so")
 # FQ_TRACE_LIB=1 loads the instrumented build (device timelines; profiling scripts only)
 if os.environ.get("FQ_TRACE_LIB") == "1":
     LIB_PATH = os.path.join(HERE, "libflatquant_trace.so")
+# FQ_LIB=<path>: an experiment build (paper_2410_09426_b200.build.build_variant); testing aid only
+if os.environ.get("FQ_LIB"):
+    LIB_PATH = os.environ["FQ_LIB"]
 
 FQ_OK, FQ_EINVAL, FQ_ESHAPE, FQ_ENOTSUP, FQ_ECUDA, FQ_ESINGULAR = 0, 1, 2, 3, 4, 5
 FQ_F16, FQ_BF16 = 0, 1

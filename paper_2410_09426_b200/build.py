@@ -67,6 +67,22 @@ def _compile(src: str, defs: list[str]) -> tuple[str, str]:
     return obj, log
 
 
+def build_variant(name: str, defines: list[str], only: list[str]) -> str:
+    """Experiment build (never loaded by the product): libflatquant_<name>.so with `defines`
+    applied to the sources named in `only`; load it with FQ_LIB=<path>."""
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    objs = []
+    for src in sources():
+        defs = defines if os.path.basename(src) in only else []
+        objs.append(_compile(src, defs)[0])
+    lib = os.path.join(HERE, f"libflatquant_{name}.so")
+    r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib] + objs,
+                       capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(r.stdout + r.stderr)
+    return lib
+
+
 def build(verbose: bool = False, force: bool = False, trace: bool = False) -> str:
     """Build libflatquant.so; trace=True builds the instrumented libflatquant_trace.so instead
     (-DFQ_TRACE: device timelines for scripts/trace_*.py; never loaded by the product)."""
@@ -106,7 +122,20 @@ def build(verbose: bool = False, force: bool = False, trace: bool = False) -> st
         sys.stderr.write(log)
     with open(stamp, "w") as f:
         f.write(dig)
+    _prune()
     return lib
+
+
+def _prune() -> None:
+    """drop cached objects of older source versions (keep the current plain and trace builds)"""
+    keep = set()
+    for src in sources():
+        for defs in ([], ["-DFQ_TRACE"]):
+            key = _hash([src] + _headers(), " ".join(NVCC_FLAGS + defs))[:16]
+            keep.add(f"{os.path.basename(src)[:-3]}-{key}.o")
+    for f in glob.glob(os.path.join(OBJ_DIR, "*.o")):
+        if os.path.basename(f) not in keep:
+            os.remove(f)
 
 
 if __name__ == "__main__":

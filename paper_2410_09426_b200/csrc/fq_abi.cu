@@ -45,16 +45,18 @@ int num_sms() {
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-// ---- programmatic dependent launch: parameter hazard check ----------------------------------
-// The tensor-core kernels trigger their dependents early (griddepcontrol.launch_dependents at
-// their start), so the next kernel of the stream may begin while they still write.  A kernel
-// launched with PDL may therefore read a buffer before its griddepcontrol.wait only if the
-// immediately preceding kernel does not write it.  Activations are always read after the wait.
-// Parameters (p1, p2, qw, sw, colsum_w) are read before it -- overlapping their loads with the
-// tail of the preceding kernel -- unless they overlap the outputs of the last kernel this library
-// enqueued on the same stream, in which case the kernel reads them after the wait.  Work enqueued
-// in between by anyone else (copies, kernels without early triggers) completes before a PDL
-// kernel may start, so tracking this library's own last launch per stream is sufficient.
+// ---- programmatic dependent launch: host-side hazard check ------------------------------------
+// Protocol (fq_internal.h): every PDL kernel of this library signals its dependents only after its
+// own griddepcontrol.wait has returned, so a kernel running BEFORE its wait can overlap only its
+// immediate predecessor on the stream.  Whatever else was enqueued earlier has completed by then;
+// so has any work of other origin in between (copies, kernels that do not trigger PDL early),
+// which a PDL kernel can never overlap.  The host therefore records, per stream, the buffers the
+// last kernel this library enqueued reads and writes, and lets the next kernel
+//   read its parameters early  (PDL_P)   if no parameter overlaps the predecessor's outputs,
+//   read its activations early (PDL_X)   if no activation overlaps the predecessor's outputs,
+//   write its outputs early    (PDL_OUT) if no output overlaps the predecessor's inputs or outputs.
+// Weights and P stream in while the previous kernel finishes, and a kernel whose data is disjoint
+// from its predecessor's (e.g. the next linear's transform after a GEMM) runs concurrently with it.
 struct Span {
   uintptr_t lo, hi;
 };
@@ -62,27 +64,43 @@ static Span span(const void* p, size_t bytes) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(p);
   return Span{a, p ? a + bytes : a};
 }
+using Spans = std::initializer_list<Span>;
+struct LaunchRec {
+  std::vector<Span> in, out;
+};
 static std::mutex g_pdl_mu;
-static std::unordered_map<void*, std::vector<Span>> g_pdl_out;   // stream -> outputs of our last launch
+static std::unordered_map<void*, LaunchRec> g_pdl_rec;   // stream -> last PDL kernel's buffers
 
-static bool params_early(cudaStream_t st, std::initializer_list<Span> params) {
-  std::lock_guard<std::mutex> lk(g_pdl_mu);
-  auto it = g_pdl_out.find(static_cast<void*>(st));
-  if (it == g_pdl_out.end()) return true;
-  for (const Span& o : it->second)
-    for (const Span& p : params)
-      if (p.lo < p.hi && o.lo < o.hi && p.lo < o.hi && o.lo < p.hi) return false;
-  return true;
+static bool overlap(Spans a, const std::vector<Span>& b) {
+  for (const Span& x : a)
+    for (const Span& y : b)
+      if (x.lo < x.hi && y.lo < y.hi && x.lo < y.hi && y.lo < x.hi) return true;
+  return false;
 }
-static void record_outputs(cudaStream_t st, std::initializer_list<Span> outs) {
+static int pdl_flags(cudaStream_t st, Spans params, Spans acts, Spans outs) {
   std::lock_guard<std::mutex> lk(g_pdl_mu);
-  auto& v = g_pdl_out[static_cast<void*>(st)];
-  v.assign(outs.begin(), outs.end());
+  auto it = g_pdl_rec.find(static_cast<void*>(st));
+  if (it == g_pdl_rec.end()) return PDL_P | PDL_X | PDL_OUT;
+  const LaunchRec& r = it->second;
+  int f = 0;
+  if (!overlap(params, r.out)) f |= PDL_P;
+  if (!overlap(acts, r.out)) f |= PDL_X;
+  if (!overlap(outs, r.out) && !overlap(outs, r.in)) f |= PDL_OUT;
+  return f;
 }
-static void clear_outputs(cudaStream_t st) {
+// after a launch: a PDL kernel becomes the stream's overlappable predecessor; after anything else
+// (a kernel without early trigger, a copy) the next kernel cannot start before it completes
+static void record_launch(cudaStream_t st, bool pdl_kernel, Spans ins, Spans outs) {
   std::lock_guard<std::mutex> lk(g_pdl_mu);
-  g_pdl_out.erase(static_cast<void*>(st));
+  if (!pdl_kernel) {
+    g_pdl_rec.erase(static_cast<void*>(st));
+    return;
+  }
+  LaunchRec& r = g_pdl_rec[static_cast<void*>(st)];
+  r.in.assign(ins.begin(), ins.end());
+  r.out.assign(outs.begin(), outs.end());
 }
+static void clear_outputs(cudaStream_t st) { record_launch(st, false, {}, {}); }
 
 static fq_status cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return FQ_OK;
@@ -135,11 +153,13 @@ static fq_status run_tq(const void* x, int32_t x_dtype, int64_t T, int64_t ldx, 
   if (!tq_kernel_available(a)) return FQ_ENOTSUP;
   if (zero && !tq_asym_supported(a)) return FQ_ENOTSUP;
   const int64_t n = int64_t(n1) * n2;
-  a.params_early = params_early(a.stream, {span(p1, size_t(n1) * n1 * 2), span(p2, size_t(n2) * n2 * 2)});
+  const Span sp1 = span(p1, size_t(n1) * n1 * 2), sp2 = span(p2, size_t(n2) * n2 * 2);
+  const Span sx = span(x, size_t(T - 1) * size_t(ldx) * 2 + size_t(n) * 2);
+  const Span sq = span(q, size_t(T) * size_t(n / 2)), ss = span(scale, size_t(T) * 4), sz = span(zero, size_t(T)),
+             sy = span(y, y ? size_t(T) * size_t(n) * 4 : 0);
+  a.pdl = pdl_flags(a.stream, {sp1, sp2}, {sx}, {sq, ss, sz, sy});
   const fq_status s = cuda_status(transform_quant_launch(a));
-  if (s == FQ_OK)
-    record_outputs(a.stream, {span(q, size_t(T) * size_t(n / 2)), span(scale, size_t(T) * 4),
-                              span(zero, size_t(T)), span(y, y ? size_t(T) * size_t(n) * 4 : 0)});
+  if (s == FQ_OK) record_launch(a.stream, tq_is_pdl(a), {sp1, sp2, sx}, {sq, ss, sz, sy});
   return s;
 }
 
@@ -155,7 +175,7 @@ static fq_status validate_gemm(const uint8_t* qa, int64_t T, int32_t K, const ui
   return FQ_OK;
 }
 
-static fq_status launch_gemm(GemmArgs& a);
+static fq_status launch_gemm(GemmArgs& a, bool& pdl_kernel);
 
 static fq_status run_gemm(const uint8_t* qa, const float* sa, int64_t T, int32_t K, const uint8_t* qw,
                           const float* sw, int32_t N, void* y, bool y_bf16, bool out_i32, void* stream,
@@ -174,16 +194,22 @@ static fq_status run_gemm(const uint8_t* qa, const float* sa, int64_t T, int32_t
   a.za = za;
   a.colsum = colsum;
   a.stream = static_cast<cudaStream_t>(stream);
-  a.params_early = params_early(a.stream, {span(qw, size_t(N) * size_t(K / 2)), span(sw, sw ? size_t(N) * 4 : 0),
-                                           span(colsum, colsum ? size_t(N) * 4 : 0)});
-  const fq_status s = launch_gemm(a);
-  if (s == FQ_OK) record_outputs(a.stream, {span(y, size_t(T) * size_t(N) * (out_i32 ? 4 : 2))});
+  const Span sqw = span(qw, size_t(N) * size_t(K / 2)), ssw = span(sw, sw ? size_t(N) * 4 : 0),
+             scs = span(colsum, colsum ? size_t(N) * 4 : 0);
+  const Span sqa = span(qa, size_t(T) * size_t(K / 2)), ssa = span(sa, sa ? size_t(T) * 4 : 0),
+             sza = span(za, za ? size_t(T) : 0);
+  const Span sy = span(y, size_t(T) * size_t(N) * (out_i32 ? 4 : 2));
+  a.pdl = pdl_flags(a.stream, {sqw, ssw, scs}, {sqa, ssa, sza}, {sy});
+  bool pdl_kernel = false;
+  const fq_status s = launch_gemm(a, pdl_kernel);
+  if (s == FQ_OK) record_launch(a.stream, pdl_kernel, {sqw, ssw, scs, sqa, ssa, sza}, {sy});
   return s;
 }
 
-static fq_status launch_gemm(GemmArgs& a) {
+static fq_status launch_gemm(GemmArgs& a, bool& pdl_kernel) {
   const int impl = g_gemm_impl.load();
   const bool za = a.za != nullptr;
+  pdl_kernel = true;                               // decode and pair kernels use PDL
   // impl 0: decode kernel for T <= 64, else the pair kernel with the tile width picked per shape;
   // 3 / 4 / 5: pair kernel with the width forced to 192 / 160 / 128; 6: decode kernel forced
   if (impl == 6 || (impl == 0 && gemm_dec_supported(a))) {
@@ -198,6 +224,7 @@ static fq_status launch_gemm(GemmArgs& a) {
   }
   if (pair && gemm_pair_supported(a)) return cuda_status(gemm_pair_launch(a, bn));
   if (impl >= 3) return FQ_ENOTSUP;   // a forced pair width the shape does not support
+  pdl_kernel = false;                              // cross-check kernels: plain launches
   if (impl == 2 && gemm_tc05_supported(a)) return cuda_status(gemm_tc05_launch(a));
   return cuda_status(gemm_mma_launch(a));
 }
@@ -323,7 +350,7 @@ fq_status fq_weight_colsum(const uint8_t* qw, int32_t N, int32_t K, int32_t* col
   if (K % 2 != 0) return FQ_ESHAPE;
   if ((reinterpret_cast<uintptr_t>(colsum) & 3u) != 0) return FQ_ESHAPE;
   const fq_status s = cuda_status(weight_colsum_launch(qw, N, K, colsum, static_cast<cudaStream_t>(stream)));
-  if (s == FQ_OK) record_outputs(static_cast<cudaStream_t>(stream), {span(colsum, size_t(N) * 4)});
+  if (s == FQ_OK) clear_outputs(static_cast<cudaStream_t>(stream));   // plain launch: completes before the next
   return s;
 }
 
@@ -396,9 +423,12 @@ fq_status fq_kv_quant(const void* kv, int32_t kv_dtype, int64_t R, int64_t ldkv,
   a.bf16 = kv_dtype == FQ_BF16;
   a.stream = static_cast<cudaStream_t>(stream);
   if (!kv_quant_supported(a)) return FQ_ESHAPE;
+  const Span sq = span(q, size_t(R) * size_t(head_dim / 2)), ss = span(scale, size_t(R) * 4), sz = span(zero, size_t(R));
+  const Span skv = span(kv, size_t(R - 1) * size_t(ldkv) * 2 + size_t(head_dim) * 2),
+             sp = span(p_h, size_t(head_dim) * head_dim * 2);
+  a.pdl = pdl_flags(a.stream, {sp}, {skv}, {sq, ss, sz});      // (the KV kernel waits before any access)
   const fq_status s = cuda_status(kv_quant_launch(a));
-  if (s == FQ_OK)
-    record_outputs(a.stream, {span(q, size_t(R) * size_t(head_dim / 2)), span(scale, size_t(R) * 4), span(zero, size_t(R))});
+  if (s == FQ_OK) record_launch(a.stream, true, {skv, sp}, {sq, ss, sz});
   return s;
 }
 

@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(THREADS, FQ_DEC_MINB)
 gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA,
                 const float* __restrict__ sa, int T, int TN, int K, const float* __restrict__ sw, int N,
                 void* __restrict__ yv, const int8_t* __restrict__ za, const int32_t* __restrict__ colsum,
-                int S, int params_early) {
+                int S, int pdl) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;                                        // widened stages [W 16 KB | A 8 KB]
@@ -193,7 +193,6 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (threadIdx.x == 0) tc::griddep_launch();   // the next kernel may start launching (PDL)
   if (threadIdx.x == 0) dtrace(tslot, 1);
 
   // activation rows (TN x 4 chunks) -> widened SWIZZLE_128B K-major stage, by 256 threads
@@ -220,14 +219,14 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     if (lane == 0) {
       // the weights are parameters: unless the preceding kernel of the stream writes them
       // (host-side hazard check, fq_abi.cu), start streaming them before the wait
-      if (!params_early) tc::griddep_wait();
+      if (!(pdl & PDL_P)) tc::griddep_wait();
       const int pre = nk < PSTAGES ? nk : PSTAGES;
       for (int j = 0; j < pre; ++j) {
         if (j < 36) dtrace(tslot, 4 + j);
         tc::mbar_expect_tx(&pfull[j], uint32_t(WP_BYTES + ap_bytes));
         tc::tma_load_2d(sP + size_t(j) * P_BYTES, &tmW, &pfull[j], kb_of(j) * (BK / 2), fb * BM);
       }
-      if (params_early) tc::griddep_wait();      // qa written by the transform kernel is visible
+      if (!(pdl & PDL_X)) tc::griddep_wait();    // qa written by the transform kernel is visible
       for (int j = 0; j < pre; ++j)
         tc::tma_load_2d(sP + size_t(j) * P_BYTES + WP_BYTES, &tmA, &pfull[j], kb_of(j) * (BK / 2), 0);
       for (int j = pre; j < nk; ++j) {
@@ -329,6 +328,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     // ======================= TMEM -> shared-memory partial tile =======================
     // while the main loop runs: stage the epilogue's scales in shared memory
     tc::griddep_wait();
+    if (threadIdx.x == EPI_WARP0 * 32) tc::griddep_launch();   // only after the wait (fq_internal.h)
     {
       const int e = threadIdx.x - EPI_WARP0 * 32;          // 0..127
       const int o = fb * BM + e;
@@ -530,7 +530,7 @@ cudaError_t gemm_dec_launch(const GemmArgs& a, int split) {
                  a.K, (long long)a.T, S, fbs * S, dec_max_clusters(reinterpret_cast<const void*>(kern), S));
   cudaError_t e = launch_pdl_policy(kern, dim3(unsigned(fbs * S)), dim3(THREADS), SMEM_BYTES, a.stream, S,
                                     dec_policy(), mw, ma, a.sa, int(a.T), TN, a.K, a.sw, a.N, a.y, a.za, a.colsum, S,
-                                    int(a.params_early));
+                                    a.pdl);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

@@ -48,8 +48,8 @@ FQ_DEVICE void trace(int) {}
 #endif
 
 constexpr int BM = 256, BM_CTA = 128;     // tokens per pair tile / per CTA
-#ifndef FQ_GEMM_STAGES
-#define FQ_GEMM_STAGES 2
+#ifndef FQ_GEMM_MAX_STAGES
+#define FQ_GEMM_MAX_STAGES 4
 #endif
 #ifndef FQ_GEMM_PSTAGES
 #define FQ_GEMM_PSTAGES 4
@@ -59,8 +59,6 @@ constexpr int BM = 256, BM_CTA = 128;     // tokens per pair tile / per CTA
 #endif
 constexpr int BK = 256;                   // int8 K per stage (two 128-byte swizzle atoms)
 constexpr int UK = 32;
-constexpr int STAGES = FQ_GEMM_STAGES;    // MMA stages (TMEM A / widened smem B)
-constexpr int PSTAGES = FQ_GEMM_PSTAGES;  // packed A+B ring (TMA)
 constexpr int AP_BYTES = BM_CTA * BK / 2; // 8 KB packed A per ring stage
 constexpr int EPI_BYTES = 32 * 128;       // per epilogue warp: 32 rows x 64 fp16 columns (SW128)
 constexpr int A_COLS = BK / 4;            // TMEM columns per A stage
@@ -96,8 +94,15 @@ struct Geo {
   static constexpr int B_ATOM = BN_CTA * 128;              // one 128-byte K atom of the widened B stage
   static constexpr int B_TOTAL = BN_CTA * B_CHUNKS;        // B conversion tasks per stage
   static constexpr int B_TASKS = (B_TOTAL + NUM_B_WARPS * 32 - 1) / (NUM_B_WARPS * 32);
+  // MMA stages (TMEM A / widened smem B): as many as the TMEM left beside the accumulators holds
+  // (192: 2, 160: 3, 128 and 256: 4); the packed TMA ring gets the shared memory that is left
+  static constexpr int STAGES_FIT = (TMEM_COLS - NACC * BN) / A_COLS;
+  static constexpr int STAGES = STAGES_FIT < FQ_GEMM_MAX_STAGES ? STAGES_FIT : FQ_GEMM_MAX_STAGES;
+  static constexpr int SMEM_AVAIL = 232448 - 1024 - 512 - NUM_EPI_WARPS * EPI_BYTES - STAGES * B_BYTES;
+  static constexpr int PSTAGES = SMEM_AVAIL / P_BYTES < FQ_GEMM_PSTAGES ? SMEM_AVAIL / P_BYTES : FQ_GEMM_PSTAGES;
   static constexpr size_t SMEM_BYTES =
       size_t(STAGES) * B_BYTES + size_t(PSTAGES) * P_BYTES + NUM_EPI_WARPS * EPI_BYTES + 1024 + 512;
+  static_assert(STAGES >= 2 && PSTAGES >= 2, "pipeline depth");
   static constexpr uint32_t IDESC = tc::idesc_i8(BM, BN);
   static_assert(TMEM_A0 + STAGES * A_COLS <= TMEM_COLS, "TMEM budget");
   static_assert(B_ATOM % 1024 == 0 && P_BYTES % 1024 == 0, "SWIZZLE_128B atoms stay 1024-B aligned");
@@ -154,6 +159,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   using GE = Geo<BN>;
   constexpr int BN_CTA = GE::BN_CTA, B_BYTES = GE::B_BYTES, P_BYTES = GE::P_BYTES, TMEM_A0 = GE::TMEM_A0;
   constexpr int B_ATOM = GE::B_ATOM, B_TASKS = GE::B_TASKS;
+  constexpr int STAGES = GE::STAGES, PSTAGES = GE::PSTAGES;
   constexpr uint32_t IDESC = GE::IDESC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -210,8 +216,8 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   tc::cluster_sync();            // peer barriers initialised before any remote arrive
   tc::fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (threadIdx.x == 0) tc::griddep_launch();   // the next kernel may start launching (PDL)
   tc::griddep_wait();                            // qa / sa written by the previous kernel are visible
+  if (threadIdx.x == 0) tc::griddep_launch();   // dependents launch only after the wait (fq_internal.h)
 
   // Every converter warp signals the leader's `full` barrier on its own (CTA-scope arrive in the
   // leader, release.cluster remote arrive from the peer), so the A and B paths and the warps of
@@ -270,6 +276,13 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         tc::mbar_wait(&pfull[sp], (jb / PSTAGES) & 1);
         const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES) + roff;
         uint32_t w[8 * A_CH];
+#ifdef FQ_EXP_SKIP_A      // experiment build only: A conversion removed (garbage A) to bound the rest
+        if (true) {
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&pempty[sp]);
+          return;
+        }
+#endif
 #pragma unroll
         for (int c = 0; c < A_CH; ++c) {
           const uint4 pk = tc::lds128(src + ((uint32_t(A_CH * kpart + c) ^ sw) << 4));
@@ -323,6 +336,19 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES + AP_BYTES);
         const uint32_t dst = smem_u32(smem + size_t(stage) * B_BYTES);
         uint32_t o[B_TASKS][8];
+#ifdef FQ_EXP_SKIP_B      // experiment build only: B conversion removed (garbage B)
+#pragma unroll
+        for (int i = 0; i < B_TASKS; ++i) o[i][0] = 0;
+        if (true) {
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&pempty[sp]);
+          signal_full(&full[stage]);
+          ++job;
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          cv.next(sc);
+          continue;
+        }
+#endif
 #pragma unroll
         for (int i = 0; i < B_TASKS; ++i) {
           const int task = ct + i * NUM_B_WARPS * 32;

@@ -15,6 +15,16 @@ enum TmapSwizzle { TMAP_SW_NONE = 0, TMAP_SW64 = 64, TMAP_SW128 = 128 };
 bool tmap_encode(CUtensorMap* m, const void* base, int elem_bytes, int rank, const uint64_t* dims,
                  const uint64_t* strides_bytes, const uint32_t* box, TmapSwizzle swizzle);
 
+// Programmatic dependent launch protocol of every PDL kernel in this library:
+//   * a kernel signals its dependents (griddepcontrol.launch_dependents) only AFTER its own
+//     griddepcontrol.wait has returned, so while a kernel runs before its wait, the only kernel
+//     that can still be running is its immediate predecessor on the stream;
+//   * before its wait a kernel may read parameters (PDL_P), read activations (PDL_X) and write
+//     its outputs (PDL_OUT) only when the host found that the predecessor -- the last kernel
+//     this library enqueued on the stream -- neither writes those inputs nor touches those
+//     outputs (fq_abi.cu).  Anything else runs after the wait.
+constexpr int PDL_P = 1, PDL_X = 2, PDL_OUT = 4;
+
 struct TQArgs {
   const void* x;
   int64_t T, ldx;
@@ -27,7 +37,7 @@ struct TQArgs {
   float* y;         // optional fp32 export of the transformed activations (debug / parity)
   int8_t* zero;     // FQ_ASYM: per-token zero point - 8 (output); nullptr for FQ_SYM
   bool bf16;
-  bool params_early;  // PDL: p1 / p2 may be read before griddepcontrol.wait (fq_abi.cu hazard check)
+  int pdl;            // PDL_* flags (fq_abi.cu hazard check): what may happen before griddepcontrol.wait
   cudaStream_t stream;
 };
 
@@ -44,7 +54,7 @@ struct GemmArgs {
   const int32_t* colsum;    // asymmetric activations: sum_k qw[o,k] per output channel
   bool y_bf16;
   bool out_i32;
-  bool params_early;  // PDL: qw / sw / colsum may be read before griddepcontrol.wait (fq_abi.cu)
+  int pdl;            // PDL_* flags (fq_abi.cu hazard check)
   cudaStream_t stream;
 };
 
@@ -58,6 +68,7 @@ struct KVArgs {     // KV-cache quantization (fq_kv_quant)
   float* scale;     // [R]
   int8_t* zero;     // [R] z - 8
   bool bf16;
+  int pdl;          // PDL_* flags (the KV kernel waits before any access regardless)
   cudaStream_t stream;
 };
 
@@ -129,6 +140,7 @@ cudaError_t launch_pdl_policy(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 
 cudaError_t transform_quant_launch(const TQArgs& a);   // impl selection (fq_set_tq_impl)
 bool tq_kernel_available(const TQArgs& a);             // some kernel serves this call
+bool tq_is_pdl(const TQArgs& a);                       // the kernel it picks uses PDL (tcgen05 kernels)
 bool tq_simt_supported(int n1, int n2);
 bool tq_mma_supported(int n1, int n2);                 // legacy mma.sync kernel instantiations
 cudaError_t tq_mma_launch(const TQArgs& a);

@@ -99,8 +99,8 @@ kv_quant_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
       tc::mbar_init(&dempty[b], 4);
     }
     tc::fence_barrier_init();
-    tc::griddep_launch();
     tc::griddep_wait();
+    tc::griddep_launch();              // dependents launch only after the wait (fq_internal.h)
     tc::mbar_expect_tx(pfull, C::P_BYTES);
 #pragma unroll
     for (int a = 0; a < C::KA; ++a) tc::tma_load_2d(sP + a * D * 128, &tmP, pfull, a * 64, 0);

@@ -175,8 +175,7 @@ template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM, bool SMALL = false
 __global__ void __launch_bounds__(Cfg<N1, N2, SMALL>::THREADS, 1)
 tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmP1,
                const __grid_constant__ CUtensorMap tmP2, int64_t T, float alpha, uint8_t* __restrict__ q,
-               float* __restrict__ scale, float* __restrict__ y_out, int8_t* __restrict__ zero,
-               int params_early) {
+               float* __restrict__ scale, float* __restrict__ y_out, int8_t* __restrict__ zero, int pdl) {
   using C = Cfg<N1, N2, SMALL>;
   constexpr int S = C::STAGES, TOK = C::TOK, G = C::GROUPS, THREADS = C::THREADS;
   constexpr uint32_t IDESC1 = tc::idesc_f16(128, N1, BF16 ? 1 : 0, 1, 1);
@@ -233,23 +232,28 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
       tc::mbar_init(&d2full[b], 1);
     }
     tc::fence_barrier_init();
-    tc::griddep_launch();              // the next kernel may start launching (PDL)
-    // P1, P2 are parameters: unless the preceding kernel of the stream writes them (host-side
-    // hazard check, fq_abi.cu), they stream in while that kernel finishes; X is its output
+    // PDL (fq_internal.h): P1, P2 and X stream in while the preceding kernel finishes unless it
+    // writes them (host-side hazard check, fq_abi.cu)
     auto load_p = [&] {
       tc::mbar_expect_tx(pfull, C::P1_BYTES + C::P2_BYTES);
       for (int a = 0; a < C::P1_ATOMS; ++a) tc::tma_load_2d(sP1 + a * N1 * 128, &tmP1, pfull, a * 64, 0);
       for (int b = 0; b < C::JB; ++b) tc::tma_load_2d(sP2 + b * N2 * 128, &tmP2, pfull, b * 64, 0);
     };
-    if (params_early) load_p();
+    if (pdl & PDL_P) load_p();
     trace(3);
-    tc::griddep_wait();                // inputs of this kernel are final (PDL)
-    if (!params_early) load_p();
+    if ((pdl & (PDL_P | PDL_X)) != (PDL_P | PDL_X)) tc::griddep_wait();
+    if (!(pdl & PDL_P)) load_p();
     trace(4);
     for (int k = 0; k < prefill; ++k) issue_x(k);
     trace(1);
   }
-  if (warp == 2) tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == 2) {
+    tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
+    if (lane == 0) {
+      tc::griddep_wait();              // dependents launch only after this kernel's wait returned
+      tc::griddep_launch();
+    }
+  }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -342,6 +346,7 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     };
     constexpr int QROW = N2 / 2;                         // packed bytes per row i of a token
     constexpr int QTOK = N1 * N2 / 2;                    // packed bytes per token
+    bool waited = (pdl & PDL_OUT) != 0;                  // outputs written before the wait only if allowed
     for (int k = grp; k < my_tiles; k += G) {
       const int par = grp;                               // == k % G
       const uint32_t ph = (k / G) & 1;
@@ -461,6 +466,10 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
         B15 = 8.0f / 15.0f;
       }
       uint8_t* qrow = q + (store ? t * QTOK + i * QROW : 0);
+      if (!waited) {
+        tc::griddep_wait();
+        waited = true;
+      }
       tmem_chunks<N2>(d2, [&](const uint32_t* v, int, int col) {   // N2 % 32 == 0: full chunks
         uint32_t w[4];
 #pragma unroll
@@ -546,7 +555,7 @@ static cudaError_t launch(const TQArgs& a) {
   const int64_t tiles = (a.T + C::TOK - 1) / C::TOK;
   const int grid = int(std::min<int64_t>(tiles, num_sms()));
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(C::THREADS), C::SMEM, a.stream, 1, mx, m1, m2, a.T, a.alpha,
-                             a.q, a.scale, a.y, a.zero, int(a.params_early));
+                             a.q, a.scale, a.y, a.zero, a.pdl);
   count_launch();
   return e;
 }

@@ -98,8 +98,7 @@ template <int N2, bool BF16, bool WRITE_Y, bool ASYM>
 __global__ void __launch_bounds__(THREADS, 1)
 tq_wide_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmP1,
                const __grid_constant__ CUtensorMap tmP2, int64_t T, float alpha, uint8_t* __restrict__ q,
-               float* __restrict__ scale, float* __restrict__ y_out, int8_t* __restrict__ zero,
-               int params_early) {
+               float* __restrict__ scale, float* __restrict__ y_out, int8_t* __restrict__ zero, int pdl) {
   using C = Cfg<N2>;
   constexpr int S = C::STAGES;
   constexpr uint32_t IDESC1 = tc::idesc_f16(128, N2, BF16 ? 1 : 0, 1, 1);
@@ -147,18 +146,23 @@ tq_wide_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     tc::mbar_init(d2full, 1);
     tc::mbar_init(d2empty, 4);
     tc::fence_barrier_init();
-    tc::griddep_launch();              // the next kernel may start launching (PDL)
-    auto load_p = [&] {                // parameters: before the wait unless the preceding kernel writes them
+    auto load_p = [&] {                // PDL (fq_internal.h): before the wait unless the predecessor writes them
       tc::mbar_expect_tx(pfull, C::P1_BYTES + C::P2_BYTES);
       for (int a = 0; a < 2; ++a) tc::tma_load_2d(sP1 + a * N1 * 128, &tmP1, pfull, a * 64, 0);
       for (int b = 0; b < C::JB; ++b) tc::tma_load_2d(sP2 + b * N2 * 128, &tmP2, pfull, b * 64, 0);
     };
-    if (params_early) load_p();
-    tc::griddep_wait();                // X of the preceding kernel is final (PDL)
-    if (!params_early) load_p();
+    if (pdl & PDL_P) load_p();
+    if ((pdl & (PDL_P | PDL_X)) != (PDL_P | PDL_X)) tc::griddep_wait();
+    if (!(pdl & PDL_P)) load_p();
     for (int k = 0; k < prefill; ++k) issue_x(k);
   }
-  if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
+  if (warp == 2) {
+    tc::tmem_alloc(tmem_slot, 512);
+    if (lane == 0) {
+      tc::griddep_wait();              // dependents launch only after this kernel's wait returned
+      tc::griddep_launch();
+    }
+  }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -222,6 +226,7 @@ tq_wide_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
       return r;
     };
     constexpr int QROW = N2 / 2, QTOK = N1 * N2 / 2;
+    bool waited = (pdl & PDL_OUT) != 0;                  // outputs before the wait only if allowed
     for (int k = 0; k < my_tiles; ++k) {
       const int64_t t = int64_t(blockIdx.x) + int64_t(k) * gridDim.x;
       const uint32_t ph = k & 1;
@@ -295,6 +300,10 @@ tq_wide_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
         B15 = 8.0f / 15.0f;
       }
       uint8_t* qrow = q + t * QTOK + i * QROW;
+      if (!waited) {
+        tc::griddep_wait();
+        waited = true;
+      }
 #pragma unroll 1
       for (int c = 0; c < N2; c += 32) {
         uint32_t v[32];
@@ -366,7 +375,7 @@ static cudaError_t launch(const TQArgs& a) {
   }
   const int grid = int(std::min<int64_t>(a.T, num_sms()));
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(THREADS), C::SMEM, a.stream, 1, mx, m1, m2, a.T, a.alpha, a.q,
-                             a.scale, a.y, a.zero, int(a.params_early));
+                             a.scale, a.y, a.zero, a.pdl);
   count_launch();
   return e;
 }

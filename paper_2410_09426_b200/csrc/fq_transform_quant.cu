@@ -449,6 +449,10 @@ bool tq_kernel_available(const TQArgs& a) {
   return tq_simt_supported(a.n1, a.n2);
 }
 
+bool tq_is_pdl(const TQArgs& a) {
+  return a.p2 != nullptr && tq_impl() == 0 && (tq_tc05_supported(a) || tq_wide_supported(a));
+}
+
 cudaError_t transform_quant_launch(const TQArgs& a) {
   const int impl = tq_impl();
   if (a.p2 == nullptr) return tq_ident2_launch(a);     // P2 = I (validated by the ABI layer)

@@ -175,3 +175,51 @@ def test_binding_rejects_layouts_the_abi_cannot_express():
         fq.w4a4_gemm_i32(qa, torch.zeros((K // 2, N), dtype=torch.uint8, device=DEV).t())
     with pytest.raises(ValueError):                  # scale buffer of the wrong length
         fq.fq_transform_quant(big[:, :K], n1, n2, p, p, 0.9, qa, sa[:4])
+
+
+def test_pdl_chains_and_shared_workspace_match_synchronised_runs():
+    """The PDL protocol (a kernel lets dependents launch only after its own wait; inputs/outputs
+    checked against the predecessor): (i) a chain GEMM -> independent transform -> transform
+    whose P1 is the GEMM's output; (ii) one workspace reused by two linears (write-after-read:
+    the second transform overwrites codes the first GEMM reads); (iii) independent linears
+    back to back (transforms that start before the previous GEMM finishes).  Every result equals
+    the same calls with a device synchronisation after each one."""
+    n1 = n2 = 64
+    K = n1 * n2
+    e = torch.eye(64, dtype=torch.float16, device=DEV)
+    qa0, sa0 = fq.transform_quant(torch.from_numpy(synth.activations(64, K, seed=20)).to(DEV), n1, n2, e, e, 0.9)
+    qwp, swp = fq.transform_quant(torch.from_numpy(synth.weights(64, K, seed=21)).to(DEV), n1, n2, e, e, 1.0)
+    xs = [torch.from_numpy(synth.activations(1500, K, seed=22 + i)).to(DEV) for i in range(3)]
+    ws = [fq.transform_quant(torch.from_numpy(synth.weights(3072, K, seed=30 + i)).to(DEV), n1, n2, e, e, 1.0)
+          for i in range(3)]
+    torch.cuda.synchronize()
+
+    def run(sync):
+        def s():
+            if sync:
+                torch.cuda.synchronize()
+        out = {}
+        p1 = torch.zeros((64, 64), dtype=torch.float16, device=DEV)
+        fq.fq_w4a4_linear(qa0, sa0, qwp, swp, p1); s()                        # (i) GEMM writes P1
+        out["b"] = fq.transform_quant(xs[0], n1, n2, e, e, 0.9); s()          # independent transform
+        out["c"] = fq.transform_quant(xs[1], n1, n2, p1, e, 0.9); s()         # reads the GEMM's output
+        q_ws = torch.empty((1500, K // 2), dtype=torch.uint8, device=DEV)     # (ii) shared workspace
+        s_ws = torch.empty((1500,), dtype=torch.float32, device=DEV)
+        ys = []
+        for i in range(2):
+            fq.fq_transform_quant(xs[i], n1, n2, e, e, 0.9, q_ws, s_ws); s()
+            ys.append(fq.w4a4_linear(q_ws, s_ws, *ws[i])); s()
+        out["ws"] = ys
+        outs = []                                                              # (iii) independent linears
+        for i in range(3):
+            q, sc = fq.transform_quant(xs[i], n1, n2, e, e, 0.9); s()
+            outs.append(fq.w4a4_linear(q, sc, *ws[i])); s()
+        out["ind"] = outs
+        torch.cuda.synchronize()
+        return out
+
+    ref, got = run(True), run(False)
+    for k in ("b", "c"):
+        assert all(torch.equal(a, b) for a, b in zip(ref[k], got[k])), k
+    for a, b in zip(ref["ws"] + ref["ind"], got["ws"] + got["ind"]):
+        assert torch.equal(a, b)
