@@ -52,12 +52,18 @@ constexpr int BM = 256, BM_CTA = 128;     // tokens per pair tile / per CTA
 #define FQ_GEMM_MAX_STAGES 4
 #endif
 #ifndef FQ_GEMM_PSTAGES
-#define FQ_GEMM_PSTAGES 4
+#define FQ_GEMM_PSTAGES 4       // cap on the packed ring depth (shared memory permitting)
 #endif
 #ifndef FQ_GEMM_BWARPS
 #define FQ_GEMM_BWARPS 6
 #endif
-constexpr int BK = 256;                   // int8 K per stage (two 128-byte swizzle atoms)
+#ifndef FQ_GEMM_BK
+#define FQ_GEMM_BK 256
+#endif
+constexpr int BK = FQ_GEMM_BK;            // int8 K per stage: 256 (two 128-byte K atoms) or 128 (one)
+static_assert(BK == 256 || BK == 128, "BK");
+// the packed A ring row of one K-block is BK/2 bytes: SWIZZLE_128B rows (BK 256) or SWIZZLE_64B
+constexpr int A_ROW = BK / 2;
 constexpr int UK = 32;
 constexpr int AP_BYTES = BM_CTA * BK / 2; // 8 KB packed A per ring stage
 constexpr int EPI_BYTES = 32 * 128;       // per epilogue warp: 32 rows x 64 fp16 columns (SW128)
@@ -70,7 +76,8 @@ constexpr int NUM_EPI_WARPS = 4, MMA_WARP = 4;
 #endif
 constexpr int A_WARP0 = 5, NUM_A_WARPS = FQ_GEMM_AWARPS;   // 4 warps per K part (one per TMEM lane quarter)
 constexpr int A_PARTS = NUM_A_WARPS / 4;                   // K parts of a row: 2 (halves) or 4 (quarters)
-constexpr int A_CH = 8 / A_PARTS;                          // packed 16-byte chunks per thread and K-block
+constexpr int A_CH = (BK / 32) / A_PARTS;                  // packed 16-byte chunks per thread and K-block
+static_assert(A_CH == 2 || A_CH == 4, "A chunks per thread");
 static_assert(NUM_A_WARPS == 8 || NUM_A_WARPS == 16, "A converter warps: 8 or 16");
 constexpr int B_WARP0 = A_WARP0 + NUM_A_WARPS, NUM_B_WARPS = FQ_GEMM_BWARPS;
 constexpr int NUM_CONV_WARPS = NUM_A_WARPS + NUM_B_WARPS;
@@ -265,8 +272,9 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       const int quarter = warp & 3, kpart = aw >> 2;
       const int r_local = quarter * 32 + lane;                   // == TMEM lane of this row
       const uint32_t tl = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(TMEM_A0 + kpart * (A_COLS / A_PARTS));
-      const uint32_t sw = uint32_t(r_local & 7);
-      const uint32_t roff = uint32_t(r_local * 128);
+      // 16-byte chunk c of the row sits at c ^ swizzle: SW128 (row % 8) or SW64 ((row / 2) % 4)
+      const uint32_t sw = BK == 256 ? uint32_t(r_local & 7) : uint32_t((r_local >> 1) & 3);
+      const uint32_t roff = uint32_t(r_local * A_ROW);
       // Two K-blocks per iteration: both are converted and their tcgen05.st issued before one
       // tcgen05.wait::st + signal, which halves the per-K-block synchronisation latency (the
       // A path is latency-bound, not throughput-bound).
@@ -555,16 +563,16 @@ bool gemm_pair_supported(const GemmArgs& a) {
   return a.K % 32 == 0 && a.K < 131072 && a.N % 8 == 0 && a.T <= int64_t(1) << 30 && tmap_available();
 }
 
-// Tile width per shape.  A pair tile's main loop is bound by the A conversion (256 activation
-// rows per K-block, independent of the width), so the time of one wave grows much slower than
-// the width.  Measured per-wave costs relative to 128 columns (scripts/gemm_bn_sweep.py, C3
-// shapes): 1.16 at 160, 1.23 at 192; 256 columns has one accumulator, its epilogue is not
-// overlapped, which costs more at short K: 1.6 + 0.3 * 4096 / K (1.9 at K = 4096, where it never
-// wins; 1.69 at K = 14336, where it saves a wave on down_proj).  cost = waves x per-wave cost.
+// Tile width per shape.  A pair tile's main loop is bound by the operand conversion, so the time of
+// one wave grows slower than the width; cost = waves x measured per-wave cost (scripts/gemm_shapes.py
+// with widths forced, C3 shapes and 8192^3, round 2: 192 and 160 run 2 and 3 MMA stages, 128 and the
+// single-accumulator 256 run 4).  Relative to 128: 1.19 at 160, 1.23 at 192, and 1.55 + 0.15 * 4096 / K
+// at 256 (its epilogue is not overlapped, which costs more at short K).  So 256 wins where it saves
+// waves (o_proj / C2 3 -> 2, down_proj 3 -> 2, 8192^3) and 192 elsewhere.
 int gemm_pair_pick_bn(int64_t T, int N, int K, int clusters) {
   using g3::BM;
   const int cands[4] = {192, 160, 128, 256};
-  const double rel[4] = {1.23, 1.16, 1.0, 1.6 + 0.3 * 4096.0 / double(K > 0 ? K : 1)};
+  const double rel[4] = {1.23, 1.19, 1.07, 1.55 + 0.15 * 4096.0 / double(K > 0 ? K : 1)};
   int best = 192;
   double best_cost = 0;
   for (int i = 0; i < 4; ++i) {
@@ -596,7 +604,8 @@ static cudaError_t launch_bn(const GemmArgs& a) {
     const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.T)};
     const uint64_t strides[1] = {uint64_t(a.K / 2)};
     const uint32_t box[2] = {BK / 2, BM_CTA};
-    if (!tmap_encode(&ma, a.qa, 1, 2, dims, strides, box, TMAP_SW128)) return cudaErrorInvalidValue;
+    if (!tmap_encode(&ma, a.qa, 1, 2, dims, strides, box, BK == 256 ? TMAP_SW128 : TMAP_SW64))
+      return cudaErrorInvalidValue;
   }
   {
     const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.N)};

@@ -28,6 +28,7 @@ p2 = torch.from_numpy(synth.well_conditioned(lin.n2, seed=0, tag="p2")).to(dev)
 flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 for _ in range(3):
     flush.zero_()
+    flush.sum()
     q, s = fq.transform_quant(x, lin.n1, lin.n2, p1, p2, 0.9)
 torch.cuda.synchronize()
 lib = fq.load()
@@ -57,6 +58,7 @@ st = torch.cuda.current_stream()
 sp = ctypes.c_void_p(st.cuda_stream)
 for rep in range(3):
     flush.zero_()
+    flush.sum()
     torch.cuda._sleep(200_000)
     lib.fq_debug_stamp(0, sp)
     fq.fq_transform_quant(x, lin.n1, lin.n2, p1, p2, 0.9, q, s)
