@@ -87,8 +87,9 @@ typedef enum { FQ_SYM = 0, FQ_ASYM = 1 } fq_qmode;
  *   p1     [n1, n1] row-major, x_dtype.     p2 [n2, n2] row-major, x_dtype, or NULL for
  *          P2 = I_{n2}: the paper's online o_proj transform P_o (a x a) applied across the a
  *          heads of the attention output, identity inside each head of d_head = n2
- *          (PAPER.md:297 P_v fused, PAPER.md:726 a^2 parameters); stage 2 is skipped.  Shapes
- *          (n1, n2) in {(32, 128), (64, 128)} and FQ_SYM only; FQ_ENOTSUP otherwise.
+ *          (PAPER.md:297 P_v fused, PAPER.md:726 a^2 parameters); stage 2 is skipped and the
+ *          fp32 result of P1^T V is quantized directly (tcgen05 kernel; FQ_SYM and FQ_ASYM).
+ *          Shapes (n1, n2) in {(32, 128), (64, 128)}; FQ_ENOTSUP otherwise.
  *   alpha  post-sigmoid clipping ratio in (0, 1]; 1 = no clipping.
  *   qmode  FQ_SYM or FQ_ASYM.
  *   q      [T, n/2] uint8 packed codes (output).     scale [T] fp32 (output), s_t.
@@ -253,7 +254,8 @@ fq_status fq_set_gemm_impl(int32_t impl);
  * n1 in {80,96,112,128}; the wide tcgen05 kernel for n1 = 128, n2 in {160,192,224,256}; the
  * CUDA-core kernel for n1 n2 <= 1024; otherwise the legacy mma.sync kernel where instantiated,
  * else the CUDA-core kernel), 1 = legacy mma.sync kernel (else CUDA cores), 2 = CUDA-core
- * kernel.  p2 = NULL (P2 = I) always runs its mma.sync variant.  Returns FQ_EINVAL otherwise.
+ * kernel.  p2 = NULL (P2 = I) runs the tcgen05 kernel's stage-1-only variant (impl 0) or the
+ * mma.sync one (impl 1, symmetric only).  Returns FQ_EINVAL otherwise.
  * All implementations compute the same function. */
 fq_status fq_set_tq_impl(int32_t impl);
 

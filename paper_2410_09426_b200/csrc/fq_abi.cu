@@ -116,7 +116,7 @@ static fq_status validate_tq(const void* x, int32_t x_dtype, int64_t T, int64_t 
   if (!(alpha > 0.0f && alpha <= 1.0f)) return FQ_EINVAL;   // also rejects NaN
   if (T == 0) return FQ_OK;
   if (!x || !p1 || !q || !scale) return FQ_EINVAL;        // p2 == NULL: P2 = I (fq_transform_quant)
-  if (!p2 && !tq_ident2_supported(n1, n2)) return FQ_ENOTSUP;
+  if (!p2 && !tq_ident2_supported(n1, n2)) return FQ_ENOTSUP;   // P2 = I: (32, 128), (64, 128)
   const int64_t n = int64_t(n1) * n2;
   if (n % 2 != 0) return FQ_ESHAPE;
   if (ldx < n) return FQ_ESHAPE;
@@ -240,7 +240,7 @@ fq_status fq_transform_quant(const void* x, int32_t x_dtype, int64_t T, int64_t 
                              float* scale, int8_t* zero, void* stream) {
   if (qmode != FQ_SYM && qmode != FQ_ASYM) return FQ_EINVAL;
   if ((qmode == FQ_SYM) != (zero == nullptr)) return FQ_EINVAL;   // zero iff asymmetric
-  if (!p2 && qmode == FQ_ASYM) return FQ_ENOTSUP;                  // P2 = I: symmetric only
+
   fq_status s = validate_tq(x, x_dtype, T, ldx, n1, n2, p1, p2, alpha, q, scale);
   if (s != FQ_OK || T == 0) return s;
   return run_tq(x, x_dtype, T, ldx, n1, n2, p1, p2, alpha, q, scale, nullptr, zero, stream);

@@ -73,7 +73,11 @@ constexpr int SMEM_OVERHEAD = 1024 + 512;  // 1024-B alignment slack + barriers/
 // SMALL (decode-size launches, T <= 64): one epilogue group and two X stages, so a 64 x 64 CTA
 // needs ~66 KB of shared memory and 128 TMEM columns and can become resident beside a decode-GEMM CTA
 // of the preceding kernel (PDL): its setup and parameter loads then overlap that kernel's tail.
-template <int N1, int N2, bool SMALL = false>
+// IDENT2: P2 = I (the paper's online o_proj transform P_o (a x a) (x) I_{d_head}, PAPER.md:297, 726;
+// DESIGN.md reading R22): stage 1 only, its fp32 result quantized directly (no fp16 intermediate,
+// no D2 in TMEM); the A2 buffer is the staging area that turns TMEM's column-per-lane layout into
+// row-major packed codes.
+template <int N1, int N2, bool SMALL = false, bool IDENT2 = false>
 struct Cfg {
   static_assert(N2 == 64 || N2 == 128, "n2 in {64, 128}");
   static_assert(N1 % 16 == 0 && N1 >= 16 && N1 <= 128, "n1 multiple of 16, <= 128");
@@ -88,12 +92,13 @@ struct Cfg {
   static constexpr int A2_BYTES = 2 * N2 * 128;        // 2 M-atoms x N2 K-rows x 128 B
   static constexpr int D1C = G1 * N1;                  // TMEM columns of one stage-1 result
   // epilogue groups = tiles in flight (each owns a D1, D2 and A2 slot), as many as TMEM allows
-  static constexpr int GROUPS_FIT = (512 / (D1C + N2)) > MAX_GROUPS ? MAX_GROUPS : (512 / (D1C + N2));
+  static constexpr int D2C = IDENT2 ? 0 : N2;         // TMEM columns of one stage-2 result
+  static constexpr int GROUPS_FIT = (512 / (D1C + D2C)) > MAX_GROUPS ? MAX_GROUPS : (512 / (D1C + D2C));
   static constexpr int GROUPS = SMALL ? 1 : GROUPS_FIT;
   static constexpr int THREADS = (4 + 4 * GROUPS) * 32;
-  static constexpr int TMEM_USED = GROUPS * (D1C + N2);
+  static constexpr int TMEM_USED = GROUPS * (D1C + D2C);
   static constexpr int TMEM_COLS = TMEM_USED <= 128 ? 128 : (TMEM_USED <= 256 ? 256 : 512);
-  static constexpr int FIXED = P1_BYTES + P2_BYTES + GROUPS * A2_BYTES;
+  static constexpr int FIXED = P1_BYTES + (IDENT2 ? 0 : P2_BYTES) + GROUPS * A2_BYTES;
   static constexpr int STAGES_FIT = (SMEM_LIMIT - SMEM_OVERHEAD - FIXED) / X_BYTES;
   static constexpr int STAGES = SMALL ? 2 : (STAGES_FIT > 8 ? 8 : STAGES_FIT);
   static constexpr size_t SMEM = size_t(FIXED) + size_t(STAGES) * X_BYTES + SMEM_OVERHEAD;
@@ -171,12 +176,12 @@ FQ_DEVICE uint32_t pack8(const float (&v)[8]) {
   return (e & 0x0F0F0F0Fu) | ((o << 4) & 0xF0F0F0F0u);
 }
 
-template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM, bool SMALL = false>
-__global__ void __launch_bounds__(Cfg<N1, N2, SMALL>::THREADS, 1)
+template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM, bool SMALL = false, bool IDENT2 = false>
+__global__ void __launch_bounds__(Cfg<N1, N2, SMALL, IDENT2>::THREADS, 1)
 tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmP1,
                const __grid_constant__ CUtensorMap tmP2, int64_t T, float alpha, uint8_t* __restrict__ q,
                float* __restrict__ scale, float* __restrict__ y_out, int8_t* __restrict__ zero, int pdl) {
-  using C = Cfg<N1, N2, SMALL>;
+  using C = Cfg<N1, N2, SMALL, IDENT2>;
   constexpr int S = C::STAGES, TOK = C::TOK, G = C::GROUPS, THREADS = C::THREADS;
   constexpr uint32_t IDESC1 = tc::idesc_f16(128, N1, BF16 ? 1 : 0, 1, 1);
   constexpr uint32_t IDESC2 = tc::idesc_f16(128, N2, 0, 1, 1);
@@ -185,7 +190,7 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sP1 = smem;
   uint8_t* sP2 = sP1 + C::P1_BYTES;
-  uint8_t* sA2 = sP2 + C::P2_BYTES;
+  uint8_t* sA2 = sP2 + (IDENT2 ? 0 : C::P2_BYTES);
   uint8_t* sX = sA2 + G * C::A2_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sX + size_t(S) * C::X_BYTES);
   uint64_t* xfull = bars;            // [S]  TMA -> MMA
@@ -220,7 +225,7 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
   if (threadIdx.x == 0) {
     tc::tma_prefetch_desc(&tmX);
     tc::tma_prefetch_desc(&tmP1);
-    tc::tma_prefetch_desc(&tmP2);
+    if constexpr (!IDENT2) tc::tma_prefetch_desc(&tmP2);
     for (int s = 0; s < S; ++s) {
       tc::mbar_init(&xfull[s], 1);
       tc::mbar_init(&xempty[s], 1);
@@ -235,9 +240,10 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     // PDL (fq_internal.h): P1, P2 and X stream in while the preceding kernel finishes unless it
     // writes them (host-side hazard check, fq_abi.cu)
     auto load_p = [&] {
-      tc::mbar_expect_tx(pfull, C::P1_BYTES + C::P2_BYTES);
+      tc::mbar_expect_tx(pfull, C::P1_BYTES + (IDENT2 ? 0 : C::P2_BYTES));
       for (int a = 0; a < C::P1_ATOMS; ++a) tc::tma_load_2d(sP1 + a * N1 * 128, &tmP1, pfull, a * 64, 0);
-      for (int b = 0; b < C::JB; ++b) tc::tma_load_2d(sP2 + b * N2 * 128, &tmP2, pfull, b * 64, 0);
+      if constexpr (!IDENT2)
+        for (int b = 0; b < C::JB; ++b) tc::tma_load_2d(sP2 + b * N2 * 128, &tmP2, pfull, b * 64, 0);
     };
     if (pdl & PDL_P) load_p();
     trace(3);
@@ -264,7 +270,7 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
   // stage 2 runs in fp16 (R9): a bf16 P2 becomes fp16 P2 * 2^e2 in place (power-of-two scaled
   // into fp16 range, so no entry overflows); 2^-e2 is applied to the statistics below, exactly
   float inv_p2 = 1.0f;
-  if constexpr (BF16) {
+  if constexpr (BF16 && !IDENT2) {
     __shared__ uint32_t p2max;
     inv_p2 = exp2i(-bf16_to_f16_pow2(sP2, C::P2_BYTES / 2, &p2max));
   } else {
@@ -321,7 +327,7 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
           if (k >= G) tc::mbar_wait(&a2full[k % G], ((k - G) / G) & 1);
           mma1(k);
         }
-      } else {
+      } else if constexpr (!IDENT2) {
         for (int k = 0; k < my_tiles; ++k) mma2(k);
         trace(122);
       }
@@ -351,6 +357,116 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
       const int par = grp;                               // == k % G
       const uint32_t ph = (k / G) & 1;
       const int64_t t0 = int64_t(int(blockIdx.x) + k * int(gridDim.x)) * TOK;
+      if constexpr (IDENT2) {
+        // ---- P2 = I: D1 lane j, column i holds Y_t[i][j] (fp32, the whole token in 128 lanes) ----
+        tc::mbar_wait(&d1full[par], ph);
+        tc::fence_after();
+        uint8_t* stg = sA2 + par * C::A2_BYTES;          // [N1][N2/2] packed bytes of one token
+#pragma unroll 1
+        for (int g = 0; g < C::G1; ++g) {
+          const uint32_t d1 = lane_base + uint32_t(par * C::D1C + g * N1);
+          const int64_t t = t0 + g;
+          float m1 = 0.f, hi1 = 0.f, lo1 = 0.f;
+          tmem_chunks<N1>(d1, [&](const uint32_t* v, int n, int) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              if (e < n) {
+                const float a0 = __uint_as_float(v[e]), a1 = __uint_as_float(v[e + 1]);
+                if constexpr (ASYM) {
+                  hi1 = max3f(hi1, a0, a1);
+                  lo1 = max3f(lo1, -a0, -a1);
+                } else {
+                  m1 = max3f(m1, fabsf(a0), fabsf(a1));
+                }
+              }
+            }
+          });
+          auto tok_max = [](float4 r) { return fmaxf(fmaxf(r.x, r.y), fmaxf(r.z, r.w)); };
+          float mp, lop = 0.f;
+          if constexpr (ASYM) {
+            const float hip = tok_max(exchange(hi1));
+            lop = tok_max(exchange(lo1));
+            mp = hip + lop;
+          } else {
+            mp = tok_max(exchange(m1));
+          }
+          float c15, B15, zq = 0.f;                        // the quantizer of the two-stage path below
+          if constexpr (ASYM) {
+            const float sp = alpha * mp * (1.0f / 15.0f);
+            zq = sp > 0.f ? rintf(__fdiv_rn(alpha * lop, sp)) : 0.f;
+            c15 = sp > 0.f ? __frcp_rn(alpha * mp) : 0.f;
+            B15 = zq * (1.0f / 15.0f);
+          } else {
+            c15 = mp > 0.f ? __fdividef(7.0f / 15.0f, alpha * mp) : 0.f;
+            B15 = 8.0f / 15.0f;
+          }
+          // codes of column j (this lane) for every row i, 8 nibbles per word (nibble e = row 8w + e)
+          uint32_t cw[N1 / 8];
+          tmem_chunks<N1>(d1, [&](const uint32_t* v, int n, int col) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 8) {
+              if (e < n) {
+                uint32_t wv = 0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                  const float z = fmaf(fma_sat(__uint_as_float(v[e + u]), c15, B15), 15.0f, MAGIC - 8.0f);
+                  wv |= (__float_as_uint(z) & 0xFu) << (4 * u);
+                }
+                cw[(col + e) / 8] = wv;
+              }
+            }
+          });
+          if constexpr (WRITE_Y) {
+            if (t < T)
+              tmem_chunks<N1>(d1, [&](const uint32_t* v, int n, int col) {
+#pragma unroll
+                for (int e = 0; e < 32; ++e)
+                  if (e < n) y_out[t * (N1 * N2) + int64_t(col + e) * N2 + L] = __uint_as_float(v[e]);
+              });
+          }
+          if (g == C::G1 - 1) {                            // D1 slot read completely: MMA1 may reuse it
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&a2full[par]);
+          }
+          // column pair (j, j+1) -> one byte per row i (low nibble = even j): the even lane of the
+          // pair writes rows [0, N1/2), the odd lane rows [N1/2, N1)
+          uint32_t ow[N1 / 8];
+#pragma unroll
+          for (int w = 0; w < N1 / 8; ++w) ow[w] = __shfl_xor_sync(0xffffffffu, cw[w], 1);
+          const bool odd = L & 1;
+#pragma unroll
+          for (int w = 0; w < N1 / 16; ++w) {
+            const uint32_t lo = odd ? ow[w + N1 / 16] : cw[w];    // codes of column j & ~1
+            const uint32_t hi = odd ? cw[w + N1 / 16] : ow[w];    // codes of column j | 1
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int i = (odd ? N1 / 2 : 0) + 8 * w + u;
+              stg[i * (N2 / 2) + (L >> 1)] = uint8_t(((lo >> (4 * u)) & 0xFu) | (((hi >> (4 * u)) & 0xFu) << 4));
+            }
+          }
+          named_bar_sync(1 + grp, 128);                    // the token's packed bytes are staged
+          if (!waited) {
+            tc::griddep_wait();
+            waited = true;
+          }
+          if (t < T) {
+            constexpr int CH = N1 * N2 / 2 / 16;           // 16-byte chunks of one token
+#pragma unroll
+            for (int c = L; c < CH; c += 128)
+              *reinterpret_cast<uint4*>(q + t * (N1 * N2 / 2) + c * 16) = *reinterpret_cast<const uint4*>(stg + c * 16);
+            if (L == 0) {
+              if constexpr (ASYM) {
+                scale[t] = mp > 0.f ? alpha * mp / 15.0f : 1.0f;
+                zero[t] = int8_t(int(zq) - 8);
+              } else {
+                scale[t] = mp > 0.f ? alpha * mp / 7.0f : 1.0f;
+              }
+            }
+          }
+        }
+        continue;
+      }
       // -------- stage-1 epilogue: D1 (fp32) -> prescaled fp16 A operand of stage 2 --------
       int pe[TOK];                                       // per-token prescale exponents
       tc::mbar_wait(&d1full[par], ph);
@@ -527,10 +643,10 @@ static bool small_enabled() {                      // FQ_TQ_SMALL=0: testing aid
   return on;
 }
 
-template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM = false, bool SMALL = false>
+template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM = false, bool SMALL = false, bool IDENT2 = false>
 static cudaError_t launch(const TQArgs& a) {
-  using C = Cfg<N1, N2, SMALL>;
-  auto kern = tq_tc05_kernel<N1, N2, BF16, WRITE_Y, ASYM, SMALL>;
+  using C = Cfg<N1, N2, SMALL, IDENT2>;
+  auto kern = tq_tc05_kernel<N1, N2, BF16, WRITE_Y, ASYM, SMALL, IDENT2>;
   static std::atomic<uint64_t> attr_done{0};   // devices configured for this kernel
   if (cudaError_t e = ensure_smem_attr(kern, int(C::SMEM), attr_done); e != cudaSuccess) return e;
   CUtensorMap mx, m1, m2;
@@ -546,7 +662,9 @@ static cudaError_t launch(const TQArgs& a) {
     const uint32_t box[2] = {64, uint32_t(N1)};
     if (!tmap_encode(&m1, a.p1, 2, 2, dims, strides, box, TMAP_SW128)) return cudaErrorInvalidValue;
   }
-  {
+  if (IDENT2) {
+    m2 = m1;                                       // unused
+  } else {
     const uint64_t dims[2] = {uint64_t(N2), uint64_t(N2)};
     const uint64_t strides[1] = {uint64_t(N2) * 2};
     const uint32_t box[2] = {64, uint32_t(N2)};
@@ -558,6 +676,14 @@ static cudaError_t launch(const TQArgs& a) {
                              a.q, a.scale, a.y, a.zero, a.pdl);
   count_launch();
   return e;
+}
+
+template <int N1>
+static cudaError_t dispatch_ident2(const TQArgs& a) {     // P2 = I, n2 = 128
+  if (a.zero) return a.bf16 ? launch<N1, 128, true, false, true, false, true>(a)
+                            : launch<N1, 128, false, false, true, false, true>(a);
+  if (a.bf16) return a.y ? launch<N1, 128, true, true, false, false, true>(a) : launch<N1, 128, true, false, false, false, true>(a);
+  return a.y ? launch<N1, 128, false, true, false, false, true>(a) : launch<N1, 128, false, false, false, false, true>(a);
 }
 
 template <int N1, int N2>
@@ -591,8 +717,9 @@ extern "C" int fq_debug_stamps(unsigned long long* out) {
 #endif
 
 bool tq_tc05_supported(const TQArgs& a) {
-  const bool shape = (a.n1 == 64 && (a.n2 == 64 || a.n2 == 128)) ||
-                     (a.n2 == 128 && (a.n1 == 80 || a.n1 == 96 || a.n1 == 112 || a.n1 == 128));
+  const bool shape = a.p2 == nullptr ? (a.n2 == 128 && (a.n1 == 32 || a.n1 == 64))   // P2 = I
+                                     : (a.n1 == 64 && (a.n2 == 64 || a.n2 == 128)) ||
+                                           (a.n2 == 128 && (a.n1 == 80 || a.n1 == 96 || a.n1 == 112 || a.n1 == 128));
   const bool al = ((reinterpret_cast<uintptr_t>(a.x) | reinterpret_cast<uintptr_t>(a.p1) |
                     reinterpret_cast<uintptr_t>(a.p2) | reinterpret_cast<uintptr_t>(a.q)) & 15u) == 0 &&
                   (a.ldx * 2) % 16 == 0 && a.T < (int64_t(1) << 31);
@@ -601,6 +728,11 @@ bool tq_tc05_supported(const TQArgs& a) {
 
 cudaError_t tq_tc05_launch(const TQArgs& a) {
   using namespace tq5;
+  if (a.p2 == nullptr) {
+    if (a.n1 == 32 && a.n2 == 128) return dispatch_ident2<32>(a);
+    if (a.n1 == 64 && a.n2 == 128) return dispatch_ident2<64>(a);
+    return cudaErrorInvalidValue;
+  }
   if (a.n1 == 64 && a.n2 == 64) return dispatch<64, 64>(a);
   if (a.n1 == 64 && a.n2 == 128) return dispatch<64, 128>(a);
   if (a.n1 == 80 && a.n2 == 128) return dispatch<80, 128>(a);

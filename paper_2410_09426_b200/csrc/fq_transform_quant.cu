@@ -441,7 +441,8 @@ bool tq_asym_supported(const TQArgs& a) {
 // instead of a launch that cannot fit its shared memory)
 bool tq_kernel_available(const TQArgs& a) {
   const int impl = tq_impl();
-  if (a.p2 == nullptr) return tq_ident2_supported(a.n1, a.n2);
+  if (a.p2 == nullptr)                             // P2 = I: tcgen05 (sym/asym), else mma.sync (sym)
+    return (impl == 0 && tq_tc05_supported(a)) || (!a.zero && tq_ident2_supported(a.n1, a.n2));
   if (impl == 0 && (tq_tc05_supported(a) || tq_wide_supported(a))) return true;
   if (impl == 0 && int64_t(a.n1) * a.n2 <= 1024 && tq_simt_supported(a.n1, a.n2)) return true;
   const bool tc_shape = (a.n1 % 16 == 0) && (a.n2 % 16 == 0);
@@ -450,12 +451,13 @@ bool tq_kernel_available(const TQArgs& a) {
 }
 
 bool tq_is_pdl(const TQArgs& a) {
-  return a.p2 != nullptr && tq_impl() == 0 && (tq_tc05_supported(a) || tq_wide_supported(a));
+  return tq_impl() == 0 && (tq_tc05_supported(a) || (a.p2 != nullptr && tq_wide_supported(a)));
 }
 
 cudaError_t transform_quant_launch(const TQArgs& a) {
   const int impl = tq_impl();
-  if (a.p2 == nullptr) return tq_ident2_launch(a);     // P2 = I (validated by the ABI layer)
+  if (a.p2 == nullptr)                                  // P2 = I (validated by the ABI layer)
+    return (impl == 0 && tq_tc05_supported(a)) ? tq_tc05_launch(a) : tq_ident2_launch(a);
   if (a.zero) {                          // asymmetric: tcgen05 kernel, else the CUDA-core kernel
     if (impl == 0 && tq_tc05_supported(a)) return tq_tc05_launch(a);
     if (impl == 0 && tq_wide_supported(a)) return tq_wide_launch(a);

@@ -146,6 +146,41 @@ def test_transform_p2_identity(n1, alpha, tdtype):
     assert torch.equal(q2.cpu(), q.cpu()) and torch.equal(s2.cpu(), s.cpu())
 
 
+@pytest.mark.parametrize("n1", [32, 64])
+@pytest.mark.parametrize("impl", [0, 1], ids=["tcgen05", "mma_sync"])
+@pytest.mark.parametrize("T", [1, 2, 3, 149, 297])
+def test_transform_p2_identity_kernels_and_tails(n1, impl, T):
+    """P2 = I on both kernels (tcgen05 stage-1-only, the default; legacy mma.sync) at token counts
+    around the tile (1 or 2 tokens) and grid sizes: nothing written past T, parity with the oracle."""
+    n2 = 128
+    x, p1, _ = make_inputs(T, n1, n2, seed=T + n1)
+    q = torch.full((T + 2, n1 * n2 // 2), 0xAB, dtype=torch.uint8, device=DEV)
+    s = torch.full((T + 2,), -1.0, dtype=torch.float32, device=DEV)
+    fq.fq_set_tq_impl(impl)
+    try:
+        fq.fq_transform_quant(x.to(DEV), n1, n2, p1.to(DEV), None, 0.9, q[:T], s[:T])
+        torch.cuda.synchronize()
+    finally:
+        fq.fq_set_tq_impl(0)
+    assert np.all(np_of(q[T:]) == 0xAB) and np.all(np_of(s[T:]) == -1.0)
+    qo, so, yo = O.transform_quant(x.float().numpy(), p1.float().numpy(), np.eye(n2), 0.9)
+    parity.check_transform(np_of(q[:T]), np_of(s[:T]), None, yo, qo, so, label=f"P2=I impl {impl} T={T}")
+
+
+@pytest.mark.parametrize("n1", [32, 64])
+@pytest.mark.parametrize("alpha", [1.0, 0.9])
+@pytest.mark.parametrize("tdtype", [torch.float16, torch.bfloat16])
+def test_transform_p2_identity_asym(n1, alpha, tdtype):
+    """FQ_ASYM with P2 = I (tcgen05 kernel): codes, scales and zero points against the oracle's
+    asymmetric quantizer of P1^T V (reading R19, R22)."""
+    n2, T = 128, 211
+    x, p1, _ = make_inputs(T, n1, n2, seed=n1 + 11, tdtype=tdtype)
+    q, s, z = fq.transform_quant_asym(x.to(DEV), n1, n2, p1.to(DEV), None, alpha)
+    torch.cuda.synchronize()
+    qo, so, zo, yo = O.transform_quant_asym(x.float().numpy(), p1.float().numpy(), np.eye(n2), alpha)
+    parity.check_asym(np_of(q), np_of(s), np_of(z), yo, alpha, qo, so, zo, label=f"asym P2=I a={n1}")
+
+
 def test_gpu_weight_prep_p2_identity():
     """fq_prepare_weight with p2 = NULL: W' = P1^{-1} W~ (P2 = I, so P2^{-T} = I); parity as in
     test_gpu_weight_prep_matches_oracle (oracle with the fp16-rounded P1^{-T} and the identity)."""
