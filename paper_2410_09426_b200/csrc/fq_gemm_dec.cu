@@ -78,8 +78,16 @@ constexpr int UK = 32;                        // K per tcgen05.mma kind::i8
 // tcgen05.st by one converter thread per weight row), only the widened activations to shared
 // memory -- 6 MMA stages in flight instead of 2 within the same shared-memory budget.
 constexpr bool TMEMW = FQ_DEC_TMEMW != 0;
-constexpr int STAGES = TMEMW ? 6 : FQ_DEC_STAGES;   // widened operand stages
+#ifndef FQ_DEC_TSTAGES
+#define FQ_DEC_TSTAGES 6
+#endif
+constexpr int STAGES = TMEMW ? FQ_DEC_TSTAGES : FQ_DEC_STAGES;   // widened operand stages
 constexpr int PSTAGES = FQ_DEC_PSTAGES;       // packed TMA ring
+#ifndef FQ_DEC_BATCH
+#define FQ_DEC_BATCH 2
+#endif
+constexpr int DB = FQ_DEC_BATCH;              // K-blocks converted per synchronisation (TMEMW path)
+static_assert(DB >= 1 && DB < FQ_DEC_PSTAGES, "batch within the packed ring");
 constexpr int WP_BYTES = BM * BK / 2;         // packed weights per stage (8 KB at BK = 128)
 constexpr int AP_BYTES = TN_MAX * BK / 2;     // packed activations per stage (max)
 constexpr int P_BYTES = WP_BYTES + AP_BYTES;  // ring stage (1 KB multiple)
@@ -97,7 +105,15 @@ constexpr int THREADS = (CONV_WARP0 + NUM_CONV_WARPS) * 32;
 constexpr int CONV_THREADS = NUM_CONV_WARPS * 32;
 // TMEMW: warps 8-11 widen the weights into TMEM; the activations are widened by warps 12-15 AND
 // the epilogue warps 4-7 (idle until the last MMA), one 16-byte chunk per thread at T = 64
-constexpr int NUM_ARRIVE = TMEMW ? 12 : NUM_CONV_WARPS;   // converter warps signalling per stage
+#ifndef FQ_DEC_L2PF
+#define FQ_DEC_L2PF 0
+#endif
+#ifndef FQ_DEC_EPI_CONV
+#define FQ_DEC_EPI_CONV 0     // round 2: the converter warps alone are as fast (C4 74.7 vs 77.9 us)
+#endif
+constexpr bool EPI_CONV = FQ_DEC_EPI_CONV != 0;            // epilogue warps help widen activations
+constexpr int A_CONV_THREADS = EPI_CONV ? 256 : 128;
+constexpr int NUM_ARRIVE = TMEMW ? (EPI_CONV ? 12 : 8) : NUM_CONV_WARPS;   // converter warps signalling per stage
 constexpr int TMEM_COLS = TMEMW ? 256 : 64;
 constexpr int MAX_SPLIT = 8;                  // portable cluster size
 constexpr size_t SMEM_BYTES = size_t(STAGES) * W_BYTES + size_t(PSTAGES) * P_BYTES + 1024 + 256;
@@ -197,20 +213,32 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
 
   // activation rows (TN x 4 chunks) -> widened SWIZZLE_128B K-major stage, by 256 threads
   // (at = 0..255: epilogue warps 4-7 and converter warps 12-15)
+  // Both converter paths work on DB K-blocks per iteration and synchronise once per batch (one
+  // fence / tcgen05.wait::st for the DB stages), so DB K-blocks are in conversion at a time: a
+  // single K-block's wait -> load -> widen -> store -> fence -> signal chain is latency-bound
+  // (~0.27 us on the B200, scripts/trace_dec.py), far longer than its share of the weight stream.
   auto convert_a = [&](int at) {
-    for (int j = 0; j < nk; ++j) {
-      const int sp = j % PSTAGES, st = j % STAGES;
-      tc::mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1);
-      tc::mbar_wait(&pfull[sp], (j / PSTAGES) & 1);
-      const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES + WP_BYTES);
-      const uint32_t dst = smem_u32(sW + size_t(st) * W_BYTES);
-      for (int task = at; task < TN * CPR; task += 256)
-        convert_chunk(src + uint32_t(task * 16), dst, task / CPR, task % CPR, AW_ATOM);
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&pempty[sp]);
+    for (int j0 = 0; j0 < nk; j0 += DB) {
+      const int nb = nk - j0 < DB ? nk - j0 : DB;
+#pragma unroll
+      for (int b = 0; b < DB; ++b) {
+        if (b < nb) {
+          const int j = j0 + b, sp = j % PSTAGES, st = j % STAGES;
+          tc::mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1);
+          tc::mbar_wait(&pfull[sp], (j / PSTAGES) & 1);
+          const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES + WP_BYTES);
+          const uint32_t dst = smem_u32(sW + size_t(st) * W_BYTES);
+          for (int task = at; task < TN * CPR; task += A_CONV_THREADS)
+            convert_chunk(src + uint32_t(task * 16), dst, task / CPR, task % CPR, AW_ATOM);
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&pempty[sp]);
+        }
+      }
       tc::fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&full[st]);
+#pragma unroll
+      for (int b = 0; b < DB; ++b)
+        if (b < nb && lane == 0) tc::mbar_arrive(&full[(j0 + b) % STAGES]);
     }
   };
 
@@ -221,6 +249,11 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       // (host-side hazard check, fq_abi.cu), start streaming them before the wait
       if (!(pdl & PDL_P)) tc::griddep_wait();
       const int pre = nk < PSTAGES ? nk : PSTAGES;
+#if FQ_DEC_L2PF
+      // the rest of this CTA's weight slice into L2 now (one bulk tensor prefetch per K-block):
+      // the ring's loads then hit L2 instead of waiting a full HBM round trip each
+      for (int j = pre; j < nk; ++j) tc::tma_prefetch_l2_2d(&tmW, kb_of(j) * (BK / 2), fb * BM);
+#endif
       for (int j = 0; j < pre; ++j) {
         if (j < 36) dtrace(tslot, 4 + j);
         tc::mbar_expect_tx(&pfull[j], uint32_t(WP_BYTES + ap_bytes));
@@ -252,31 +285,39 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         // (conflict-free) -> widened in registers -> tcgen05.st into this stage's TMEM columns
         const int q = warp & 3, r = q * 32 + lane;
         const uint32_t tl = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(W_COL0);
-        for (int j = 0; j < nk; ++j) {
-          const int sp = j % PSTAGES, st = j % STAGES;
-          tc::mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1);
-          tc::mbar_wait(&pfull[sp], (j / PSTAGES) & 1);
-          const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES) + uint32_t(r * 64);
-          uint32_t w[32];
+        for (int j0 = 0; j0 < nk; j0 += DB) {
+          const int nb = nk - j0 < DB ? nk - j0 : DB;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const uint4 pk = tc::lds128(src + uint32_t((c ^ ((r >> 1) & 3)) << 4));
-            widen8(pk.x, w[8 * c + 0], w[8 * c + 1]);
-            widen8(pk.y, w[8 * c + 2], w[8 * c + 3]);
-            widen8(pk.z, w[8 * c + 4], w[8 * c + 5]);
-            widen8(pk.w, w[8 * c + 6], w[8 * c + 7]);
+          for (int b = 0; b < DB; ++b) {
+            if (b < nb) {
+              const int j = j0 + b, sp = j % PSTAGES, st = j % STAGES;
+              tc::mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1);
+              tc::mbar_wait(&pfull[sp], (j / PSTAGES) & 1);
+              const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES) + uint32_t(r * 64);
+              uint32_t w[32];
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const uint4 pk = tc::lds128(src + uint32_t((c ^ ((r >> 1) & 3)) << 4));
+                widen8(pk.x, w[8 * c + 0], w[8 * c + 1]);
+                widen8(pk.y, w[8 * c + 2], w[8 * c + 3]);
+                widen8(pk.z, w[8 * c + 4], w[8 * c + 5]);
+                widen8(pk.w, w[8 * c + 6], w[8 * c + 7]);
+              }
+              tc::tmem_st32(tl + uint32_t(st * WT_COLS), w);
+              __syncwarp();
+              if (lane == 0) tc::mbar_arrive(&pempty[sp]);   // the loads were consumed by the st
+            }
           }
-          tc::tmem_st32(tl + uint32_t(st * WT_COLS), w);
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&pempty[sp]);   // the loads were consumed by the st
           tc::tmem_st_wait();
           tc::fence_before();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&full[st]);
-          if (threadIdx.x == CONV_WARP0 * 32 && j < 36) dtrace(tslot, 40 + j);
+#pragma unroll
+          for (int b = 0; b < DB; ++b)
+            if (b < nb && lane == 0) tc::mbar_arrive(&full[(j0 + b) % STAGES]);
+          if (threadIdx.x == CONV_WARP0 * 32 && j0 < 36) dtrace(tslot, 40 + j0);
         }
       } else {
-        convert_a(threadIdx.x - (CONV_WARP0 + 4) * 32 + 128);
+        convert_a(threadIdx.x - (CONV_WARP0 + 4) * 32 + (EPI_CONV ? 128 : 0));
       }
     } else
     for (int j = 0; j < nk; ++j) {
@@ -341,7 +382,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         }
       }
     }
-    if constexpr (TMEMW) convert_a(threadIdx.x - EPI_WARP0 * 32);
+    if constexpr (TMEMW && EPI_CONV) convert_a(threadIdx.x - EPI_WARP0 * 32);
     tc::mbar_wait(tfull, 0);
     tc::fence_after();
     if (threadIdx.x == EPI_WARP0 * 32) dtrace(tslot, 112);

@@ -11,11 +11,13 @@
 // shared-memory and L1 traffic per MAC relative to a single-CTA tile.
 //   warps 0-3  : epilogue (own TMEM lanes -> dequant -> swizzled smem -> TMA bulk store)
 //   warp  4    : TMEM allocator (both CTAs) + MMA issuer (leader CTA only)
-//   warps 5-12 : A converters, half an activation row per thread: packed row from the TMA ring
-//                (SWIZZLE_64B, conflict-free) -> widened in registers -> tcgen05.st into TMEM
-//   warps 13-18: B converters, 4 threads per weight row: packed rows from the TMA ring ->
-//                widened SWIZZLE_128B K-major operand in shared memory
-//   warp  19   : TMA producer of the packed A+B ring (PSTAGES K-blocks deep)
+//   warps 5-8  : A converters (FQ_GEMM_AWARPS), one activation row per thread: packed row from the
+//                TMA ring (SWIZZLE_128B, conflict-free) -> widened in registers -> tcgen05.st into TMEM
+//   warps 9-12 : B converters (FQ_GEMM_BWARPS), 16-byte packed chunks of the weight rows from the
+//                ring -> widened SWIZZLE_128B K-major operand in shared memory
+//   warp  13   : TMA producer of the packed A+B ring (PSTAGES K-blocks deep)
+// (Round 2 measured the converter warp counts: 4 A + 4 B warps beat 8 + 6 by 3-8% on every C3
+// shape -- fewer warps contend less for the shared-memory pipe -- scripts/gemm_shapes.py.)
 // Loads are fully asynchronous (TMA, no registers, no LSU queue); per K-block and SM the shared-
 // memory traffic is 14 KB (TMA) + 14 KB (converter reads) + 12 KB (widened B) + 12 KB (MMA read of
 // B), the A operand never touches shared memory after conversion.
@@ -55,7 +57,7 @@ constexpr int BM = 256, BM_CTA = 128;     // tokens per pair tile / per CTA
 #define FQ_GEMM_PSTAGES 4       // cap on the packed ring depth (shared memory permitting)
 #endif
 #ifndef FQ_GEMM_BWARPS
-#define FQ_GEMM_BWARPS 6
+#define FQ_GEMM_BWARPS 4     // measured best (round 2: 2-10 tried; fewer B warps, less contention)
 #endif
 #ifndef FQ_GEMM_BK
 #define FQ_GEMM_BK 256
@@ -72,13 +74,13 @@ constexpr int TMEM_ACC0 = 0;              // two accumulators [0, 2*BN)
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_EPI_WARPS = 4, MMA_WARP = 4;
 #ifndef FQ_GEMM_AWARPS
-#define FQ_GEMM_AWARPS 8
+#define FQ_GEMM_AWARPS 4     // measured best (round 2: 4 > 8 > 16; one full row per thread)
 #endif
 constexpr int A_WARP0 = 5, NUM_A_WARPS = FQ_GEMM_AWARPS;   // 4 warps per K part (one per TMEM lane quarter)
 constexpr int A_PARTS = NUM_A_WARPS / 4;                   // K parts of a row: 2 (halves) or 4 (quarters)
 constexpr int A_CH = (BK / 32) / A_PARTS;                  // packed 16-byte chunks per thread and K-block
-static_assert(A_CH == 2 || A_CH == 4, "A chunks per thread");
-static_assert(NUM_A_WARPS == 8 || NUM_A_WARPS == 16, "A converter warps: 8 or 16");
+static_assert(A_CH == 2 || A_CH == 4 || A_CH == 8, "A chunks per thread");
+static_assert(NUM_A_WARPS == 4 || NUM_A_WARPS == 8 || NUM_A_WARPS == 16, "A converter warps: 4, 8 or 16");
 constexpr int B_WARP0 = A_WARP0 + NUM_A_WARPS, NUM_B_WARPS = FQ_GEMM_BWARPS;
 constexpr int NUM_CONV_WARPS = NUM_A_WARPS + NUM_B_WARPS;
 constexpr int TMA_WARP = B_WARP0 + NUM_B_WARPS;
@@ -299,8 +301,14 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           widen8(pk.z, w[8 * c + 4], w[8 * c + 5]);
           widen8(pk.w, w[8 * c + 6], w[8 * c + 7]);
         }
-        if constexpr (A_CH == 4) tc::tmem_st32(tl + uint32_t(st * A_COLS), *reinterpret_cast<uint32_t(*)[32]>(w));
-        else tmem_st16(tl + uint32_t(st * A_COLS), *reinterpret_cast<uint32_t(*)[16]>(w));
+        if constexpr (A_CH == 8) {
+          tc::tmem_st32(tl + uint32_t(st * A_COLS), *reinterpret_cast<uint32_t(*)[32]>(w));
+          tc::tmem_st32(tl + uint32_t(st * A_COLS + 32), *reinterpret_cast<uint32_t(*)[32]>(w + 32));
+        } else if constexpr (A_CH == 4) {
+          tc::tmem_st32(tl + uint32_t(st * A_COLS), *reinterpret_cast<uint32_t(*)[32]>(w));
+        } else {
+          tmem_st16(tl + uint32_t(st * A_COLS), *reinterpret_cast<uint32_t(*)[16]>(w));
+        }
         // release the ring slot only after the loaded values were consumed (the tcgen05.st reads
         // them): mbarrier.arrive does not wait for an outstanding ld.shared, so an arrive right
         // after the loads lets the TMA overwrite the slot before a delayed load has read it
