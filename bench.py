@@ -338,12 +338,10 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    from paper_2410_09426_b200 import sharding
+
     def max_over_ranks(v):
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return sharding.max_over_ranks(v, dev)
 
     def timed_steps(n, **kw):
         """n steps, L2 flushed before each (flush untimed); returns the summed step time (ms)."""
@@ -402,14 +400,10 @@ def run_ours(args):
     if world > 1:
         props = torch.cuda.get_device_properties(dev)
         bus = float(getattr(props, "pci_bus_id", -1)) * 1000.0 + float(getattr(props, "pci_device_id", 0))
-        mine = torch.tensor([float(rank), float(T), my_ms, float(props.multi_processor_count), bus],
-                            dtype=torch.float64, device=dev)
-        allr = [torch.empty_like(mine) for _ in range(world)]
-        dist.all_gather(allr, mine)
+        rows = sharding.rank_table([rank, T, my_ms, props.multi_processor_count, bus], dev)
         rank_lines = [{"rank": int(r[0]), "tokens": int(r[1]), "ms_per_step": round(float(r[2]), 4),
                        "tokens_per_s": round(float(r[1]) / (float(r[2]) * 1e-3), 1), "sms": int(r[3]),
-                       "pci": int(r[4])}
-                      for r in (t.tolist() for t in allr)]
+                       "pci": int(r[4])} for r in rows]
     sys.stderr.write(f"[bench] rank {rank}/{world} cuda:{local} {torch.cuda.get_device_name(dev)} "
                      f"backend={'nccl' if world > 1 else 'none'} tokens [{lo},{hi}) of {total_T}: "
                      f"{my_ms:.4f} ms/step\n")
@@ -576,22 +570,18 @@ def run_ours(args):
     #      streams, same kernels) and compares bit for bit; every rank checks its own block.
     verify = None
     if world > 1 and not args.no_verify:
-        from paper_2410_09426_b200.sharding import gather_rows, shard_range
         L0 = layers[0]
         lin = L0["lin"]
         step()
         torch.cuda.synchronize()
-        full = gather_rows(L0["y"], total_T if scaling == "strong" else world * T)
-        own = bool(torch.equal(full[lo:hi], L0["y"]))
-        ok = torch.tensor([1 if own else 0], device=dev)
-        if rank == 0:
-            rlo, rhi = shard_range(full.shape[0], world - 1, world)
+
+        def recompute_last(rlo, rhi):
             xr = torch.from_numpy(synth.activations(rhi, lin.K, seed=1000, tag=lin.name, rows=range(rlo, rhi))).to(dev)
             yr = fq.flatquant_linear(xr, lin.n1, lin.n2, L0["p1"], L0["p2"], args.alpha, L0["qw"], L0["sw"])
             torch.cuda.synchronize()
-            ok &= torch.tensor([1 if torch.equal(full[rlo:rhi], yr) else 0], device=dev)
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        verify = bool(ok.item() == 1)
+            return yr
+
+        verify = sharding.verify_gather(L0["y"], total_T, recompute_last)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -166,6 +166,27 @@ FQ_DEVICE void tmem_chunks(uint32_t taddr, F&& fn) {
   }
 }
 
+// Single-pass variant for rows of N <= 64 columns: the row is loaded from TMEM once into
+// registers and both the statistics and the conversion read the registers (TMEM reads are the
+// epilogues' throughput limit: one pass instead of two halves them).
+template <int N>
+FQ_DEVICE void tmem_ld_row(uint32_t taddr, uint32_t* v) {
+  static_assert(N % 16 == 0 && N <= 64, "");
+#pragma unroll
+  for (int c = 0; c < N; c += 16) tc::tmem_ld16(taddr + uint32_t(c), *reinterpret_cast<uint32_t(*)[16]>(v + c));
+  tc::tmem_ld_wait();
+}
+template <int N, bool SINGLE, typename F>
+FQ_DEVICE void row_chunks(uint32_t taddr, const uint32_t* regs, F&& fn) {
+  if constexpr (SINGLE) {
+    static_assert(N % 32 == 0, "");
+#pragma unroll
+    for (int c = 0; c < N; c += 32) fn(regs + c, 32, c);
+  } else {
+    tmem_chunks<N>(taddr, fn);
+  }
+}
+
 // 8 quantized values in MAGIC form (low nibble of the bit pattern = two's-complement code)
 // -> one 32-bit word, element 2m in the low nibble of byte m.
 FQ_DEVICE uint32_t pack8(const float (&v)[8]) {
@@ -474,12 +495,17 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
       if (L == 0 && k < 16) trace(56 + k);
 #define FQ_SUB(sub) \
   if (L == 0 && k < 8) trace(128 + k * 16 + (sub))
+      constexpr bool SINGLE1 = (N1 == 64);               // row of 64: one TMEM pass (registers)
+      constexpr bool SINGLE2 = (N2 == 64);
 #pragma unroll
       for (int g = 0; g < C::G1; ++g) {
         const uint32_t d1 = lane_base + uint32_t(par * C::D1C + g * N1);
-        // pass 1: max |W| over this lane's row (two-pass keeps <= 32 values in registers)
+        uint32_t rv1[SINGLE1 ? N1 : 1];
+        if constexpr (SINGLE1) tmem_ld_row<N1>(d1, rv1);
+        // pass 1: max |W| over this lane's row (rows > 64 columns: two passes over TMEM keep
+        // <= 32 values in registers)
         float m1 = 0.f;
-        tmem_chunks<N1>(d1, [&](const uint32_t* v, int n, int) {
+        row_chunks<N1, SINGLE1>(d1, rv1, [&](const uint32_t* v, int n, int) {
 #pragma unroll
           for (int e = 0; e < 32; e += 2)
             if (e < n) m1 = max3f(m1, fabsf(__uint_as_float(v[e])), fabsf(__uint_as_float(v[e + 1])));
@@ -500,7 +526,7 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
         const int j = (N2 == 64) ? (L & 63) : L;         // K row (j') of the stage-2 A operand
         const uint32_t row = smem_u32(sA2) + uint32_t(par * C::A2_BYTES + j * 128);
         // pass 2: prescale, fp16, swizzled MN-major row j of A2
-        tmem_chunks<N1>(d1, [&](const uint32_t* v, int n, int col) {
+        row_chunks<N1, SINGLE1>(d1, rv1, [&](const uint32_t* v, int n, int col) {
 #pragma unroll
           for (int e = 0; e < 32; e += 8) {
             if (e < n) {
@@ -533,7 +559,9 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
       const int i = (N1 == 64) ? (L & 63) : L;
       const bool valid = (N1 == 64) || (L < N1);
       float m2 = 0.f, hi2 = 0.f, lo2 = 0.f;             // sym: max |y|; asym: max(max y, 0), -min(min y, 0)
-      tmem_chunks<N2>(d2, [&](const uint32_t* v, int, int) {
+      uint32_t rv2[SINGLE2 ? N2 : 1];
+      if constexpr (SINGLE2) tmem_ld_row<N2>(d2, rv2);
+      row_chunks<N2, SINGLE2>(d2, rv2, [&](const uint32_t* v, int, int) {
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
           const float a0 = __uint_as_float(v[e]), a1 = __uint_as_float(v[e + 1]);
@@ -586,7 +614,7 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
         tc::griddep_wait();
         waited = true;
       }
-      tmem_chunks<N2>(d2, [&](const uint32_t* v, int, int col) {   // N2 % 32 == 0: full chunks
+      row_chunks<N2, SINGLE2>(d2, rv2, [&](const uint32_t* v, int, int col) {   // N2 % 32 == 0: full chunks
         uint32_t w[4];
 #pragma unroll
         for (int c8 = 0; c8 < 4; ++c8) {

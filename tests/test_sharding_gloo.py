@@ -77,3 +77,40 @@ def test_gloo_world2_gather_and_timing(T):
     assert sorted(res) == [0, 1]
     for r, flags in res.items():
         assert all(flags), f"rank {r}: {flags}"
+
+
+def _bench_helpers_worker(rank, world, port, results):
+    """bench.py's multi-GPU helpers on gloo: max over ranks, the per-rank table, and the gather
+    verification (passes on correct shards, fails on a corrupted one, same verdict everywhere)."""
+    from paper_2410_09426_b200 import sharding
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dev = torch.device("cpu")
+        T = 37
+        full = torch.arange(T * 5, dtype=torch.float32).reshape(T, 5) * 0.5
+        lo, hi = sharding.shard_range(T, rank, world)
+        mx = sharding.max_over_ranks(3.0 + rank, dev)
+        tab = sharding.rank_table([rank, hi - lo, 1.5 * rank], dev)
+        good = sharding.verify_gather(full[lo:hi].clone(), T, lambda a, b: full[a:b].clone())
+        bad_local = full[lo:hi].clone()
+        if rank == world - 1:
+            bad_local[0, 0] += 1.0                   # the last shard is wrong
+        bad = sharding.verify_gather(bad_local, T, lambda a, b: full[a:b].clone())
+        results[rank] = (mx == 3.0 + world - 1, [int(r[0]) for r in tab] == list(range(world)),
+                         sum(int(r[1]) for r in tab) == T, good, not bad)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_bench_helpers():
+    world = 2
+    port = _free_port()
+    with mp.Manager() as m:
+        results = m.dict()
+        mp.spawn(_bench_helpers_worker, args=(world, port, results), nprocs=world, join=True)
+        res = dict(results)
+    assert sorted(res) == [0, 1]
+    for r, flags in res.items():
+        assert all(flags), f"rank {r}: {flags}"
