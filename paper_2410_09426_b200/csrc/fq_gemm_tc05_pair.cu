@@ -571,16 +571,16 @@ bool gemm_pair_supported(const GemmArgs& a) {
   return a.K % 32 == 0 && a.K < 131072 && a.N % 8 == 0 && a.T <= int64_t(1) << 30 && tmap_available();
 }
 
-// Tile width per shape.  A pair tile's main loop is bound by the operand conversion, so the time of
-// one wave grows slower than the width; cost = waves x measured per-wave cost (scripts/gemm_shapes.py
-// with widths forced, C3 shapes and 8192^3, round 2: 192 and 160 run 2 and 3 MMA stages, 128 and the
-// single-accumulator 256 run 4).  Relative to 128: 1.19 at 160, 1.23 at 192, and 1.55 + 0.15 * 4096 / K
-// at 256 (its epilogue is not overlapped, which costs more at short K).  So 256 wins where it saves
-// waves (o_proj / C2 3 -> 2, down_proj 3 -> 2, 8192^3) and 192 elsewhere.
+// Tile width per shape: cost = waves x measured per-wave cost (scripts/gemm_shapes.py with the
+// widths forced; round 2, 4 A + 4 B converter warps; 192 and 160 run 2 and 3 MMA stages, 128 and
+// the single-accumulator 256 run 4).  Relative to 128: 1.19 at 160, 1.23 at 192, and
+// 1.23 x (1.12 + 0.2 x 4096 / K) at 256 (its epilogue is not overlapped, which costs more at short
+// K).  256 wins where it saves waves: qkv 4 -> 3, o_proj / C2 3 -> 2, down_proj 3 -> 2, 8192^3;
+// 192 keeps gate/up (17 vs 13 waves, equal time).
 int gemm_pair_pick_bn(int64_t T, int N, int K, int clusters) {
   using g3::BM;
   const int cands[4] = {192, 160, 128, 256};
-  const double rel[4] = {1.23, 1.19, 1.07, 1.55 + 0.15 * 4096.0 / double(K > 0 ? K : 1)};
+  const double rel[4] = {1.23, 1.19, 1.07, 1.23 * (1.12 + 0.2 * 4096.0 / double(K > 0 ? K : 1))};
   int best = 192;
   double best_cost = 0;
   for (int i = 0; i < 4; ++i) {
