@@ -3,7 +3,7 @@
   profiles/<tag>_<name>.txt        --set full summary + top source lines of each capture
   profiles/ncu_traffic.json        dram bytes (read + write) per launch of each captured kernel,
                                    read by bench.py for roofline.traffic
-usage: python scripts/make_profiles.py <tag> [gpurun_out]"""
+usage: python scripts/make_profiles.py <tag> [gpurun_out] [out_dir]"""
 import csv
 import io
 import json
@@ -14,7 +14,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag = sys.argv[1]
 src = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out")
-prof = os.path.join(ROOT, "profiles")
+prof = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "profiles")
 os.makedirs(prof, exist_ok=True)
 
 
@@ -26,7 +26,7 @@ launches = os.path.join(src, "launches.csv")
 if os.path.exists(launches):
     with open(os.path.join(prof, f"{tag}_launches.txt"), "w") as f:
         f.write("# ncu --metrics gpu__time_duration.sum --clock-control none: python bench.py --steps 2 --warmup 3 "
-                "--no-cpu --no-e2e --no-fp16 (C3).  Cold-cache serialised launches: compare shares.\n")
+                "--no-cpu --no-e2e --no-fp16 --no-kv --no-fig6 (C3).  Cold-cache serialised launches: compare shares.\n")
         f.write(run(os.path.join(ROOT, "scripts", "launch_summary.py"), launches))
         f.write("\n## last 8 launches = one step (4 linears x transform+quant, W4A4 GEMM)\n")
         f.write(run(os.path.join(ROOT, "scripts", "launch_summary.py"), launches, "--last", "8"))
