@@ -579,12 +579,13 @@ bool gemm_pair_supported(const GemmArgs& a) {
 // 192 keeps gate/up (17 vs 13 waves, equal time).
 int gemm_pair_pick_bn(int64_t T, int N, int K, int clusters) {
   using g3::BM;
-  const double r256 = 1.23 * (1.12 + 0.2 * 4096.0 / double(K > 0 ? K : 1));
-  const int cands[5] = {192, 160, 128, 256, 224};
-  const double rel[5] = {1.23, 1.19, 1.07, r256, r256 * 224.0 / 256.0};
+  // (a 224-wide single-accumulator tile was measured too: gate/up 176 us in 14 waves vs 169 us in 17
+  // waves of 192 -- not a candidate)
+  const int cands[4] = {192, 160, 128, 256};
+  const double rel[4] = {1.23, 1.19, 1.07, 1.23 * (1.12 + 0.2 * 4096.0 / double(K > 0 ? K : 1))};
   int best = 192;
   double best_cost = 0;
-  for (int i = 0; i < 5; ++i) {
+  for (int i = 0; i < 4; ++i) {
     const int bn = cands[i];
     const int64_t tiles = ((T + BM - 1) / BM) * ((N + bn - 1) / bn);
     const double cost = double((tiles + clusters - 1) / clusters) * rel[i];
@@ -648,7 +649,6 @@ cudaError_t gemm_pair_launch(const GemmArgs& a, int bn) {
   if (bn == 0) bn = gemm_pair_pick_bn(a.T, a.N, a.K, std::max(1, num_sms() / 2));
   switch (bn) {
     case 256: return launch_bn<256>(a);
-    case 224: return launch_bn<224>(a);
     case 160: return launch_bn<160>(a);
     case 128: return launch_bn<128>(a);
     case 96: return launch_bn<96>(a);
