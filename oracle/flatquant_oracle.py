@@ -309,7 +309,8 @@ def flatquant_linear(x, p1, p2, alpha, w, alpha_w=1.0):
 # ---------------------------------------------------------------------------
 # Near-tie classification used by the code-parity bar (SURVEY.md §8(c) bar 3):
 # v = y/s in code units; a code may differ by +-1 only where v is within tau
-# of a rounding boundary (k + 1/2) or of a clamp boundary.
+# of a rounding boundary (k + 1/2).  (The asymmetric bar's additional clamp
+# exemption is applied by the test helper, tests/parity.py:check_asym.)
 # ---------------------------------------------------------------------------
 def near_tie_mask(y, s, tau: float) -> np.ndarray:
     v = _f64(y) / _f64(s)[:, None]
