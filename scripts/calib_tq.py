@@ -50,7 +50,7 @@ for mb in (8.4, 16.8, 64.0):
     out(what=f"copy {mb} MB -> {mb} MB", gbs=round(2 * n * 2 / (r["mean_us"] * 1e-6) / 1e9, 1), **r)
 
 cfg = synth.config(os.environ.get("CFG", "C3"))
-T = cfg["T"]
+T = int(os.environ.get("T", cfg["T"]))
 for lin in cfg["linears"]:
     x = torch.from_numpy(synth.activations(T, lin.K, seed=1, tag=lin.name)).to(dev)
     p1 = torch.from_numpy(synth.well_conditioned(lin.n1, seed=0, tag="p1")).to(dev)
