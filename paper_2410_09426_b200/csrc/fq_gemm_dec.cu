@@ -118,6 +118,24 @@ constexpr int TMEM_COLS = TMEMW ? 256 : 64;
 constexpr int MAX_SPLIT = 8;                  // portable cluster size
 constexpr size_t SMEM_BYTES = size_t(STAGES) * W_BYTES + size_t(PSTAGES) * P_BYTES + 1024 + 256;
 static_assert(RED_BYTES <= STAGES * W_BYTES, "the partial tile reuses the widened-operand stages");
+
+// Two resident-CTA configurations, picked per shape at launch (round 2): CFG 0 -- two CTAs per SM,
+// 6 MMA stages, a 5-deep packed ring (the shapes with more feature blocks than SMs: gate/up); CFG 1
+// -- one CTA per SM, 4 MMA stages and a 14-deep packed ring (112 KB of weights in flight per CTA,
+// prefetched before the PDL wait): the decode GEMM streams weights at the rate its bytes in flight
+// allow (Little's law, ~1.3 us per round trip), and the shapes with few feature blocks cannot fill
+// two CTAs per SM under cluster residency limits.
+template <int CFG>
+struct DecCfg {
+  static constexpr int STAGES = CFG == 0 ? gd::STAGES : 4;
+  static constexpr int PSTAGES = CFG == 0 ? gd::PSTAGES : 14;
+  static constexpr int MINB = CFG == 0 ? FQ_DEC_MINB : 1;
+  static constexpr size_t SMEM = size_t(STAGES) * W_BYTES + size_t(PSTAGES) * P_BYTES + 1024 + 256;
+  static_assert(RED_BYTES <= STAGES * W_BYTES, "partial tile in the operand stages");
+  static_assert(!TMEMW || W_COL0 + STAGES * WT_COLS <= TMEM_COLS, "TMEM budget");
+  static_assert(SMEM * MINB <= 232448, "shared memory per SM");
+  static_assert(DB < PSTAGES, "batch within the packed ring");
+};
 static_assert(P_BYTES % 1024 == 0 && W_BYTES % 1024 == 0 && WW_BYTES % 1024 == 0, "1 KB alignment");
 static_assert(!TMEMW || (BK == 128 && W_COL0 + STAGES * WT_COLS <= TMEM_COLS), "TMEM budget");
 
@@ -153,12 +171,13 @@ FQ_DEVICE void convert_chunk(uint32_t src, uint32_t dst_rows, int row, int c, in
   tc::sts128(rowp + uint32_t(((2 * cc + 1) ^ (row & 7)) << 4), o[4], o[5], o[6], o[7]);
 }
 
-template <bool OUT_I32, bool BF16, bool ASYM>
-__global__ void __launch_bounds__(THREADS, FQ_DEC_MINB)
+template <int CFG, bool OUT_I32, bool BF16, bool ASYM>
+__global__ void __launch_bounds__(THREADS, DecCfg<CFG>::MINB)
 gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA,
                 const float* __restrict__ sa, int T, int TN, int K, const float* __restrict__ sw, int N,
                 void* __restrict__ yv, const int8_t* __restrict__ za, const int32_t* __restrict__ colsum,
                 int S, int pdl) {
+  constexpr int STAGES = DecCfg<CFG>::STAGES, PSTAGES = DecCfg<CFG>::PSTAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;                                        // widened stages [W 16 KB | A 8 KB]
@@ -228,8 +247,10 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
           tc::mbar_wait(&pfull[sp], (j / PSTAGES) & 1);
           const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES + WP_BYTES);
           const uint32_t dst = smem_u32(sW + size_t(st) * W_BYTES);
+#ifndef FQ_EXP_DEC_SKIPA          // (experiment build: activation conversion removed)
           for (int task = at; task < TN * CPR; task += A_CONV_THREADS)
             convert_chunk(src + uint32_t(task * 16), dst, task / CPR, task % CPR, AW_ATOM);
+#endif
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&pempty[sp]);
         }
@@ -295,6 +316,13 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
               tc::mbar_wait(&pfull[sp], (j / PSTAGES) & 1);
               const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES) + uint32_t(r * 64);
               uint32_t w[32];
+#ifdef FQ_EXP_DEC_SKIPW           // experiment build only: weight conversion removed
+              if (true) {
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&pempty[sp]);
+                continue;
+              }
+#endif
 #pragma unroll
               for (int c = 0; c < 4; ++c) {
                 const uint4 pk = tc::lds128(src + uint32_t((c ^ ((r >> 1) & 3)) << 4));
@@ -319,7 +347,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       } else {
         convert_a(threadIdx.x - (CONV_WARP0 + 4) * 32 + (EPI_CONV ? 128 : 0));
       }
-    } else
+    } else {
     for (int j = 0; j < nk; ++j) {
       const int sp = j % PSTAGES, st = j % STAGES;
       tc::mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1);
@@ -337,6 +365,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&full[st]);
       if (threadIdx.x == CONV_WARP0 * 32 && j < 36) dtrace(tslot, 40 + j);
+    }
     }
   } else if (warp == MMA_WARP) {
     // ======================= MMA issuer =======================
@@ -388,12 +417,28 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     if (threadIdx.x == EPI_WARP0 * 32) dtrace(tslot, 112);
     const int q = warp & 3, f = q * 32 + lane;
     int32_t* red = reinterpret_cast<int32_t*>(sW);           // [token][BM] (MMAs have finished)
-    for (int c = 0; c < TN / 16; ++c) {
-      uint32_t v[16];
-      tc::tmem_ld16(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(c * 16), v);
+    if constexpr (DecCfg<CFG>::MINB == 1) {
+      // all of this lane's accumulator columns in one TMEM round trip, then the stores (the
+      // one-CTA-per-SM configuration has the registers for it)
+      uint32_t v[TN_MAX];
+#pragma unroll
+      for (int c = 0; c < TN_MAX / 16; ++c)
+        if (c < TN / 16) tc::tmem_ld16(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(c * 16),
+                                       *reinterpret_cast<uint32_t(*)[16]>(v + c * 16));
       tc::tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 16; ++i) red[(c * 16 + i) * BM + f] = int32_t(v[i]);
+      for (int c = 0; c < TN_MAX / 16; ++c)
+        if (c < TN / 16)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) red[(c * 16 + i) * BM + f] = int32_t(v[c * 16 + i]);
+    } else {
+      for (int c = 0; c < TN / 16; ++c) {
+        uint32_t v[16];
+        tc::tmem_ld16(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(c * 16), v);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) red[(c * 16 + i) * BM + f] = int32_t(v[i]);
+      }
     }
   }
 
@@ -489,15 +534,16 @@ static int dec_policy() {                         // FQ_DEC_POLICY: testing aid 
 }
 
 // How many clusters of S CTAs the hardware keeps resident at once (cluster placement is bounded
-// by the GPC structure, not only by the per-SM limits); cached per S.
+// by the GPC structure, not only by the per-SM limits); cached per (configuration, S).
+template <int CFG>
 static int dec_max_clusters(const void* kern, int S) {
   static int cache[gd::MAX_SPLIT + 1] = {0};
-  if (S <= 1) return FQ_DEC_MINB * num_sms();
+  if (S <= 1) return gd::DecCfg<CFG>::MINB * num_sms();
   if (cache[S] > 0) return cache[S];
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(S * 64));
   cfg.blockDim = dim3(gd::THREADS);
-  cfg.dynamicSmemBytes = gd::SMEM_BYTES;
+  cfg.dynamicSmemBytes = gd::DecCfg<CFG>::SMEM;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = unsigned(S);
@@ -515,7 +561,7 @@ static int dec_max_clusters(const void* kern, int S) {
   int n = 0;
   if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
     cudaGetLastError();
-    n = FQ_DEC_MINB * num_sms() / S;
+    n = gd::DecCfg<CFG>::MINB * num_sms() / S;
   }
   cache[S] = n;
   return n;
@@ -523,24 +569,27 @@ static int dec_max_clusters(const void* kern, int S) {
 
 // Split: the largest S <= 8 (and <= the number of K-blocks) for which every cluster of the grid
 // is resident at once; shapes with more feature blocks than that run unsplit.
+template <int CFG>
 static int dec_pick_split(const void* kern, int N, int K) {
   const int fbs = (N + gd::BM - 1) / gd::BM;
   const int nkb = (K + gd::BK - 1) / gd::BK;
   int s = 1;
   for (int c = 2; c <= gd::MAX_SPLIT && c <= nkb; ++c)
-    if (fbs * c <= FQ_DEC_MINB * num_sms() && fbs <= dec_max_clusters(kern, c)) s = c;
+    if (fbs * c <= gd::DecCfg<CFG>::MINB * num_sms() && fbs <= dec_max_clusters<CFG>(kern, c)) s = c;
   return s;
 }
 
-cudaError_t gemm_dec_launch(const GemmArgs& a, int split) {
+template <int CFG>
+static cudaError_t dec_launch_cfg(const GemmArgs& a, int split) {
   using namespace gd;
+  using DC = DecCfg<CFG>;
   const bool asym = a.za != nullptr && !a.out_i32;
-  auto kern = a.out_i32 ? gemm_dec_kernel<true, false, false>
-              : asym    ? (a.y_bf16 ? gemm_dec_kernel<false, true, true> : gemm_dec_kernel<false, false, true>)
-                        : (a.y_bf16 ? gemm_dec_kernel<false, true, false> : gemm_dec_kernel<false, false, false>);
+  auto kern = a.out_i32 ? gemm_dec_kernel<CFG, true, false, false>
+              : asym    ? (a.y_bf16 ? gemm_dec_kernel<CFG, false, true, true> : gemm_dec_kernel<CFG, false, false, true>)
+                        : (a.y_bf16 ? gemm_dec_kernel<CFG, false, true, false> : gemm_dec_kernel<CFG, false, false, false>);
   static std::atomic<uint64_t> attr_done[5];   // per kernel variant: devices configured
   const int which = a.out_i32 ? 0 : (a.y_bf16 ? 1 : 2) + (asym ? 2 : 0);
-  if (cudaError_t e = ensure_smem_attr(kern, int(SMEM_BYTES), attr_done[which]); e != cudaSuccess) return e;
+  if (cudaError_t e = ensure_smem_attr(kern, int(DC::SMEM), attr_done[which]); e != cudaSuccess) return e;
   const int TN = int((a.T + 15) / 16) * 16;
   CUtensorMap mw{}, ma{};
   {
@@ -557,24 +606,36 @@ cudaError_t gemm_dec_launch(const GemmArgs& a, int split) {
     if (!tmap_encode(&ma, a.qa, 1, 2, dims, strides, box, TMAP_SW_NONE)) return cudaErrorInvalidValue;
   }
   const int nkb = (a.K + BK - 1) / BK;
-  static const int env_split = [] {                 // FQ_DEC_SPLIT: testing aid (forces S)
-    const char* v = std::getenv("FQ_DEC_SPLIT");
-    return v ? std::atoi(v) : 0;
-  }();
-  if (split <= 0) split = env_split;
-  int S = split > 0 ? split : dec_pick_split(reinterpret_cast<const void*>(kern), a.N, a.K);
+  int S = split > 0 ? split : dec_pick_split<CFG>(reinterpret_cast<const void*>(kern), a.N, a.K);
   S = std::max(1, std::min({S, MAX_SPLIT, nkb}));
   const int fbs = (a.N + BM - 1) / BM;
   static const bool dbg = std::getenv("FQ_DEC_DEBUG") != nullptr;
   if (dbg)
-    std::fprintf(stderr, "[fq] decode GEMM N=%d K=%d T=%lld: split %d, %d CTAs, max resident clusters %d\n", a.N,
-                 a.K, (long long)a.T, S, fbs * S, dec_max_clusters(reinterpret_cast<const void*>(kern), S));
-  cudaError_t e = launch_pdl_policy(kern, dim3(unsigned(fbs * S)), dim3(THREADS), SMEM_BYTES, a.stream, S,
+    std::fprintf(stderr, "[fq] decode GEMM N=%d K=%d T=%lld: config %d, split %d, %d CTAs, max resident clusters %d\n",
+                 a.N, a.K, (long long)a.T, CFG, S, fbs * S,
+                 dec_max_clusters<CFG>(reinterpret_cast<const void*>(kern), S));
+  cudaError_t e = launch_pdl_policy(kern, dim3(unsigned(fbs * S)), dim3(THREADS), DC::SMEM, a.stream, S,
                                     dec_policy(), mw, ma, a.sa, int(a.T), TN, a.K, a.sw, a.N, a.y, a.za, a.colsum, S,
                                     a.pdl);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+cudaError_t gemm_dec_launch(const GemmArgs& a, int split) {
+  static const int env_split = [] {                 // FQ_DEC_SPLIT: testing aid (forces S)
+    const char* v = std::getenv("FQ_DEC_SPLIT");
+    return v ? std::atoi(v) : 0;
+  }();
+  static const int env_cfg = [] {                   // FQ_DEC_CFG: testing aid (forces 0 or 1)
+    const char* v = std::getenv("FQ_DEC_CFG");
+    return v ? std::atoi(v) : -1;
+  }();
+  if (split <= 0) split = env_split;
+  const int fbs = (a.N + gd::BM - 1) / gd::BM;
+  // one CTA per SM with the deep ring whenever every feature block gets its own SM
+  const bool deep = env_cfg >= 0 ? env_cfg == 1 : (fbs <= num_sms());
+  return deep ? dec_launch_cfg<1>(a, split) : dec_launch_cfg<0>(a, split);
 }
 
 }  // namespace fq
