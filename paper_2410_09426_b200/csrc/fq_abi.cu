@@ -296,6 +296,47 @@ static fq_status validate_linear(const void* x, int32_t x_dtype, int64_t T, int3
   if (!aligned16(sw)) return FQ_ESHAPE;
   return FQ_OK;
 }
+
+bool fused_enabled() {                             // FQ_FUSED=0: testing aid (two kernels always)
+  static const bool on = [] {
+    const char* e = std::getenv("FQ_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// one launch for the whole linear (transform + quantize + GEMM + dequant) where a fused kernel
+// exists: FQ_ENOTSUP (nothing enqueued) otherwise
+static fq_status run_fused(const void* x, int32_t x_dtype, int64_t T, int32_t n1, int32_t n2, const void* p1,
+                           const void* p2, float alpha, const uint8_t* qw, const float* sw, int32_t N, void* y,
+                           bool y_bf16, uint8_t* q_ws, float* s_ws, void* stream) {
+  const int64_t n = int64_t(n1) * n2;
+  GemmArgs a{};
+  a.qa = q_ws;
+  a.sa = s_ws;
+  a.T = T;
+  a.K = int32_t(n);
+  a.qw = qw;
+  a.sw = sw;
+  a.N = N;
+  a.y = y;
+  a.y_bf16 = y_bf16;
+  a.stream = static_cast<cudaStream_t>(stream);
+  if (!fused_dec_supported(a, n1, n2, x_dtype == FQ_BF16, p2)) return FQ_ENOTSUP;
+  FdArgs f{x, n, p1, p2, alpha};
+  const Span sqw = span(qw, size_t(N) * size_t(n / 2)), ssw = span(sw, size_t(N) * 4);
+  const Span sp1 = span(p1, size_t(n1) * n1 * 2), sp2 = span(p2, size_t(n2) * n2 * 2);
+  const Span sx = span(x, size_t(T) * size_t(n) * 2);
+  const Span sq = span(q_ws, size_t(T) * size_t(n / 2)), ss = span(s_ws, size_t(T) * 4);
+  const Span sy = span(y, size_t(T) * size_t(N) * 2);
+  a.pdl = pdl_flags(a.stream, {sqw, ssw, sp1, sp2}, {sx}, {sq, ss, sy});
+  const cudaError_t e = fused_dec_launch(a, f);
+  if (e == cudaErrorNotSupported) return FQ_ENOTSUP;
+  const fq_status s = cuda_status(e);
+  if (s == FQ_OK) record_launch(a.stream, true, {sqw, ssw, sp1, sp2, sx}, {sq, ss, sy});
+  return s;
+}
+
 }  // namespace fq
 
 extern "C" {
@@ -306,6 +347,12 @@ fq_status fq_flatquant_linear(const void* x, int32_t x_dtype, int64_t T, int32_t
   fq_status s = validate_linear(x, x_dtype, T, n1, n2, p1, p2, alpha, qw, sw, N, y, y_dtype, q_ws, s_ws);
   if (s != FQ_OK || T == 0 || N == 0) return s;
   const int64_t n = int64_t(n1) * n2;
+  if (fused_enabled() && g_gemm_impl.load() == 0 && g_tq_impl.load() == 0) {
+    // decode sizes: the transform runs inside the GEMM launch (NEXT-4(i)); FQ_ENOTSUP-free
+    // fallback to the two kernels below when the shape has no fused kernel
+    s = run_fused(x, x_dtype, T, n1, n2, p1, p2, alpha, qw, sw, N, y, y_dtype == FQ_BF16, q_ws, s_ws, stream);
+    if (s != FQ_ENOTSUP) return s;
+  }
   s = run_tq(x, x_dtype, T, n, n1, n2, p1, p2, alpha, q_ws, s_ws, nullptr, nullptr, stream);
   if (s != FQ_OK) return s;
   return run_gemm(q_ws, s_ws, T, int32_t(n), qw, sw, N, y, y_dtype == FQ_BF16, false, stream);

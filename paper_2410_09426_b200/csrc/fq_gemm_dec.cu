@@ -32,6 +32,7 @@
 #include "fq_device.cuh"
 #include "fq_internal.h"
 #include "fq_tc05.cuh"
+#include "fq_quant.cuh"
 
 namespace fq {
 namespace gd {
@@ -125,13 +126,16 @@ static_assert(RED_BYTES <= STAGES * W_BYTES, "the partial tile reuses the widene
 // prefetched before the PDL wait): the decode GEMM streams weights at the rate its bytes in flight
 // allow (Little's law, ~1.3 us per round trip), and the shapes with few feature blocks cannot fill
 // two CTAs per SM under cluster residency limits.
-template <int CFG>
+template <int CFG, bool FUSED = false>
 struct DecCfg {
-  static constexpr int STAGES = CFG == 0 ? gd::STAGES : 4;
+  // FUSED: the transform tile of phase A borrows the widened-operand stages (48 KB), so the
+  // one-CTA-per-SM configuration keeps 6 of them (TMEM: 64 + 6 x 32 columns)
+  static constexpr int STAGES = CFG == 0 ? gd::STAGES : (FUSED ? 6 : 4);
   static constexpr int PSTAGES = CFG == 0 ? gd::PSTAGES : 14;
   static constexpr int MINB = CFG == 0 ? FQ_DEC_MINB : 1;
-  static constexpr size_t SMEM = size_t(STAGES) * W_BYTES + size_t(PSTAGES) * P_BYTES + 1024 + 256;
+  static constexpr size_t SMEM = size_t(STAGES) * W_BYTES + size_t(PSTAGES) * P_BYTES + 1024 + (FUSED ? 512 : 256);
   static_assert(RED_BYTES <= STAGES * W_BYTES, "partial tile in the operand stages");
+  static_assert(!FUSED || STAGES * W_BYTES >= 48 * 1024, "phase-A transform tile in the operand stages");
   static_assert(!TMEMW || W_COL0 + STAGES * WT_COLS <= TMEM_COLS, "TMEM budget");
   static_assert(SMEM * MINB <= 232448, "shared memory per SM");
   static_assert(DB < PSTAGES, "batch within the packed ring");
@@ -171,13 +175,49 @@ FQ_DEVICE void convert_chunk(uint32_t src, uint32_t dst_rows, int row, int c, in
   tc::sts128(rowp + uint32_t(((2 * cc + 1) ^ (row & 7)) << 4), o[4], o[5], o[6], o[7]);
 }
 
-template <int CFG, bool OUT_I32, bool BF16, bool ASYM>
-__global__ void __launch_bounds__(THREADS, DecCfg<CFG>::MINB)
+// ---- fused decode linear (NEXT-4(i)): transform + quantize inside the GEMM launch ----
+// The first `ntiles` CTAs of the grid ("ticket" CTAs) each transform one two-token tile
+// (n1 = n2 = 64: Y_t = P1^T V_t P2, Eq.3) exactly as fq_tq_tc05.cu's kernel does
+// (same tcgen05 MMAs, same fp16 intermediate with the power-of-two prescale, same quantizer from
+// fq_quant.cuh), write the codes and scales to the caller's workspace (L2-resident at decode
+// sizes), and count themselves into a per-launch counter; every CTA streams its weight slice from
+// the start of the kernel and loads the activation codes once the count is complete.  The
+// counter pair (arrivals, departures) lives in a ring of slots in this module's device memory
+// and is reset by the last CTA to leave, so a slot is reusable by a later launch (and by a CUDA
+// graph replay).  Ticket CTAs are the lowest block indices and the grid is sized to be resident
+// at once (dec_pick_split), so the tickets can always run.
+constexpr int FD_SLOTS = 1024;
+__device__ unsigned g_fd_sync[2 * FD_SLOTS];
+
+struct alignas(64) FdParams {
+  CUtensorMap tmX, tmP1, tmP2;   // x [T][64][64] (box 64 x 64 x 2 tokens), P1, P2 [64][64] (SWIZZLE_128B)
+  float alpha;
+  uint8_t* q;                    // [T, 2048] packed codes (the caller's q_ws)
+  float* s;                      // [T] scales (s_ws)
+  unsigned* sync;                // {arrivals, departures} of this launch's slot
+  int ntiles;                    // ticket CTAs = ceil(T / 2)
+};
+constexpr int FD_N = 64;                                  // n1 = n2 = 64
+constexpr int FD_X_BYTES = 2 * FD_N * 128, FD_P_BYTES = FD_N * 128, FD_A2_BYTES = 2 * FD_N * 128;
+constexpr uint32_t FD_IDESC = tc::idesc_f16(128, FD_N, 0, 1, 1);   // fp16 x fp16 -> fp32, both MN-major
+
+FQ_DEVICE unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+FQ_DEVICE void red_release_gpu_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+FQ_DEVICE void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
+
+template <int CFG, bool OUT_I32, bool BF16, bool ASYM, bool FUSED = false>
+__global__ void __launch_bounds__(THREADS, DecCfg<CFG, FUSED>::MINB)
 gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA,
                 const float* __restrict__ sa, int T, int TN, int K, const float* __restrict__ sw, int N,
                 void* __restrict__ yv, const int8_t* __restrict__ za, const int32_t* __restrict__ colsum,
-                int S, int pdl) {
-  constexpr int STAGES = DecCfg<CFG>::STAGES, PSTAGES = DecCfg<CFG>::PSTAGES;
+                int S, int pdl, const __grid_constant__ FdParams fd) {
+  constexpr int STAGES = DecCfg<CFG, FUSED>::STAGES, PSTAGES = DecCfg<CFG, FUSED>::PSTAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;                                        // widened stages [W 16 KB | A 8 KB]
@@ -188,7 +228,19 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   uint64_t* pfull = bars + 2 * STAGES;     // [PSTAGES] TMA -> converters
   uint64_t* pempty = pfull + PSTAGES;      // [PSTAGES] converter warps -> TMA
   uint64_t* tfull = pempty + PSTAGES;      // [1]       last MMA commit -> partial-tile warps
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* fdx = tfull + 1;               // FUSED: X tile + P1 + P2 landed (ticket CTAs)
+  uint64_t* fd1 = fdx + 1;                 //        stage-1 MMA commit -> epilogue warps
+  uint64_t* fda2 = fd1 + 1;                //        stage-1 epilogue (4 warps) -> stage-2 MMA
+  uint64_t* fd2 = fda2 + 1;                //        stage-2 MMA commit -> epilogue warps
+  uint64_t* actready = fd2 + 1;            //        all tickets counted: codes and scales visible
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1 + (FUSED ? 5 : 0));
+  // FUSED phase A borrows the widened-operand stages: X tile | P1 | P2 | stage-2 A operand
+  uint8_t* fsX = sW;
+  uint8_t* fsP1 = sW + FD_X_BYTES;
+  uint8_t* fsP2 = fsP1 + FD_P_BYTES;
+  uint8_t* fsA2 = fsP2 + FD_P_BYTES;
+  __shared__ float fd_red[8];                                // [2 parities][4 warps] token maxima
+  const bool ticket = FUSED && int(blockIdx.x) < fd.ntiles;
   __shared__ float s_sa[TN_MAX];                             // sa[t] / 256 (0 past T)
   __shared__ int s_za[TN_MAX];                               // 256 (z_t - 8) (asymmetric)
   __shared__ __align__(16) float s_sw[BM];                  // sw of this feature block
@@ -219,9 +271,21 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       tc::mbar_init(&pempty[s], NUM_ARRIVE);
     }
     tc::mbar_init(tfull, 1);
+    if constexpr (FUSED) {
+      tc::mbar_init(fdx, 1);
+      tc::mbar_init(fd1, 1);
+      tc::mbar_init(fda2, 4);
+      tc::mbar_init(fd2, 1);
+      tc::mbar_init(actready, 1);
+    }
     tc::fence_barrier_init();
     tc::tma_prefetch_desc(&tmW);
     tc::tma_prefetch_desc(&tmA);
+    if (ticket) {
+      tc::tma_prefetch_desc(&fd.tmX);
+      tc::tma_prefetch_desc(&fd.tmP1);
+      tc::tma_prefetch_desc(&fd.tmP2);
+    }
   }
   if (warp == ALLOC_WARP) tc::tmem_alloc(tmem_slot, TMEM_COLS);
   tc::fence_before();
@@ -266,6 +330,16 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   if (warp == TMA_WARP) {
     // ======================= TMA producer =======================
     if (lane == 0) {
+      if constexpr (FUSED) {
+        if (ticket) {
+          // phase A first: this CTA's two tokens, P1 and P2 (x is an activation, P1/P2 parameters)
+          if ((pdl & (PDL_P | PDL_X)) != (PDL_P | PDL_X)) tc::griddep_wait();
+          tc::mbar_expect_tx(fdx, uint32_t(FD_X_BYTES + 2 * FD_P_BYTES));
+          tc::tma_load_3d(fsX, &fd.tmX, fdx, 0, 0, 2 * int(blockIdx.x));
+          tc::tma_load_2d(fsP1, &fd.tmP1, fdx, 0, 0);
+          tc::tma_load_2d(fsP2, &fd.tmP2, fdx, 0, 0);
+        }
+      }
       // the weights are parameters: unless the preceding kernel of the stream writes them
       // (host-side hazard check, fq_abi.cu), start streaming them before the wait
       if (!(pdl & PDL_P)) tc::griddep_wait();
@@ -280,7 +354,24 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         tc::mbar_expect_tx(&pfull[j], uint32_t(WP_BYTES + ap_bytes));
         tc::tma_load_2d(sP + size_t(j) * P_BYTES, &tmW, &pfull[j], kb_of(j) * (BK / 2), fb * BM);
       }
-      if (!(pdl & PDL_X)) tc::griddep_wait();    // qa written by the transform kernel is visible
+      if constexpr (FUSED) {
+        // every ticket CTA has stored its codes and scales (release/acquire at GPU scope); the
+        // activation codes are then read through the async proxy (TMA)
+        const unsigned need = unsigned(fd.ntiles);
+        const long long t_start = clock64();
+        while (ld_acquire_gpu(fd.sync) < need) {
+          if (clock64() - t_start > (1ll << 32)) __trap();    // never hang the GPU: ~2 s without progress
+        }
+        fence_proxy_async_global();
+        tc::mbar_arrive(actready);
+        // last CTA out resets the slot for its next launch (all arrivals have been counted)
+        if (atomicAdd(fd.sync + 1, 1u) == gridDim.x - 1) {
+          atomicExch(fd.sync, 0u);
+          atomicExch(fd.sync + 1, 0u);
+        }
+      } else if (!(pdl & PDL_X)) {
+        tc::griddep_wait();                      // qa written by the transform kernel is visible
+      }
       for (int j = 0; j < pre; ++j)
         tc::tma_load_2d(sP + size_t(j) * P_BYTES + WP_BYTES, &tmA, &pfull[j], kb_of(j) * (BK / 2), 0);
       for (int j = pre; j < nk; ++j) {
@@ -370,6 +461,27 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   } else if (warp == MMA_WARP) {
     // ======================= MMA issuer =======================
     if (lane == 0) {
+      if (ticket) {
+        // phase A (fq_tq_tc05.cu, n1 = n2 = 64, two tokens = M 128): D = X^T P1 into the accumulator
+        // columns [0, 64) (unused until the first GEMM MMA, which comes after every ticket's
+        // epilogue has read them), then D = W P2 into the same columns once the stage-1 epilogue
+        // has read D and written W (fp16) to shared memory
+        tc::mbar_wait(fdx, 0);
+        tc::fence_after();
+        const uint32_t xs = smem_u32(fsX), p1a = smem_u32(fsP1), p2a = smem_u32(fsP2), a2 = smem_u32(fsA2);
+#pragma unroll
+        for (int kk = 0; kk < FD_N / 16; ++kk)
+          tc::mma_ss<false>(tmem_base, tc::sdesc_sw128(xs + kk * 2048, FD_N * 128, 1024),
+                            tc::sdesc_sw128(p1a + kk * 2048, FD_N * 128, 1024), FD_IDESC, kk > 0);
+        tc::mma_commit(fd1);
+        tc::mbar_wait(fda2, 0);
+        tc::fence_after();
+#pragma unroll
+        for (int kk = 0; kk < FD_N / 16; ++kk)
+          tc::mma_ss<false>(tmem_base, tc::sdesc_sw128(a2 + kk * 2048, FD_N * 128, 1024),
+                            tc::sdesc_sw128(p2a + kk * 2048, FD_N * 128, 1024), FD_IDESC, kk > 0);
+        tc::mma_commit(fd2);
+      }
       for (int j = 0; j < nk; ++j) {
         const int st = j % STAGES;
         tc::mbar_wait(&full[st], (j / STAGES) & 1);
@@ -396,6 +508,106 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     __syncwarp();
   } else if (warp >= EPI_WARP0) {
     // ======================= TMEM -> shared-memory partial tile =======================
+    if constexpr (FUSED) {
+      if (ticket) {
+        // ---- phase A epilogues (fq_tq_tc05.cu's, one group of 4 warps, 16-column TMEM chunks) ----
+        const int qd = warp & 3, L = qd * 32 + lane;
+        const uint32_t lb = tmem_base + (uint32_t(qd * 32) << 16);
+        int rp = 0;
+        auto exchange = [&](float m) {                     // per-warp max -> the 4 warps' maxima
+          m = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(m)));   // m >= 0
+          if (lane == 0) fd_red[rp * 4 + qd] = m;
+          named_bar_sync(1, 128);
+          const float4 r = make_float4(fd_red[rp * 4 + 0], fd_red[rp * 4 + 1], fd_red[rp * 4 + 2], fd_red[rp * 4 + 3]);
+          rp ^= 1;
+          return r;
+        };
+        auto ld16 = [&](int c, uint32_t(&v)[16]) {
+          tc::tmem_ld16(lb + uint32_t(c), v);
+          tc::tmem_ld_wait();
+        };
+        // stage 1: D lane (t, j), column i = W_t[i][j]; token t = L / 64
+        tc::mbar_wait(fd1, 0);
+        tc::fence_after();
+        float m1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < FD_N; c += 16) {
+          uint32_t v[16];
+          ld16(c, v);
+#pragma unroll
+          for (int e = 0; e < 16; e += 2)
+            m1 = qz::max3f(m1, fabsf(__uint_as_float(v[e])), fabsf(__uint_as_float(v[e + 1])));
+        }
+        const float4 r1 = exchange(m1);
+        const int pe0 = qz::prescale_exp(fmaxf(r1.x, r1.y)), pe1 = qz::prescale_exp(fmaxf(r1.z, r1.w));
+        const int tt = L >> 6;
+        const float pre = qz::exp2i(tt ? pe1 : pe0);
+        {
+          const int j = L & 63;                            // K row j' of the stage-2 A operand
+          const uint32_t row = smem_u32(fsA2) + uint32_t(tt * (FD_N * 128) + j * 128);
+#pragma unroll
+          for (int c = 0; c < FD_N; c += 16) {
+            uint32_t v[16];
+            ld16(c, v);
+#pragma unroll
+            for (int e = 0; e < 16; e += 8) {
+              const int ch = ((c + e) >> 3) & 7;
+              tc::sts128(row + uint32_t((ch ^ (j & 7)) << 4),
+                         pack_half2(__uint_as_float(v[e + 0]) * pre, __uint_as_float(v[e + 1]) * pre),
+                         pack_half2(__uint_as_float(v[e + 2]) * pre, __uint_as_float(v[e + 3]) * pre),
+                         pack_half2(__uint_as_float(v[e + 4]) * pre, __uint_as_float(v[e + 5]) * pre),
+                         pack_half2(__uint_as_float(v[e + 6]) * pre, __uint_as_float(v[e + 7]) * pre));
+            }
+          }
+        }
+        tc::fence_proxy_async_smem();
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(fda2);
+        // stage 2: D lane (t, i), column j = Y_t[i][j] (prescaled by 2^pe)
+        tc::mbar_wait(fd2, 0);
+        tc::fence_after();
+        float m2 = 0.f;
+#pragma unroll
+        for (int c = 0; c < FD_N; c += 16) {
+          uint32_t v[16];
+          ld16(c, v);
+#pragma unroll
+          for (int e = 0; e < 16; e += 2)
+            m2 = qz::max3f(m2, fabsf(__uint_as_float(v[e])), fabsf(__uint_as_float(v[e + 1])));
+        }
+        const float4 r2 = exchange(m2);
+        const float mp = tt == 0 ? fmaxf(r2.x, r2.y) : fmaxf(r2.z, r2.w);
+        const int t = 2 * int(blockIdx.x) + tt, i = L & 63;
+        const bool store = t < T;
+        const float inv_pre = qz::exp2i(-(tt ? pe1 : pe0));
+        const float c15 = qz::sym_c15(fd.alpha, mp);
+        if (!(pdl & PDL_OUT)) tc::griddep_wait();          // the predecessor no longer reads q_ws / s_ws
+        uint8_t* qrow = fd.q + (store ? size_t(t) * (FD_N * FD_N / 2) + size_t(i) * (FD_N / 2) : 0);
+#pragma unroll
+        for (int c = 0; c < FD_N; c += 32) {
+          uint32_t v[32];
+          tc::tmem_ld16(lb + uint32_t(c), *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+          tc::tmem_ld16(lb + uint32_t(c + 16), *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+          tc::tmem_ld_wait();
+          uint32_t w[4];
+#pragma unroll
+          for (int c8 = 0; c8 < 4; ++c8) {
+            float z[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) z[e] = qz::sym_code(__uint_as_float(v[8 * c8 + e]), c15);
+            w[c8] = qz::pack8(z);
+          }
+          if (store) *reinterpret_cast<uint4*>(qrow + c / 2) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        if (store && i == 0) fd.s[t] = mp > 0.f ? fd.alpha * (mp * inv_pre) / 7.0f : 1.0f;
+        __threadfence();                                   // codes and scale visible GPU-wide ...
+        fence_proxy_async_global();                        // ... and to the consumers' TMA loads
+        tc::fence_before();
+        named_bar_sync(1, 128);
+        if (L == 0) red_release_gpu_add(fd.sync, 1u);      // this tile is done
+      }
+    }
     // while the main loop runs: stage the epilogue's scales in shared memory
     tc::griddep_wait();
     if (threadIdx.x == EPI_WARP0 * 32) tc::griddep_launch();   // only after the wait (fq_internal.h)
@@ -406,7 +618,8 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         s_sw[e] = o < N ? __ldg(sw + o) : 0.f;
         if constexpr (ASYM) s_cs[e] = o < N ? __ldg(colsum + o) : 0;
         if (e < TN_MAX) {
-          s_sa[e] = e < T ? sa[e] * (ASYM ? 1.0f : 1.0f / 256.0f) : 0.f;
+          if constexpr (FUSED) tc::mbar_wait(actready, 0);     // the scales come from the tickets
+          s_sa[e] = e < T ? (FUSED ? __ldcg(sa + e) : sa[e]) * (ASYM ? 1.0f : 1.0f / 256.0f) : 0.f;
           if constexpr (ASYM) s_za[e] = e < T ? int(za[e]) : 0;
         }
       }
@@ -535,15 +748,15 @@ static int dec_policy() {                         // FQ_DEC_POLICY: testing aid 
 
 // How many clusters of S CTAs the hardware keeps resident at once (cluster placement is bounded
 // by the GPC structure, not only by the per-SM limits); cached per (configuration, S).
-template <int CFG>
+template <int CFG, bool FUSED>
 static int dec_max_clusters(const void* kern, int S) {
   static int cache[gd::MAX_SPLIT + 1] = {0};
-  if (S <= 1) return gd::DecCfg<CFG>::MINB * num_sms();
+  if (S <= 1) return gd::DecCfg<CFG, FUSED>::MINB * num_sms();
   if (cache[S] > 0) return cache[S];
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(S * 64));
   cfg.blockDim = dim3(gd::THREADS);
-  cfg.dynamicSmemBytes = gd::DecCfg<CFG>::SMEM;
+  cfg.dynamicSmemBytes = gd::DecCfg<CFG, FUSED>::SMEM;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = unsigned(S);
@@ -561,7 +774,7 @@ static int dec_max_clusters(const void* kern, int S) {
   int n = 0;
   if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
     cudaGetLastError();
-    n = gd::DecCfg<CFG>::MINB * num_sms() / S;
+    n = gd::DecCfg<CFG, FUSED>::MINB * num_sms() / S;
   }
   cache[S] = n;
   return n;
@@ -569,27 +782,43 @@ static int dec_max_clusters(const void* kern, int S) {
 
 // Split: the largest S <= 8 (and <= the number of K-blocks) for which every cluster of the grid
 // is resident at once; shapes with more feature blocks than that run unsplit.
-template <int CFG>
+template <int CFG, bool FUSED>
 static int dec_pick_split(const void* kern, int N, int K) {
   const int fbs = (N + gd::BM - 1) / gd::BM;
   const int nkb = (K + gd::BK - 1) / gd::BK;
   int s = 1;
   for (int c = 2; c <= gd::MAX_SPLIT && c <= nkb; ++c)
-    if (fbs * c <= gd::DecCfg<CFG>::MINB * num_sms() && fbs <= dec_max_clusters<CFG>(kern, c)) s = c;
+    if (fbs * c <= gd::DecCfg<CFG, FUSED>::MINB * num_sms() && fbs <= dec_max_clusters<CFG, FUSED>(kern, c)) s = c;
   return s;
 }
 
-template <int CFG>
-static cudaError_t dec_launch_cfg(const GemmArgs& a, int split) {
+// device address of this launch's {arrivals, departures} slot (FUSED); slots are handed out
+// round-robin per device, so up to FD_SLOTS fused launches may be in flight on a device at once
+static unsigned* fd_sync_slot() {
+  static unsigned* base[64] = {nullptr};
+  static std::atomic<uint32_t> next[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!base[dev]) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, gd::g_fd_sync) != cudaSuccess) return nullptr;
+    base[dev] = static_cast<unsigned*>(p);
+  }
+  return base[dev] + 2 * (next[dev].fetch_add(1, std::memory_order_relaxed) % gd::FD_SLOTS);
+}
+
+template <int CFG, bool FUSED>
+static cudaError_t dec_launch_cfg(const GemmArgs& a, int split, const FdArgs* f) {
   using namespace gd;
-  using DC = DecCfg<CFG>;
+  using DC = DecCfg<CFG, FUSED>;
   const bool asym = a.za != nullptr && !a.out_i32;
-  auto kern = a.out_i32 ? gemm_dec_kernel<CFG, true, false, false>
-              : asym    ? (a.y_bf16 ? gemm_dec_kernel<CFG, false, true, true> : gemm_dec_kernel<CFG, false, false, true>)
-                        : (a.y_bf16 ? gemm_dec_kernel<CFG, false, true, false> : gemm_dec_kernel<CFG, false, false, false>);
+  auto kern = a.out_i32 ? gemm_dec_kernel<CFG, true, false, false, FUSED>
+              : asym    ? (a.y_bf16 ? gemm_dec_kernel<CFG, false, true, true, FUSED>
+                                    : gemm_dec_kernel<CFG, false, false, true, FUSED>)
+                        : (a.y_bf16 ? gemm_dec_kernel<CFG, false, true, false, FUSED>
+                                    : gemm_dec_kernel<CFG, false, false, false, FUSED>);
   static std::atomic<uint64_t> attr_done[5];   // per kernel variant: devices configured
   const int which = a.out_i32 ? 0 : (a.y_bf16 ? 1 : 2) + (asym ? 2 : 0);
-  if (cudaError_t e = ensure_smem_attr(kern, int(DC::SMEM), attr_done[which]); e != cudaSuccess) return e;
   const int TN = int((a.T + 15) / 16) * 16;
   CUtensorMap mw{}, ma{};
   {
@@ -606,36 +835,73 @@ static cudaError_t dec_launch_cfg(const GemmArgs& a, int split) {
     if (!tmap_encode(&ma, a.qa, 1, 2, dims, strides, box, TMAP_SW_NONE)) return cudaErrorInvalidValue;
   }
   const int nkb = (a.K + BK - 1) / BK;
-  int S = split > 0 ? split : dec_pick_split<CFG>(reinterpret_cast<const void*>(kern), a.N, a.K);
+  int S = split > 0 ? split : dec_pick_split<CFG, FUSED>(reinterpret_cast<const void*>(kern), a.N, a.K);
   S = std::max(1, std::min({S, MAX_SPLIT, nkb}));
   const int fbs = (a.N + BM - 1) / BM;
+  FdParams fd{};
+  if constexpr (FUSED) {
+    // ticket CTAs: one per two-token tile, all within the (resident) grid
+    fd.ntiles = int((a.T + 1) / 2);
+    if (fbs * S < fd.ntiles) return cudaErrorNotSupported;      // caller falls back (nothing launched)
+    const uint64_t xd[3] = {uint64_t(FD_N), uint64_t(FD_N), uint64_t(a.T)};
+    const uint64_t xs[2] = {uint64_t(FD_N) * 2, uint64_t(f->ldx) * 2};
+    const uint32_t xb[3] = {64, uint32_t(FD_N), 2};
+    if (!tmap_encode(&fd.tmX, f->x, 2, 3, xd, xs, xb, TMAP_SW128)) return cudaErrorInvalidValue;
+    const uint64_t pd[2] = {uint64_t(FD_N), uint64_t(FD_N)};
+    const uint64_t ps[1] = {uint64_t(FD_N) * 2};
+    const uint32_t pb[2] = {64, uint32_t(FD_N)};
+    if (!tmap_encode(&fd.tmP1, f->p1, 2, 2, pd, ps, pb, TMAP_SW128)) return cudaErrorInvalidValue;
+    if (!tmap_encode(&fd.tmP2, f->p2, 2, 2, pd, ps, pb, TMAP_SW128)) return cudaErrorInvalidValue;
+    fd.alpha = f->alpha;
+    fd.q = const_cast<uint8_t*>(a.qa);
+    fd.s = const_cast<float*>(a.sa);
+    fd.sync = fd_sync_slot();
+    if (!fd.sync) return cudaErrorInvalidValue;
+  }
+  if (cudaError_t e = ensure_smem_attr(kern, int(DC::SMEM), attr_done[which]); e != cudaSuccess) return e;
   static const bool dbg = std::getenv("FQ_DEC_DEBUG") != nullptr;
   if (dbg)
-    std::fprintf(stderr, "[fq] decode GEMM N=%d K=%d T=%lld: config %d, split %d, %d CTAs, max resident clusters %d\n",
-                 a.N, a.K, (long long)a.T, CFG, S, fbs * S,
-                 dec_max_clusters<CFG>(reinterpret_cast<const void*>(kern), S));
+    std::fprintf(stderr, "[fq] decode GEMM%s N=%d K=%d T=%lld: config %d, split %d, %d CTAs, max resident clusters %d\n",
+                 FUSED ? " (fused transform)" : "", a.N, a.K, (long long)a.T, CFG, S, fbs * S,
+                 dec_max_clusters<CFG, FUSED>(reinterpret_cast<const void*>(kern), S));
   cudaError_t e = launch_pdl_policy(kern, dim3(unsigned(fbs * S)), dim3(THREADS), DC::SMEM, a.stream, S,
                                     dec_policy(), mw, ma, a.sa, int(a.T), TN, a.K, a.sw, a.N, a.y, a.za, a.colsum, S,
-                                    a.pdl);
+                                    a.pdl, fd);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
-cudaError_t gemm_dec_launch(const GemmArgs& a, int split) {
-  static const int env_split = [] {                 // FQ_DEC_SPLIT: testing aid (forces S)
-    const char* v = std::getenv("FQ_DEC_SPLIT");
-    return v ? std::atoi(v) : 0;
+static int dec_env_split() {                      // FQ_DEC_SPLIT: testing aid (forces S)
+  static const int v = [] {
+    const char* e = std::getenv("FQ_DEC_SPLIT");
+    return e ? std::atoi(e) : 0;
   }();
-  static const int env_cfg = [] {                   // FQ_DEC_CFG: testing aid (forces 0 or 1)
+  return v;
+}
+static bool dec_deep(const GemmArgs& a) {         // FQ_DEC_CFG: testing aid (forces 0 or 1)
+  static const int env_cfg = [] {
     const char* v = std::getenv("FQ_DEC_CFG");
     return v ? std::atoi(v) : -1;
   }();
-  if (split <= 0) split = env_split;
   const int fbs = (a.N + gd::BM - 1) / gd::BM;
   // one CTA per SM with the deep ring whenever every feature block gets its own SM
-  const bool deep = env_cfg >= 0 ? env_cfg == 1 : (fbs <= num_sms());
-  return deep ? dec_launch_cfg<1>(a, split) : dec_launch_cfg<0>(a, split);
+  return env_cfg >= 0 ? env_cfg == 1 : (fbs <= num_sms());
+}
+
+cudaError_t gemm_dec_launch(const GemmArgs& a, int split) {
+  if (split <= 0) split = dec_env_split();
+  return dec_deep(a) ? dec_launch_cfg<1, false>(a, split, nullptr) : dec_launch_cfg<0, false>(a, split, nullptr);
+}
+
+bool fused_dec_supported(const GemmArgs& a, int n1, int n2, bool x_bf16, const void* p2) {
+  return n1 == gd::FD_N && n2 == gd::FD_N && !x_bf16 && p2 != nullptr && a.za == nullptr && !a.out_i32 &&
+         gemm_dec_supported(a) && a.K == gd::FD_N * gd::FD_N;
+}
+
+cudaError_t fused_dec_launch(const GemmArgs& a, const FdArgs& f) {
+  const int split = dec_env_split();
+  return dec_deep(a) ? dec_launch_cfg<1, true>(a, split, &f) : dec_launch_cfg<0, true>(a, split, &f);
 }
 
 }  // namespace fq

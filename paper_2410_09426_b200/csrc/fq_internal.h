@@ -164,6 +164,19 @@ int gemm_pair_pick_bn(int64_t T, int N, int K, int clusters);
 cudaError_t gemm_dec_launch(const GemmArgs& a, int split = 0);  // decode (T <= 64): swapped operands,
 bool gemm_dec_supported(const GemmArgs& a);                     // cluster split-K; split 0 = per shape
 bool gemm_pair_supported(const GemmArgs& a);
+// fused decode linear (T <= 64, n1 = n2 = 64, fp16 x, P2 given, symmetric): the transform +
+// quantize of x (into the codes/scales buffers named by the GemmArgs) runs inside the decode GEMM
+// launch (fq_gemm_dec.cu, FUSED); cudaErrorNotSupported (nothing launched) when the grid for the
+// shape has fewer CTAs than two-token tiles
+struct FdArgs {
+  const void* x;
+  int64_t ldx;
+  const void* p1;
+  const void* p2;
+  float alpha;
+};
+bool fused_dec_supported(const GemmArgs& a, int n1, int n2, bool x_bf16, const void* p2);
+cudaError_t fused_dec_launch(const GemmArgs& a, const FdArgs& f);
 size_t weight_prep_workspace(int n1, int n2);
 cudaError_t inverse_t_launch(const void* p, int n, bool bf16, void* aug, void* out, int* status,
                              cudaStream_t stream);

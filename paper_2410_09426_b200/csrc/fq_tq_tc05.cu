@@ -34,6 +34,7 @@
 #include "fq_device.cuh"
 #include "fq_internal.h"
 #include "fq_tc05.cuh"
+#include "fq_quant.cuh"
 
 namespace fq {
 namespace tq5 {
@@ -106,29 +107,7 @@ struct Cfg {
   static_assert(STAGES >= 2, "shared-memory budget");
 };
 
-constexpr float MAGIC = 12582912.0f;   // 1.5 * 2^23: fma(y, c, MAGIC) rounds y*c half-to-even
-
-// per-token exact power-of-two exponent e with m * 2^e in [2^14, 2^15) (fp16-safe); m >= 0 and
-// finite.  A subnormal (or zero) m gets the largest scale 2^126.
-FQ_DEVICE int prescale_exp(float m) {
-  const int be = int(__float_as_uint(m) >> 23);       // biased exponent (sign bit is 0)
-  if (be == 0) return 126;
-  const int e = 14 - (be - 127);
-  return e < -126 ? -126 : (e > 126 ? 126 : e);
-}
-
-FQ_DEVICE float exp2i(int e) { return __int_as_float((127 + e) << 23); }
-
-FQ_DEVICE float max3f(float a, float b, float c) {   // FMNMX3 (sm_100); |.| folds into operand modifiers
-  float r;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-  return r;
-}
-FQ_DEVICE float fma_sat(float a, float b, float c) {  // FFMA.SAT: clamp to [0, 1]
-  float r;
-  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-  return r;
-}
+using namespace qz;   // MAGIC, prescale_exp, exp2i, max3f, fma_sat (fq_quant.cuh)
 
 // max |v[i]| over N values: 8 independent accumulators fed two values per 3-input max
 // (a running max would be a dependent chain of N operations)
@@ -185,16 +164,6 @@ FQ_DEVICE void row_chunks(uint32_t taddr, const uint32_t* regs, F&& fn) {
   } else {
     tmem_chunks<N>(taddr, fn);
   }
-}
-
-// 8 quantized values in MAGIC form (low nibble of the bit pattern = two's-complement code)
-// -> one 32-bit word, element 2m in the low nibble of byte m.
-FQ_DEVICE uint32_t pack8(const float (&v)[8]) {
-  const uint32_t e = __byte_perm(__byte_perm(__float_as_uint(v[0]), __float_as_uint(v[2]), 0x0040),
-                                 __byte_perm(__float_as_uint(v[4]), __float_as_uint(v[6]), 0x0040), 0x5410);
-  const uint32_t o = __byte_perm(__byte_perm(__float_as_uint(v[1]), __float_as_uint(v[3]), 0x0040),
-                                 __byte_perm(__float_as_uint(v[5]), __float_as_uint(v[7]), 0x0040), 0x5410);
-  return (e & 0x0F0F0F0Fu) | ((o << 4) & 0xF0F0F0F0u);
 }
 
 template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM, bool SMALL = false, bool IDENT2 = false>
