@@ -3,7 +3,9 @@
 
 One step = the whole hot path over one batch of synthetic tokens:
 for every linear of the configuration, fq_transform_quant (Kronecker transform + clip + INT4
-quantize/pack) followed by fq_w4a4_linear (tcgen05 W4A4 GEMM + dequant epilogue).
+quantize/pack) followed by fq_w4a4_linear (tcgen05 W4A4 GEMM + dequant epilogue) -- or, at decode
+sizes (T <= 64, 64 x 64 decomposition), fq_flatquant_linear, which runs both in ONE fused launch
+(NEXT-4(i); --no-fused keeps the two calls).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
 
@@ -78,6 +80,8 @@ def parse():
     ap.add_argument("--no-kv", action="store_true", help="skip the KV-cache quantization measurement")
     ap.add_argument("--no-verify", action="store_true", help="N > 1: skip the untimed all-gather check")
     ap.add_argument("--no-fig6", action="store_true", help="skip the per-transform in-step overhead steps")
+    ap.add_argument("--no-fused", action="store_true",
+                    help="decode: call fq_transform_quant + fq_w4a4_linear instead of the fused fq_flatquant_linear")
     return ap.parse_args()
 
 
@@ -198,6 +202,20 @@ def build_workload(cfg_name, rank, world, dev, torch, fq):
     return cfg, layers, T
 
 
+def fused_linear(T, lin):
+    """The library runs fq_flatquant_linear as ONE fused launch (transform + quantize inside the
+    decode GEMM, NEXT-4(i)) for T <= 64 with the 64 x 64 decomposition and fp16 activations
+    (fq_gemm_dec.cu FUSED); the bench checks this against its launch count."""
+    return T <= 64 and lin.n1 == 64 and lin.n2 == 64
+
+
+def fused_bytes(T, lin):
+    """Algorithmic bytes of one fused decode linear: the transform's (X in, codes + scales out to
+    the caller's workspace, P1, P2) plus the GEMM's weights, weight scales and output; the codes are
+    read back from L2 inside the launch, so they count once."""
+    return tq_bytes(T, lin) + gemm_min_bytes(T, lin) - (T * lin.K // 2 + 4 * T)
+
+
 def tq_bytes(T, lin):
     return T * (2 * lin.K + lin.K // 2 + 4) + 2 * (lin.n1 ** 2 + lin.n2 ** 2)
 
@@ -313,9 +331,20 @@ def run_ours(args):
         torch.sum(flush, dim=0, out=flush_sum)
         torch.cuda._sleep(400_000)    # lets the host enqueue the whole step before the GPU reaches it
 
+    fused = [not args.no_fused and fused_linear(T, L["lin"]) for L in layers]
+
     def step(evs=None, tq_mask=None, gemm=True, po_paper=None):
         for i, L in enumerate(layers):
             lin = L["lin"]
+            if fused[i] and gemm and (tq_mask is None or tq_mask[i]) and po_paper is None:
+                # the whole linear in one launch (events around it in the GEMM slot)
+                if evs is not None:
+                    evs[2 * i + 1][0].record(stream)
+                fq.fq_flatquant_linear(L["x"], lin.n1, lin.n2, L["p1"], L["p2"], args.alpha, L["qw"], L["sw"],
+                                       L["y"], L["q"], L["s"])
+                if evs is not None:
+                    evs[2 * i + 1][1].record(stream)
+                continue
             if tq_mask is None or tq_mask[i]:
                 if evs is not None:
                     evs[2 * i][0].record(stream)
@@ -344,7 +373,10 @@ def run_ours(args):
         return sharding.max_over_ranks(v, dev)
 
     def timed_steps(n, **kw):
-        """n steps, L2 flushed before each (flush untimed); returns the summed step time (ms)."""
+        """n steps, L2 flushed before each (flush untimed); returns the summed step time (ms).
+        One untimed step first: a variant's first launches pay one-time host costs (kernel
+        attributes, occupancy queries) that the device sleep after the flush does not cover."""
+        step(**kw)
         tot = 0.0
         for _ in range(n):
             flush_l2()
@@ -387,6 +419,8 @@ def run_ours(args):
         step(evs)
         torch.cuda.synchronize()
         for k, (ea, eb) in enumerate(evs):
+            if k % 2 == 0 and fused[k // 2]:
+                continue                                 # fused linear: one launch, in the GEMM slot
             per_kernel[k][0] += ea.elapsed_time(eb)
             per_kernel[k][1] += 1
     barrier()
@@ -413,16 +447,23 @@ def run_ours(args):
     gemm_ms = sum(per_kernel[2 * i + 1][0] for i in range(len(layers))) / args.steps
     tq_ms = sum(per_kernel[2 * i][0] for i in range(len(layers))) / args.steps
     g_ops = sum(gemm_ops(T, L["lin"]) for L in layers)
-    t_bytes = sum(tq_bytes(T, L["lin"]) for L in layers)
-    t_flops = sum(tq_flops(T, L["lin"]) for L in layers)
+    t_bytes = sum(tq_bytes(T, L["lin"]) for i, L in enumerate(layers) if not fused[i])
+    t_flops = sum(tq_flops(T, L["lin"]) for i, L in enumerate(layers) if not fused[i])
     int8_peak, int8_src, int8_alt = int8_peak_tops(pk, peak_src)
     gemm_tops = g_ops / (gemm_ms * 1e-3) / 1e12
-    tq_gbs = t_bytes / (tq_ms * 1e-3) / 1e9
+    tq_gbs = t_bytes / (tq_ms * 1e-3) / 1e9 if tq_ms > 0 else 0.0
     kernels = {}
     for i, L in enumerate(layers):
         lin = L["lin"]
         tq_i = per_kernel[2 * i][0] / args.steps
         gm_i = per_kernel[2 * i + 1][0] / args.steps
+        if fused[i]:
+            kernels[lin.name] = {
+                "n1xn2": f"{lin.n1}x{lin.n2}", "N": lin.N, "fused": True,
+                "linear_us": round(gm_i * 1e3, 2), "linear_gbs": round(fused_bytes(T, lin) / (gm_i * 1e-3) / 1e9, 1),
+                "gemm_tops": round(gemm_ops(T, lin) / (gm_i * 1e-3) / 1e12, 1),
+                "note": "fq_flatquant_linear: transform + quantize + GEMM + dequant in one launch"}
+            continue
         kernels[lin.name] = {
             "n1xn2": f"{lin.n1}x{lin.n2}", "N": lin.N,
             "tq_us": round(tq_i * 1e3, 2), "tq_gbs": round(tq_bytes(T, lin) / (tq_i * 1e-3) / 1e9, 1),
@@ -590,13 +631,19 @@ def run_ours(args):
     gemm_traffic = ncu_traffic(args.config, [L["lin"] for L in layers], "gemm")
     tq_traffic = ncu_traffic(args.config, [L["lin"] for L in layers], "tq")
     decode = T <= 64     # decode step (C4): the GEMM streams the weights, HBM-bound (SURVEY 8(a) sizes)
-    g_bytes = sum(gemm_min_bytes(T, L["lin"]) for L in layers)
+    g_bytes = sum(fused_bytes(T, L["lin"]) if fused[i] else gemm_min_bytes(T, L["lin"]) for i, L in enumerate(layers))
     if decode:
         g_gbs = g_bytes / (gemm_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": "fq_w4a4_linear (decode kernel: tcgen05 kind::i8, cluster split-K)",
+        kname = "fq_w4a4_linear (decode kernel: tcgen05 kind::i8, cluster split-K)"
+        if any(fused):
+            kname = ("decode GEMM launches: fq_flatquant_linear fused (transform + tcgen05 kind::i8 GEMM, "
+                     + ", ".join(L["lin"].name for i, L in enumerate(layers) if fused[i]) + "), fq_w4a4_linear ("
+                     + ", ".join(L["lin"].name for i, L in enumerate(layers) if not fused[i]) + ")")
+        roof = {"bound": "hbm", "kernel": kname,
                 "achieved": round(g_gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": round(g_gbs / pk["hbm_gbs"], 4), "traffic": gemm_traffic,
-                "per": "aggregate of the step's GEMM launches (sum of compulsory bytes / sum of their durations)",
+                "per": "aggregate of the step's GEMM launches (sum of compulsory bytes / sum of their durations; "
+                       "a fused launch counts its transform's bytes too)",
                 "algorithmic_bytes_per_step": int(g_bytes), "tops": round(gemm_tops, 1),
                 "peak_source": f"{peak_src}: hbm_gbs"}
     else:
@@ -613,7 +660,7 @@ def run_ours(args):
     tq_roof = {"bound": "hbm", "kernel": "fq_transform_quant", "achieved": round(tq_gbs, 1),
                "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(tq_gbs / pk["hbm_gbs"], 4),
                "traffic": tq_traffic, "algorithmic_bytes_per_step": int(t_bytes),
-               "tflops": round(t_flops / (tq_ms * 1e-3) / 1e12, 1),
+               "tflops": round(t_flops / (tq_ms * 1e-3) / 1e12, 1) if tq_ms > 0 else None,
                "per": "sum of algorithmic bytes / sum of event-timed launch durations (pass 2)",
                "event_overhead": {"empty_kernel_us": round(ev_empty * 1e3, 2),
                                   "same_bytes_copy_us": round(ev_copy * 1e3, 2),
@@ -621,6 +668,9 @@ def run_ours(args):
                                   "note": "an event-bracketed empty kernel and a torch copy moving one 64x64 "
                                           "launch's algorithmic bytes, timed the same way (L2 flushed): the "
                                           "ceiling an event-timed launch of this size can show"}}
+    if any(fused):
+        tq_roof["note"] = ("the transforms of " + ", ".join(L["lin"].name for i, L in enumerate(layers) if fused[i])
+                           + " run inside their fused decode launch (roofline) and are not counted here")
     if fig6 is not None:
         tq_roof["in_step"] = {"achieved": fig6["in_step_tq_gbs"],
                               "frac": round(fig6["in_step_tq_gbs"] / pk["hbm_gbs"], 4),

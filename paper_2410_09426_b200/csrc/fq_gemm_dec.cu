@@ -39,7 +39,8 @@ namespace gd {
 
 // Optional device timeline of 4 CTAs (build with -DFQ_TRACE; scripts/trace_dec.py): globaltimer
 // stamps of [0] start, [1] setup done, [2] TMA issue of stage j (4+j), converters done (40+j),
-// MMA issued (76+j), [112] tfull, [113] partial tile stored, [114] reduced, [115] end.
+// MMA issued (76+j), [112] tfull, [113] partial tile stored, [114] reduced, [115] end; FUSED: [116]
+// phase-A X tile landed, [119] stage-1 epilogue done, [117] tile counted, [118] all tiles counted.
 #ifdef FQ_TRACE
 __device__ unsigned long long g_dtrace[4 * 128];
 __device__ int g_dtrace_cta[4];
@@ -272,7 +273,6 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     }
     tc::mbar_init(tfull, 1);
     if constexpr (FUSED) {
-      tc::mbar_init(fdx, 1);
       tc::mbar_init(fd1, 1);
       tc::mbar_init(fda2, 4);
       tc::mbar_init(fd2, 1);
@@ -285,6 +285,19 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       tc::tma_prefetch_desc(&fd.tmX);
       tc::tma_prefetch_desc(&fd.tmP1);
       tc::tma_prefetch_desc(&fd.tmP2);
+    }
+  }
+  // FUSED, ticket CTAs: the phase-A loads leave first, before the setup barrier, when x, P1 and P2
+  // may be read before the PDL wait (otherwise after the weights, in the producer loop below)
+  const bool early_x = ticket && (pdl & (PDL_P | PDL_X)) == (PDL_P | PDL_X);
+  if (FUSED && ticket && warp == TMA_WARP && lane == 0) {
+    tc::mbar_init(fdx, 1);
+    tc::fence_barrier_init();
+    if (early_x) {
+      tc::mbar_expect_tx(fdx, uint32_t(FD_X_BYTES + 2 * FD_P_BYTES));
+      tc::tma_load_3d(fsX, &fd.tmX, fdx, 0, 0, 2 * int(blockIdx.x));
+      tc::tma_load_2d(fsP1, &fd.tmP1, fdx, 0, 0);
+      tc::tma_load_2d(fsP2, &fd.tmP2, fdx, 0, 0);
     }
   }
   if (warp == ALLOC_WARP) tc::tmem_alloc(tmem_slot, TMEM_COLS);
@@ -330,16 +343,6 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   if (warp == TMA_WARP) {
     // ======================= TMA producer =======================
     if (lane == 0) {
-      if constexpr (FUSED) {
-        if (ticket) {
-          // phase A first: this CTA's two tokens, P1 and P2 (x is an activation, P1/P2 parameters)
-          if ((pdl & (PDL_P | PDL_X)) != (PDL_P | PDL_X)) tc::griddep_wait();
-          tc::mbar_expect_tx(fdx, uint32_t(FD_X_BYTES + 2 * FD_P_BYTES));
-          tc::tma_load_3d(fsX, &fd.tmX, fdx, 0, 0, 2 * int(blockIdx.x));
-          tc::tma_load_2d(fsP1, &fd.tmP1, fdx, 0, 0);
-          tc::tma_load_2d(fsP2, &fd.tmP2, fdx, 0, 0);
-        }
-      }
       // the weights are parameters: unless the preceding kernel of the stream writes them
       // (host-side hazard check, fq_abi.cu), start streaming them before the wait
       if (!(pdl & PDL_P)) tc::griddep_wait();
@@ -354,6 +357,13 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         tc::mbar_expect_tx(&pfull[j], uint32_t(WP_BYTES + ap_bytes));
         tc::tma_load_2d(sP + size_t(j) * P_BYTES, &tmW, &pfull[j], kb_of(j) * (BK / 2), fb * BM);
       }
+      if (FUSED && ticket && !early_x) {          // phase-A loads that had to wait for the predecessor
+        tc::griddep_wait();
+        tc::mbar_expect_tx(fdx, uint32_t(FD_X_BYTES + 2 * FD_P_BYTES));
+        tc::tma_load_3d(fsX, &fd.tmX, fdx, 0, 0, 2 * int(blockIdx.x));
+        tc::tma_load_2d(fsP1, &fd.tmP1, fdx, 0, 0);
+        tc::tma_load_2d(fsP2, &fd.tmP2, fdx, 0, 0);
+      }
       if constexpr (FUSED) {
         // every ticket CTA has stored its codes and scales (release/acquire at GPU scope); the
         // activation codes are then read through the async proxy (TMA)
@@ -363,6 +373,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
           if (clock64() - t_start > (1ll << 32)) __trap();    // never hang the GPU: ~2 s without progress
         }
         fence_proxy_async_global();
+        dtrace(tslot, 118);
         tc::mbar_arrive(actready);
         // last CTA out resets the slot for its next launch (all arrivals have been counted)
         if (atomicAdd(fd.sync + 1, 1u) == gridDim.x - 1) {
@@ -468,6 +479,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         // has read D and written W (fp16) to shared memory
         tc::mbar_wait(fdx, 0);
         tc::fence_after();
+        dtrace(tslot, 116);
         const uint32_t xs = smem_u32(fsX), p1a = smem_u32(fsP1), p2a = smem_u32(fsP2), a2 = smem_u32(fsA2);
 #pragma unroll
         for (int kk = 0; kk < FD_N / 16; ++kk)
@@ -476,6 +488,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         tc::mma_commit(fd1);
         tc::mbar_wait(fda2, 0);
         tc::fence_after();
+        dtrace(tslot, 119);
 #pragma unroll
         for (int kk = 0; kk < FD_N / 16; ++kk)
           tc::mma_ss<false>(tmem_base, tc::sdesc_sw128(a2 + kk * 2048, FD_N * 128, 1024),
@@ -567,6 +580,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         // stage 2: D lane (t, i), column j = Y_t[i][j] (prescaled by 2^pe)
         tc::mbar_wait(fd2, 0);
         tc::fence_after();
+        if (L == 0) dtrace(tslot, 120);
         float m2 = 0.f;
 #pragma unroll
         for (int c = 0; c < FD_N; c += 16) {
@@ -601,11 +615,17 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
           if (store) *reinterpret_cast<uint4*>(qrow + c / 2) = make_uint4(w[0], w[1], w[2], w[3]);
         }
         if (store && i == 0) fd.s[t] = mp > 0.f ? fd.alpha * (mp * inv_pre) / 7.0f : 1.0f;
-        __threadfence();                                   // codes and scale visible GPU-wide ...
-        fence_proxy_async_global();                        // ... and to the consumers' TMA loads
+        if (L == 0) dtrace(tslot, 121);
+        fence_proxy_async_global();                        // (the consumers read the codes through TMA)
         tc::fence_before();
         named_bar_sync(1, 128);
-        if (L == 0) red_release_gpu_add(fd.sync, 1u);      // this tile is done
+        if (L == 0) {
+          dtrace(tslot, 122);
+          // the group's stores happen before this release through the barrier (bar.sync orders
+          // them at CTA scope; the GPU-scope release is cumulative), as in CUTLASS's grid barrier
+          red_release_gpu_add(fd.sync, 1u);                // this tile is done
+          dtrace(tslot, 117);
+        }
       }
     }
     // while the main loop runs: stage the epilogue's scales in shared memory
