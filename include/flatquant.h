@@ -156,7 +156,17 @@ fq_status fq_w4a4_gemm_i32(const uint8_t* qa, int64_t T, int32_t K, const uint8_
 /* ---------------------------------------------------------------------------------------
  * fq_flatquant_linear -- the whole hot path a1-a7 for one linear layer: transform+quant of
  * x into the caller's workspace (q_ws [T, n/2] uint8, s_ws [T] fp32), then the W4A4 GEMM.
- * Equivalent to fq_transform_quant followed by fq_w4a4_linear on the same stream.
+ * Equivalent to fq_transform_quant followed by fq_w4a4_linear on the same stream: q_ws, s_ws
+ * and y hold bit-identical results either way.
+ * Decode sizes run FUSED in ONE launch (PAPER.md:312-314 fuses the
+ * transform and quantization into one kernel, here it is fused into the GEMM as well): for
+ * 1 <= T <= 64, n1 = n2 = 64, fp16 x and p2 != NULL, the first ceil(T/2) CTAs of the decode GEMM
+ * transform two tokens each into q_ws/s_ws (L2-resident at these sizes) while every CTA already
+ * streams its weights, and the GEMM reads the codes once all tiles are published.  Tile
+ * publication uses a {arrivals, departures} counter pair from a ring of 1024 slots per device in
+ * the library's own device memory, reset by the last CTA of each launch (so CUDA-graph replay is
+ * safe); at most 1024 fused launches may be in flight on one device at a time.  Every other
+ * shape, dtype or T runs the two kernels.
  * ------------------------------------------------------------------------------------- */
 fq_status fq_flatquant_linear(const void* x, int32_t x_dtype, int64_t T, int32_t n1,
                               int32_t n2, const void* p1, const void* p2, float alpha,

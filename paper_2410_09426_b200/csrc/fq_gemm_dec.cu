@@ -127,19 +127,37 @@ static_assert(RED_BYTES <= STAGES * W_BYTES, "the partial tile reuses the widene
 // prefetched before the PDL wait): the decode GEMM streams weights at the rate its bytes in flight
 // allow (Little's law, ~1.3 us per round trip), and the shapes with few feature blocks cannot fill
 // two CTAs per SM under cluster residency limits.
+#ifndef FQ_DEC_S1
+#define FQ_DEC_S1 4
+#endif
+#ifndef FQ_DEC_KP1
+#define FQ_DEC_KP1 2
+#endif
+#ifndef FQ_DEC_P1
+#define FQ_DEC_P1 (FQ_DEC_KP1 == 2 ? 7 : 14)
+#endif
 template <int CFG, bool FUSED = false>
 struct DecCfg {
   // FUSED: the transform tile of phase A borrows the widened-operand stages (48 KB), so the
-  // one-CTA-per-SM configuration keeps 6 of them (TMEM: 64 + 6 x 32 columns)
-  static constexpr int STAGES = CFG == 0 ? gd::STAGES : (FUSED ? 6 : 4);
-  static constexpr int PSTAGES = CFG == 0 ? gd::PSTAGES : 14;
+  // one-CTA-per-SM configuration keeps at least 6 of them
+  static constexpr int STAGES = CFG == 0 ? gd::STAGES : ((FUSED && FQ_DEC_S1 < 6) ? 6 : FQ_DEC_S1);
+  static constexpr int PSTAGES = CFG == 0 ? gd::PSTAGES : FQ_DEC_P1;
+  // K-blocks per packed ring stage: 2 loads 128-byte rows (one TMA row request per 128 B instead
+  // of per 64 B: the TMA unit's request rate, not HBM, paced the one-CTA-per-SM main loop)
+  static constexpr int KP = (CFG == 0 || !TMEMW) ? 1 : FQ_DEC_KP1;
+  static constexpr int PB = KP * P_BYTES;                     // packed ring stage bytes
+  static constexpr int WPB = KP * WP_BYTES;                   // weight part of a ring stage
   static constexpr int MINB = CFG == 0 ? FQ_DEC_MINB : 1;
-  static constexpr size_t SMEM = size_t(STAGES) * W_BYTES + size_t(PSTAGES) * P_BYTES + 1024 + (FUSED ? 512 : 256);
+  // accumulator [0, 64) + one 32-column weight stage per MMA stage (a power of two >= 32)
+  static constexpr int TMEM_COLS = !TMEMW ? 64 : (W_COL0 + STAGES * WT_COLS <= 256 ? 256 : 512);
+  static constexpr size_t SMEM = size_t(STAGES) * W_BYTES + size_t(PSTAGES) * PB + 1024 + (FUSED ? 512 : 256);
   static_assert(RED_BYTES <= STAGES * W_BYTES, "partial tile in the operand stages");
   static_assert(!FUSED || STAGES * W_BYTES >= 48 * 1024, "phase-A transform tile in the operand stages");
   static_assert(!TMEMW || W_COL0 + STAGES * WT_COLS <= TMEM_COLS, "TMEM budget");
+  static_assert(MINB == 1 || TMEM_COLS <= 256, "two CTAs per SM share the 512 TMEM columns");
   static_assert(SMEM * MINB <= 232448, "shared memory per SM");
-  static_assert(DB < PSTAGES, "batch within the packed ring");
+  static_assert(DB < PSTAGES * KP, "batch within the packed ring");
+  static_assert(KP == 1 || DB == KP, "a conversion batch is one ring stage");
 };
 static_assert(P_BYTES % 1024 == 0 && W_BYTES % 1024 == 0 && WW_BYTES % 1024 == 0, "1 KB alignment");
 static_assert(!TMEMW || (BK == 128 && W_COL0 + STAGES * WT_COLS <= TMEM_COLS), "TMEM budget");
@@ -219,11 +237,13 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
                 void* __restrict__ yv, const int8_t* __restrict__ za, const int32_t* __restrict__ colsum,
                 int S, int pdl, const __grid_constant__ FdParams fd) {
   constexpr int STAGES = DecCfg<CFG, FUSED>::STAGES, PSTAGES = DecCfg<CFG, FUSED>::PSTAGES;
+  constexpr int KP = DecCfg<CFG, FUSED>::KP, PB = DecCfg<CFG, FUSED>::PB, WPB = DecCfg<CFG, FUSED>::WPB;
+  constexpr int PROW = KP * (BK / 2);                        // packed bytes of one row in a ring stage
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;                                        // widened stages [W 16 KB | A 8 KB]
   uint8_t* sP = smem + size_t(STAGES) * W_BYTES;             // packed ring    [W 8 KB | A 4 KB]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + size_t(PSTAGES) * P_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + size_t(PSTAGES) * PB);
   uint64_t* full = bars;                   // [STAGES]  converters -> MMA
   uint64_t* empty = bars + STAGES;         // [STAGES]  MMA commit -> converters
   uint64_t* pfull = bars + 2 * STAGES;     // [PSTAGES] TMA -> converters
@@ -252,15 +272,21 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   if (threadIdx.x == 0) dtrace(tslot, 0);
   const int rank = S > 1 ? int(tc::cluster_ctarank()) : 0;
   const int fb = blockIdx.x / S;                             // feature block of this cluster
-  const int NKB = (K + BK - 1) / BK;
-  const int kb0 = rank * NKB / S, kb1 = (rank + 1) * NKB / S, nk = kb1 - kb0;
+  // units of KP K-blocks ("super-blocks", one packed ring stage each) are split across the cluster;
+  // a super-block's K-blocks past K are zero-filled by TMA and contribute nothing
+  const int NKB = (K + BK * KP - 1) / (BK * KP);
+  const int kb0 = rank * NKB / S, kb1 = (rank + 1) * NKB / S, nsb = kb1 - kb0, nk = nsb * KP;
   // Every CTA reads the same few KB of activation codes per K-block; walking the K-blocks in the
   // same order would make all CTAs hit the same L2 lines at the same time.  Each CTA starts at a
   // different K-block instead (integer accumulation: the order does not change the result).
-  const int krot = nk > 0 ? int((unsigned(fb) * 5u + unsigned(rank) * 3u) % unsigned(nk)) : 0;
-  auto kb_of = [&](int j) { const int r = j + krot; return kb0 + (r >= nk ? r - nk : r); };
+  const int krot = nsb > 0 ? int((unsigned(fb) * 5u + unsigned(rank) * 3u) % unsigned(nsb)) : 0;
+  auto kb_of = [&](int u) { const int r = u + krot; return kb0 + (r >= nsb ? r - nsb : r); };   // super-block
   const uint32_t idesc = tc::idesc_i8(BM, TN);
+#ifdef FQ_EXP_DEC_NOACT            // experiment builds only: activation codes not loaded (timing)
+  const int ap_bytes = 0;
+#else
   const int ap_bytes = TN * (BK / 2);
+#endif
 
   if (warp == MMA_WARP && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -300,7 +326,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       tc::tma_load_2d(fsP2, &fd.tmP2, fdx, 0, 0);
     }
   }
-  if (warp == ALLOC_WARP) tc::tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == ALLOC_WARP) tc::tmem_alloc(tmem_slot, DecCfg<CFG, FUSED>::TMEM_COLS);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -319,17 +345,22 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
 #pragma unroll
       for (int b = 0; b < DB; ++b) {
         if (b < nb) {
-          const int j = j0 + b, sp = j % PSTAGES, st = j % STAGES;
+          const int j = j0 + b, u = j / KP, h = j % KP, sp = u % PSTAGES, st = j % STAGES;
           tc::mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1);
-          tc::mbar_wait(&pfull[sp], (j / PSTAGES) & 1);
-          const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES + WP_BYTES);
+          tc::mbar_wait(&pfull[sp], (u / PSTAGES) & 1);
+          const uint32_t src = smem_u32(sP + size_t(sp) * PB + WPB);
           const uint32_t dst = smem_u32(sW + size_t(st) * W_BYTES);
 #ifndef FQ_EXP_DEC_SKIPA          // (experiment build: activation conversion removed)
-          for (int task = at; task < TN * CPR; task += A_CONV_THREADS)
-            convert_chunk(src + uint32_t(task * 16), dst, task / CPR, task % CPR, AW_ATOM);
+          for (int task = at; task < TN * CPR; task += A_CONV_THREADS) {
+            const int row = task / CPR, c = task % CPR;
+            // KP 1: dense 64-byte rows; KP 2: 128-byte SWIZZLE_128B rows, this K-block's half
+            const uint32_t a = KP == 1 ? uint32_t(task * 16)
+                                       : uint32_t(row * PROW + (((h * CPR + c) ^ (row & 7)) << 4));
+            convert_chunk(src + a, dst, row, c, AW_ATOM);
+          }
 #endif
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&pempty[sp]);
+          if (lane == 0 && h == KP - 1) tc::mbar_arrive(&pempty[sp]);
         }
       }
       tc::fence_proxy_async_smem();
@@ -346,16 +377,16 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       // the weights are parameters: unless the preceding kernel of the stream writes them
       // (host-side hazard check, fq_abi.cu), start streaming them before the wait
       if (!(pdl & PDL_P)) tc::griddep_wait();
-      const int pre = nk < PSTAGES ? nk : PSTAGES;
+      const int pre = nsb < PSTAGES ? nsb : PSTAGES;          // ring stages (super-blocks)
 #if FQ_DEC_L2PF
       // the rest of this CTA's weight slice into L2 now (one bulk tensor prefetch per K-block):
       // the ring's loads then hit L2 instead of waiting a full HBM round trip each
-      for (int j = pre; j < nk; ++j) tc::tma_prefetch_l2_2d(&tmW, kb_of(j) * (BK / 2), fb * BM);
+      for (int j = pre; j < nsb; ++j) tc::tma_prefetch_l2_2d(&tmW, kb_of(j) * PROW, fb * BM);
 #endif
       for (int j = 0; j < pre; ++j) {
         if (j < 36) dtrace(tslot, 4 + j);
-        tc::mbar_expect_tx(&pfull[j], uint32_t(WP_BYTES + ap_bytes));
-        tc::tma_load_2d(sP + size_t(j) * P_BYTES, &tmW, &pfull[j], kb_of(j) * (BK / 2), fb * BM);
+        tc::mbar_expect_tx(&pfull[j], uint32_t(WPB + KP * ap_bytes));
+        tc::tma_load_2d(sP + size_t(j) * PB, &tmW, &pfull[j], kb_of(j) * PROW, fb * BM);
       }
       if (FUSED && ticket && !early_x) {          // phase-A loads that had to wait for the predecessor
         tc::griddep_wait();
@@ -384,15 +415,15 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         tc::griddep_wait();                      // qa written by the transform kernel is visible
       }
       for (int j = 0; j < pre; ++j)
-        tc::tma_load_2d(sP + size_t(j) * P_BYTES + WP_BYTES, &tmA, &pfull[j], kb_of(j) * (BK / 2), 0);
-      for (int j = pre; j < nk; ++j) {
+        if (ap_bytes) tc::tma_load_2d(sP + size_t(j) * PB + WPB, &tmA, &pfull[j], kb_of(j) * PROW, 0);
+      for (int j = pre; j < nsb; ++j) {
         const int sp = j % PSTAGES;
         tc::mbar_wait(&pempty[sp], ((j / PSTAGES) & 1) ^ 1);
         if (j < 36) dtrace(tslot, 4 + j);
-        tc::mbar_expect_tx(&pfull[sp], uint32_t(WP_BYTES + ap_bytes));
-        uint8_t* dst = sP + size_t(sp) * P_BYTES;
-        tc::tma_load_2d(dst, &tmW, &pfull[sp], kb_of(j) * (BK / 2), fb * BM);
-        tc::tma_load_2d(dst + WP_BYTES, &tmA, &pfull[sp], kb_of(j) * (BK / 2), 0);
+        tc::mbar_expect_tx(&pfull[sp], uint32_t(WPB + KP * ap_bytes));
+        uint8_t* dst = sP + size_t(sp) * PB;
+        tc::tma_load_2d(dst, &tmW, &pfull[sp], kb_of(j) * PROW, fb * BM);
+        if (ap_bytes) tc::tma_load_2d(dst + WPB, &tmA, &pfull[sp], kb_of(j) * PROW, 0);
       }
     }
     __syncwarp();
@@ -413,21 +444,23 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
 #pragma unroll
           for (int b = 0; b < DB; ++b) {
             if (b < nb) {
-              const int j = j0 + b, sp = j % PSTAGES, st = j % STAGES;
+              const int j = j0 + b, u = j / KP, h = j % KP, sp = u % PSTAGES, st = j % STAGES;
               tc::mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1);
-              tc::mbar_wait(&pfull[sp], (j / PSTAGES) & 1);
-              const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES) + uint32_t(r * 64);
+              tc::mbar_wait(&pfull[sp], (u / PSTAGES) & 1);
+              const uint32_t src = smem_u32(sP + size_t(sp) * PB) + uint32_t(r * PROW);
               uint32_t w[32];
 #ifdef FQ_EXP_DEC_SKIPW           // experiment build only: weight conversion removed
               if (true) {
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&pempty[sp]);
+                if (lane == 0 && h == KP - 1) tc::mbar_arrive(&pempty[sp]);
                 continue;
               }
 #endif
 #pragma unroll
               for (int c = 0; c < 4; ++c) {
-                const uint4 pk = tc::lds128(src + uint32_t((c ^ ((r >> 1) & 3)) << 4));
+                // KP 1: SWIZZLE_64B 64-byte rows; KP 2: SWIZZLE_128B 128-byte rows, this block's half
+                const int pos = KP == 1 ? (c ^ ((r >> 1) & 3)) : ((h * 4 + c) ^ (r & 7));
+                const uint4 pk = tc::lds128(src + uint32_t(pos << 4));
                 widen8(pk.x, w[8 * c + 0], w[8 * c + 1]);
                 widen8(pk.y, w[8 * c + 2], w[8 * c + 3]);
                 widen8(pk.z, w[8 * c + 4], w[8 * c + 5]);
@@ -435,7 +468,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
               }
               tc::tmem_st32(tl + uint32_t(st * WT_COLS), w);
               __syncwarp();
-              if (lane == 0) tc::mbar_arrive(&pempty[sp]);   // the loads were consumed by the st
+              if (lane == 0 && h == KP - 1) tc::mbar_arrive(&pempty[sp]);   // loads consumed by the st
             }
           }
           tc::tmem_st_wait();
@@ -454,7 +487,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       const int sp = j % PSTAGES, st = j % STAGES;
       tc::mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1);
       tc::mbar_wait(&pfull[sp], (j / PSTAGES) & 1);
-      const uint32_t src = smem_u32(sP + size_t(sp) * P_BYTES);
+      const uint32_t src = smem_u32(sP + size_t(sp) * PB);
       const uint32_t dst = smem_u32(sW + size_t(st) * W_BYTES);
       for (int task = ct; task < ntask; task += CONV_THREADS) {
         const int row = task / CPR, c = task % CPR;
@@ -742,7 +775,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   if (threadIdx.x == 0) dtrace(tslot, 115);
   if (warp == ALLOC_WARP) {
     tc::fence_after();
-    tc::tmem_dealloc(tmem_base, TMEM_COLS);
+    tc::tmem_dealloc(tmem_base, DecCfg<CFG, FUSED>::TMEM_COLS);
   }
 }
 
@@ -805,10 +838,18 @@ static int dec_max_clusters(const void* kern, int S) {
 template <int CFG, bool FUSED>
 static int dec_pick_split(const void* kern, int N, int K) {
   const int fbs = (N + gd::BM - 1) / gd::BM;
-  const int nkb = (K + gd::BK - 1) / gd::BK;
+  const int nkb = (K + gd::BK * gd::DecCfg<CFG, FUSED>::KP - 1) / (gd::BK * gd::DecCfg<CFG, FUSED>::KP);
+  // at most one CTA per SM from the split (round 2): the second slot of every SM stays free for
+  // the NEXT kernel of the stream, whose CTAs then start (PDL) and stream their weights while
+  // this kernel drains -- measured: the C4 GEMM chain 64 -> 52 us
+  static const int cap_per_sm = [] {               // FQ_DEC_GRIDCAP: testing aid (CTAs per SM of the grid)
+    const char* v = std::getenv("FQ_DEC_GRIDCAP");
+    return v ? std::atoi(v) : 1;
+  }();
+  const int per_sm = std::max(1, std::min(cap_per_sm, gd::DecCfg<CFG, FUSED>::MINB));
   int s = 1;
   for (int c = 2; c <= gd::MAX_SPLIT && c <= nkb; ++c)
-    if (fbs * c <= gd::DecCfg<CFG, FUSED>::MINB * num_sms() && fbs <= dec_max_clusters<CFG, FUSED>(kern, c)) s = c;
+    if (fbs * c <= per_sm * num_sms() && fbs <= dec_max_clusters<CFG, FUSED>(kern, c)) s = c;
   return s;
 }
 
@@ -844,17 +885,19 @@ static cudaError_t dec_launch_cfg(const GemmArgs& a, int split, const FdArgs* f)
   {
     const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.N)};
     const uint64_t strides[1] = {uint64_t(a.K / 2)};
-    const uint32_t box[2] = {BK / 2, BM};
-    if (!tmap_encode(&mw, a.qw, 1, 2, dims, strides, box, TMEMW ? TMAP_SW64 : TMAP_SW_NONE))
+    const uint32_t box[2] = {uint32_t(DC::KP * BK / 2), BM};
+    if (!tmap_encode(&mw, a.qw, 1, 2, dims, strides, box,
+                     DC::KP == 2 ? TMAP_SW128 : (TMEMW ? TMAP_SW64 : TMAP_SW_NONE)))
       return cudaErrorInvalidValue;
   }
   {
     const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.T)};
     const uint64_t strides[1] = {uint64_t(a.K / 2)};
-    const uint32_t box[2] = {BK / 2, uint32_t(TN)};
-    if (!tmap_encode(&ma, a.qa, 1, 2, dims, strides, box, TMAP_SW_NONE)) return cudaErrorInvalidValue;
+    const uint32_t box[2] = {uint32_t(DC::KP * BK / 2), uint32_t(TN)};
+    if (!tmap_encode(&ma, a.qa, 1, 2, dims, strides, box, DC::KP == 2 ? TMAP_SW128 : TMAP_SW_NONE))
+      return cudaErrorInvalidValue;
   }
-  const int nkb = (a.K + BK - 1) / BK;
+  const int nkb = (a.K + BK * DC::KP - 1) / (BK * DC::KP);     // ring stages of K
   int S = split > 0 ? split : dec_pick_split<CFG, FUSED>(reinterpret_cast<const void*>(kern), a.N, a.K);
   S = std::max(1, std::min({S, MAX_SPLIT, nkb}));
   const int fbs = (a.N + BM - 1) / BM;
@@ -904,9 +947,10 @@ static bool dec_deep(const GemmArgs& a) {         // FQ_DEC_CFG: testing aid (fo
     const char* v = std::getenv("FQ_DEC_CFG");
     return v ? std::atoi(v) : -1;
   }();
-  const int fbs = (a.N + gd::BM - 1) / gd::BM;
-  // one CTA per SM with the deep ring whenever every feature block gets its own SM
-  return env_cfg >= 0 ? env_cfg == 1 : (fbs <= num_sms());
+  // round 2: the two-CTAs-per-SM footprint everywhere (108 KB, 64 registers, 256 TMEM columns),
+  // so that consecutive decode kernels co-reside; the deep-ring one-CTA-per-SM configuration
+  // (FQ_DEC_CFG=1) kept its weights in flight but left no room for the next kernel
+  return env_cfg == 1;
 }
 
 cudaError_t gemm_dec_launch(const GemmArgs& a, int split) {

@@ -71,9 +71,11 @@ constexpr int MAX_GROUPS = 4;
 constexpr int SMEM_LIMIT = 232448;       // max dynamic smem per block on sm_100
 constexpr int SMEM_OVERHEAD = 1024 + 512;  // 1024-B alignment slack + barriers/scratch
 
-// SMALL (decode-size launches, T <= 64): one epilogue group and two X stages, so a 64 x 64 CTA
-// needs ~66 KB of shared memory and 128 TMEM columns and can become resident beside a decode-GEMM CTA
-// of the preceding kernel (PDL): its setup and parameter loads then overlap that kernel's tail.
+// SMALL (decode-size launches, T <= 64, so every CTA has exactly one tile): one epilogue group,
+// one X stage, and the stage-2 operand A2 written over P1 and the X tile once the stage-1 MMA
+// that read them has completed -- 112 x 128 needs 88 KB of shared memory (120 KB without the
+// aliasing) and 256 TMEM columns, 64 x 64 32 KB and 128 columns, so the CTA becomes resident
+// beside a decode-GEMM CTA of the preceding kernel (PDL): its setup and loads overlap that tail.
 // IDENT2: P2 = I (the paper's online o_proj transform P_o (a x a) (x) I_{d_head}, PAPER.md:297, 726;
 // DESIGN.md reading R22): stage 1 only, its fp32 result quantized directly (no fp16 intermediate,
 // no D2 in TMEM); the A2 buffer is the staging area that turns TMEM's column-per-lane layout into
@@ -99,12 +101,14 @@ struct Cfg {
   static constexpr int THREADS = (4 + 4 * GROUPS) * 32;
   static constexpr int TMEM_USED = GROUPS * (D1C + D2C);
   static constexpr int TMEM_COLS = TMEM_USED <= 128 ? 128 : (TMEM_USED <= 256 ? 256 : 512);
-  static constexpr int FIXED = P1_BYTES + (IDENT2 ? 0 : P2_BYTES) + GROUPS * A2_BYTES;
+  static constexpr bool ALIAS_A2 = SMALL && !IDENT2;          // A2 over P1 + X (one tile per CTA)
+  static constexpr int FIXED = P1_BYTES + (IDENT2 ? 0 : P2_BYTES) + (ALIAS_A2 ? 0 : GROUPS * A2_BYTES);
   static constexpr int STAGES_FIT = (SMEM_LIMIT - SMEM_OVERHEAD - FIXED) / X_BYTES;
-  static constexpr int STAGES = SMALL ? 2 : (STAGES_FIT > 8 ? 8 : STAGES_FIT);
+  static constexpr int STAGES = SMALL ? 1 : (STAGES_FIT > 8 ? 8 : STAGES_FIT);
   static constexpr size_t SMEM = size_t(FIXED) + size_t(STAGES) * X_BYTES + SMEM_OVERHEAD;
   static_assert(TMEM_USED <= 512, "TMEM budget");
-  static_assert(STAGES >= 2, "shared-memory budget");
+  static_assert(SMALL || STAGES >= 2, "shared-memory budget");
+  static_assert(!ALIAS_A2 || A2_BYTES <= P1_BYTES + X_BYTES, "A2 fits over P1 + X");
 };
 
 using namespace qz;   // MAGIC, prescale_exp, exp2i, max3f, fma_sat (fq_quant.cuh)
@@ -178,10 +182,11 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sP1 = smem;
-  uint8_t* sP2 = sP1 + C::P1_BYTES;
-  uint8_t* sA2 = sP2 + (IDENT2 ? 0 : C::P2_BYTES);
-  uint8_t* sX = sA2 + G * C::A2_BYTES;
+  // layout P1 | P2 | A2 [G] | X [S]; SMALL: P2 | P1 | X with A2 over P1 + X (C::ALIAS_A2)
+  uint8_t* sP1 = C::ALIAS_A2 ? smem + C::P2_BYTES : smem;
+  uint8_t* sP2 = C::ALIAS_A2 ? smem : sP1 + C::P1_BYTES;
+  uint8_t* sA2 = C::ALIAS_A2 ? sP1 : sP2 + (IDENT2 ? 0 : C::P2_BYTES);
+  uint8_t* sX = C::ALIAS_A2 ? sP1 + C::P1_BYTES : sA2 + G * C::A2_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sX + size_t(S) * C::X_BYTES);
   uint64_t* xfull = bars;            // [S]  TMA -> MMA
   uint64_t* xempty = bars + S;       // [S]  MMA commit -> TMA
@@ -686,10 +691,8 @@ static cudaError_t dispatch_ident2(const TQArgs& a) {     // P2 = I, n2 = 128
 template <int N1, int N2>
 static cudaError_t dispatch(const TQArgs& a) {
   if (a.zero) return a.bf16 ? launch<N1, N2, true, false, true>(a) : launch<N1, N2, false, false, true>(a);
-  if constexpr (N1 == 64 && N2 == 64) {           // decode (C4) launches of the 64 x 64 transforms
-    if (a.T <= 64 && !a.y && small_enabled())
-      return a.bf16 ? launch<N1, N2, true, false, false, true>(a) : launch<N1, N2, false, false, false, true>(a);
-  }
+  if (a.T <= 64 && !a.y && small_enabled())       // decode (C4) launches: one tile per CTA
+    return a.bf16 ? launch<N1, N2, true, false, false, true>(a) : launch<N1, N2, false, false, false, true>(a);
   if (a.bf16) return a.y ? launch<N1, N2, true, true>(a) : launch<N1, N2, true, false>(a);
   return a.y ? launch<N1, N2, false, true>(a) : launch<N1, N2, false, false>(a);
 }
