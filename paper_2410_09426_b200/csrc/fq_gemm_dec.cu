@@ -110,6 +110,9 @@ constexpr int CONV_THREADS = NUM_CONV_WARPS * 32;
 #ifndef FQ_DEC_L2PF
 #define FQ_DEC_L2PF 0
 #endif
+#ifndef FQ_DEC_L2PF_WIDE
+#define FQ_DEC_L2PF_WIDE 0    // warp 3 prefetches the CTA's weight slice into L2: 1 TMA boxes, 2 LSU lines
+#endif
 #ifndef FQ_DEC_EPI_CONV
 #define FQ_DEC_EPI_CONV 0     // round 2: the converter warps alone are as fast (C4 74.7 vs 77.9 us)
 #endif
@@ -233,6 +236,7 @@ FQ_DEVICE void fence_proxy_async_global() { asm volatile("fence.proxy.async.glob
 template <int CFG, bool OUT_I32, bool BF16, bool ASYM, bool FUSED = false>
 __global__ void __launch_bounds__(THREADS, DecCfg<CFG, FUSED>::MINB)
 gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA,
+                const __grid_constant__ CUtensorMap tmWpf, const uint8_t* __restrict__ qwp,
                 const float* __restrict__ sa, int T, int TN, int K, const float* __restrict__ sw, int N,
                 void* __restrict__ yv, const int8_t* __restrict__ za, const int32_t* __restrict__ colsum,
                 int S, int pdl, const __grid_constant__ FdParams fd) {
@@ -502,6 +506,43 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       if (threadIdx.x == CONV_WARP0 * 32 && j < 36) dtrace(tslot, 40 + j);
     }
     }
+  } else if (warp == 3) {
+#if FQ_DEC_L2PF_WIDE == 2
+    // LSU variant: every lane prefetches 128-byte lines of its rows (no TMA-engine time)
+    if (!(pdl & PDL_P)) tc::griddep_wait();
+    {
+      const int pre = nsb < PSTAGES ? nsb : PSTAGES;
+      const size_t ld = size_t(K / 2);
+      for (int u = pre; u < nsb; ++u) {
+        const int kb = kb_of(u);
+        const size_t off = size_t(kb) * PROW;
+        if (PROW < 128 && (off & 127)) continue;              // this half-line came with the previous block
+        for (int r = lane; r < BM; r += 32) {
+          const uint8_t* pa = qwp + size_t(fb * BM + r) * ld + off;
+          if (fb * BM + r < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
+        }
+      }
+    }
+#elif FQ_DEC_L2PF_WIDE
+    // ======================= L2 prefetch of this CTA's weight slice =======================
+    // The packed ring keeps only ~5 K-blocks per CTA in flight (Little's law at the HBM latency
+    // under load: ~30 GB/s per CTA); bulk prefetches into L2 (no shared memory, 256-byte x 128-row
+    // boxes, a few instructions per CTA) keep the rest of the slice in flight, so the ring's loads
+    // hit L2.  Consumption order (the rotated K walk), from the first block the ring prefill misses.
+    if (lane == 0) {
+      if (!(pdl & PDL_P)) tc::griddep_wait();
+      const int per = 256 / PROW;                           // super-blocks per prefetch box
+      const int pre = nsb < PSTAGES ? nsb : PSTAGES;
+      for (int u = pre; u < nsb;) {
+        const int kb = kb_of(u);
+        int run = 1;                                        // consecutive super-blocks (no wrap)
+        while (run < per && u + run < nsb && kb_of(u + run) == kb + run) ++run;
+        tc::tma_prefetch_l2_2d(&tmWpf, kb * PROW, fb * BM);
+        u += run;
+      }
+    }
+#endif
+    __syncwarp();
   } else if (warp == MMA_WARP) {
     // ======================= MMA issuer =======================
     if (lane == 0) {
@@ -881,7 +922,7 @@ static cudaError_t dec_launch_cfg(const GemmArgs& a, int split, const FdArgs* f)
   static std::atomic<uint64_t> attr_done[5];   // per kernel variant: devices configured
   const int which = a.out_i32 ? 0 : (a.y_bf16 ? 1 : 2) + (asym ? 2 : 0);
   const int TN = int((a.T + 15) / 16) * 16;
-  CUtensorMap mw{}, ma{};
+  CUtensorMap mw{}, ma{}, mwpf{};
   {
     const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.N)};
     const uint64_t strides[1] = {uint64_t(a.K / 2)};
@@ -889,6 +930,12 @@ static cudaError_t dec_launch_cfg(const GemmArgs& a, int split, const FdArgs* f)
     if (!tmap_encode(&mw, a.qw, 1, 2, dims, strides, box,
                      DC::KP == 2 ? TMAP_SW128 : (TMEMW ? TMAP_SW64 : TMAP_SW_NONE)))
       return cudaErrorInvalidValue;
+  }
+  {
+    const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.N)};
+    const uint64_t strides[1] = {uint64_t(a.K / 2)};
+    const uint32_t box[2] = {uint32_t(std::min(256, a.K / 2)), BM};   // L2 prefetch boxes (32 KB)
+    if (!tmap_encode(&mwpf, a.qw, 1, 2, dims, strides, box, TMAP_SW_NONE)) return cudaErrorInvalidValue;
   }
   {
     const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.T)};
@@ -928,7 +975,7 @@ static cudaError_t dec_launch_cfg(const GemmArgs& a, int split, const FdArgs* f)
                  FUSED ? " (fused transform)" : "", a.N, a.K, (long long)a.T, CFG, S, fbs * S,
                  dec_max_clusters<CFG, FUSED>(reinterpret_cast<const void*>(kern), S));
   cudaError_t e = launch_pdl_policy(kern, dim3(unsigned(fbs * S)), dim3(THREADS), DC::SMEM, a.stream, S,
-                                    dec_policy(), mw, ma, a.sa, int(a.T), TN, a.K, a.sw, a.N, a.y, a.za, a.colsum, S,
+                                    dec_policy(), mw, ma, mwpf, a.qw, a.sa, int(a.T), TN, a.K, a.sw, a.N, a.y, a.za, a.colsum, S,
                                     a.pdl, fd);
   count_launch();
   if (e != cudaSuccess) return e;

@@ -26,6 +26,10 @@ if [ -z "$NO_NCU" ]; then
   done
   timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemm_dec -s 2 -c 1 -f \
     -o gpurun_out/prof_dec_P_a python scripts/prof_kernels.py --config C4 --linear P_a > gpurun_out/ncu_dec.log 2>&1
+  timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemm_dec -s 2 -c 1 -f \
+    -o gpurun_out/prof_fused_P_a python scripts/prof_kernels.py --config C4 --linear P_a --fused > gpurun_out/ncu_fused.log 2>&1
+  timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemm_dec -s 2 -c 1 -f \
+    -o gpurun_out/prof_fused_P_ug python scripts/prof_kernels.py --config C4 --linear P_ug --fused > gpurun_out/ncu_fused_ug.log 2>&1
   mkdir -p gpurun_out/prof
   cp profiles/ncu_traffic.json gpurun_out/prof/ 2>/dev/null
   python scripts/make_profiles.py ${TAG:-r2a} gpurun_out gpurun_out/prof > gpurun_out/make_profiles.log 2>&1

@@ -15,6 +15,7 @@ ap.add_argument("--config", default="C3")
 ap.add_argument("--linear", default="P_ug")
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--gemm-impl", type=int, default=0)
+ap.add_argument("--fused", action="store_true", help="fq_flatquant_linear (the fused decode linear at T <= 64)")
 a = ap.parse_args()
 cfg = synth.config(a.config)
 lin = [l for l in cfg["linears"] if l.name == a.linear][0]
@@ -27,6 +28,9 @@ qw = torch.from_numpy(synth.random_codes(lin.N, lin.K // 2, seed=0).view(np.uint
 sw = torch.from_numpy(synth.random_scales(lin.N)).to(dev)
 fq.fq_set_gemm_impl(a.gemm_impl)
 for _ in range(a.iters):
+    if a.fused:
+        y = fq.flatquant_linear(x, lin.n1, lin.n2, p1, p2, 0.9, qw, sw)
+        continue
     q, s = fq.transform_quant(x, lin.n1, lin.n2, p1, p2, 0.9)
     y = fq.w4a4_linear(q, s, qw, sw)
 torch.cuda.synchronize()
