@@ -228,6 +228,12 @@ FQ_DEVICE unsigned ld_acquire_gpu(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+FQ_DEVICE unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+FQ_DEVICE void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;\n" ::: "memory"); }
 FQ_DEVICE void red_release_gpu_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
@@ -404,9 +410,11 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         // activation codes are then read through the async proxy (TMA)
         const unsigned need = unsigned(fd.ntiles);
         const long long t_start = clock64();
-        while (ld_acquire_gpu(fd.sync) < need) {
+        // relaxed polling (an acquire load per poll invalidates L1 each time), one acquire fence
+        while (ld_relaxed_gpu(fd.sync) < need) {
           if (clock64() - t_start > (1ll << 32)) __trap();    // never hang the GPU: ~2 s without progress
         }
+        fence_acq_rel_gpu();
         fence_proxy_async_global();
         dtrace(tslot, 118);
         tc::mbar_arrive(actready);

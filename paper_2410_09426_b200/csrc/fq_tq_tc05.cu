@@ -80,7 +80,10 @@ constexpr int SMEM_OVERHEAD = 1024 + 512;  // 1024-B alignment slack + barriers/
 // DESIGN.md reading R22): stage 1 only, its fp32 result quantized directly (no fp16 intermediate,
 // no D2 in TMEM); the A2 buffer is the staging area that turns TMEM's column-per-lane layout into
 // row-major packed codes.
-template <int N1, int N2, bool SMALL = false, bool IDENT2 = false>
+// SMALL = 2 (MULTI, experiment): one epilogue group, two X stages, no aliasing, a few tiles per
+// CTA and several CTAs per SM, so the hardware block scheduler hands the tiles to SMs as they
+// free up (e.g. while the preceding GEMM's last wave drains).
+template <int N1, int N2, int SMALL = 0, bool IDENT2 = false>
 struct Cfg {
   static_assert(N2 == 64 || N2 == 128, "n2 in {64, 128}");
   static_assert(N1 % 16 == 0 && N1 >= 16 && N1 <= 128, "n1 multiple of 16, <= 128");
@@ -101,10 +104,10 @@ struct Cfg {
   static constexpr int THREADS = (4 + 4 * GROUPS) * 32;
   static constexpr int TMEM_USED = GROUPS * (D1C + D2C);
   static constexpr int TMEM_COLS = TMEM_USED <= 128 ? 128 : (TMEM_USED <= 256 ? 256 : 512);
-  static constexpr bool ALIAS_A2 = SMALL && !IDENT2;          // A2 over P1 + X (one tile per CTA)
+  static constexpr bool ALIAS_A2 = SMALL == 1 && !IDENT2;     // A2 over P1 + X (one tile per CTA)
   static constexpr int FIXED = P1_BYTES + (IDENT2 ? 0 : P2_BYTES) + (ALIAS_A2 ? 0 : GROUPS * A2_BYTES);
   static constexpr int STAGES_FIT = (SMEM_LIMIT - SMEM_OVERHEAD - FIXED) / X_BYTES;
-  static constexpr int STAGES = SMALL ? 1 : (STAGES_FIT > 8 ? 8 : STAGES_FIT);
+  static constexpr int STAGES = SMALL == 1 ? 1 : SMALL == 2 ? 2 : (STAGES_FIT > 8 ? 8 : STAGES_FIT);
   static constexpr size_t SMEM = size_t(FIXED) + size_t(STAGES) * X_BYTES + SMEM_OVERHEAD;
   static_assert(TMEM_USED <= 512, "TMEM budget");
   static_assert(SMALL || STAGES >= 2, "shared-memory budget");
@@ -170,7 +173,7 @@ FQ_DEVICE void row_chunks(uint32_t taddr, const uint32_t* regs, F&& fn) {
   }
 }
 
-template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM, bool SMALL = false, bool IDENT2 = false>
+template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM, int SMALL = 0, bool IDENT2 = false>
 __global__ void __launch_bounds__(Cfg<N1, N2, SMALL, IDENT2>::THREADS, 1)
 tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmP1,
                const __grid_constant__ CUtensorMap tmP2, int64_t T, float alpha, uint8_t* __restrict__ q,
@@ -248,13 +251,7 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     for (int k = 0; k < prefill; ++k) issue_x(k);
     trace(1);
   }
-  if (warp == 2) {
-    tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
-    if (lane == 0) {
-      tc::griddep_wait();              // dependents launch only after this kernel's wait returned
-      tc::griddep_launch();
-    }
-  }
+  if (warp == 2) tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -270,6 +267,14 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     inv_p2 = exp2i(-bf16_to_f16_pow2(sP2, C::P2_BYTES / 2, &p2max));
   } else {
     __syncthreads();
+  }
+  // PDL protocol (fq_internal.h): dependents launch only after this kernel's griddepcontrol.wait
+  // has returned.  One thread waits (round 2c: after the last CTA-wide barrier before the roles,
+  // not in front of it) while the other warps already compute; outputs are written before the
+  // wait only if the host allowed it (PDL_OUT), see `waited` below.
+  if (warp == 2 && lane == 0) {
+    tc::griddep_wait();
+    tc::griddep_launch();
   }
 
   if (warp == 0) {
@@ -637,6 +642,14 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
 }
 
 // ------------------------------------------------------------------------------ host side
+static int multi_tpc() {                           // FQ_TQ_MULTI=<tiles per CTA>: experiment (MULTI)
+  static const int v = [] {
+    const char* e = std::getenv("FQ_TQ_MULTI");
+    return e ? std::max(0, std::atoi(e)) : 0;
+  }();
+  return v;
+}
+
 static bool small_enabled() {                      // FQ_TQ_SMALL=0: testing aid (large config)
   static const bool on = [] {
     const char* v = std::getenv("FQ_TQ_SMALL");
@@ -645,7 +658,7 @@ static bool small_enabled() {                      // FQ_TQ_SMALL=0: testing aid
   return on;
 }
 
-template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM = false, bool SMALL = false, bool IDENT2 = false>
+template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM = false, int SMALL = 0, bool IDENT2 = false>
 static cudaError_t launch(const TQArgs& a) {
   using C = Cfg<N1, N2, SMALL, IDENT2>;
   auto kern = tq_tc05_kernel<N1, N2, BF16, WRITE_Y, ASYM, SMALL, IDENT2>;
@@ -673,7 +686,7 @@ static cudaError_t launch(const TQArgs& a) {
     if (!tmap_encode(&m2, a.p2, 2, 2, dims, strides, box, TMAP_SW128)) return cudaErrorInvalidValue;
   }
   const int64_t tiles = (a.T + C::TOK - 1) / C::TOK;
-  const int grid = int(std::min<int64_t>(tiles, num_sms()));
+  const int grid = SMALL == 2 ? int((tiles + multi_tpc() - 1) / multi_tpc()) : int(std::min<int64_t>(tiles, num_sms()));
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(C::THREADS), C::SMEM, a.stream, 1, mx, m1, m2, a.T, a.alpha,
                              a.q, a.scale, a.y, a.zero, a.pdl);
   count_launch();
@@ -692,7 +705,9 @@ template <int N1, int N2>
 static cudaError_t dispatch(const TQArgs& a) {
   if (a.zero) return a.bf16 ? launch<N1, N2, true, false, true>(a) : launch<N1, N2, false, false, true>(a);
   if (a.T <= 64 && !a.y && small_enabled())       // decode (C4) launches: one tile per CTA
-    return a.bf16 ? launch<N1, N2, true, false, false, true>(a) : launch<N1, N2, false, false, false, true>(a);
+    return a.bf16 ? launch<N1, N2, true, false, false, 1>(a) : launch<N1, N2, false, false, false, 1>(a);
+  if (multi_tpc() > 0 && !a.y)                    // experiment: a few tiles per CTA, several CTAs per SM
+    return a.bf16 ? launch<N1, N2, true, false, false, 2>(a) : launch<N1, N2, false, false, false, 2>(a);
   if (a.bf16) return a.y ? launch<N1, N2, true, true>(a) : launch<N1, N2, true, false>(a);
   return a.y ? launch<N1, N2, false, true>(a) : launch<N1, N2, false, false>(a);
 }
