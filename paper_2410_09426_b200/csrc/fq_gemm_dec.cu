@@ -584,8 +584,11 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         const uint32_t w0 = smem_u32(sW + size_t(st) * W_BYTES);
         if constexpr (TMEMW) {
           const uint32_t wt = tmem_base + uint32_t(W_COL0 + st * WT_COLS);
+#ifndef FQ_EXP_DEC_NMMA
+#define FQ_EXP_DEC_NMMA (BK / UK)      // experiment builds only: fewer MMAs per K-block (timing)
+#endif
 #pragma unroll
-          for (int k = 0; k < BK / UK; ++k)
+          for (int k = 0; k < FQ_EXP_DEC_NMMA; ++k)
             tc::mma_ts<true>(tmem_base, wt + uint32_t(k * (UK / 4)), tc::sdesc_sw128(w0 + k * UK, 16, 1024), idesc,
                              (j | k) != 0);
         } else {

@@ -68,6 +68,10 @@ FQ_DEVICE void cta_stamp(int) {}
 #endif
 
 constexpr int MAX_GROUPS = 4;
+// per-launch {claims, departures} counter pairs of the dynamic tile schedule: a ring of slots in
+// this module's device memory, handed out round-robin per device, reset by each launch's last CTA
+constexpr int TQ_SLOTS = 1024;
+__device__ unsigned g_tq_sync[2 * TQ_SLOTS];
 constexpr int SMEM_LIMIT = 232448;       // max dynamic smem per block on sm_100
 constexpr int SMEM_OVERHEAD = 1024 + 512;  // 1024-B alignment slack + barriers/scratch
 
@@ -177,8 +181,18 @@ template <int N1, int N2, bool BF16, bool WRITE_Y, bool ASYM, int SMALL = 0, boo
 __global__ void __launch_bounds__(Cfg<N1, N2, SMALL, IDENT2>::THREADS, 1)
 tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmP1,
                const __grid_constant__ CUtensorMap tmP2, int64_t T, float alpha, uint8_t* __restrict__ q,
-               float* __restrict__ scale, float* __restrict__ y_out, int8_t* __restrict__ zero, int pdl) {
+               float* __restrict__ scale, float* __restrict__ y_out, int8_t* __restrict__ zero, int pdl,
+               unsigned* __restrict__ tsync) {
   using C = Cfg<N1, N2, SMALL, IDENT2>;
+  // Tile schedule.  DYN (the persistent configuration): every CTA starts with a static chunk of CH
+  // tiles and then claims further chunks from a per-launch counter, so CTAs that become resident
+  // early -- on the SMs the preceding GEMM's last wave leaves idle (PDL) -- take more of the work
+  // than CTAs placed after that GEMM has drained.  Otherwise (SMALL, IDENT2) tiles are strided.
+  // Either way the producer publishes each tile index with its X stage (tile_id, -1 = end), the
+  // stage-1 MMA thread forwards it per sequence index (seq_tile + tready) to the epilogue groups and
+  // the stage-2 MMA thread, which all stop at the first -1.
+  constexpr bool DYN = !SMALL && !IDENT2;
+  constexpr int CH = 2;                                   // tiles per claim
   constexpr int S = C::STAGES, TOK = C::TOK, G = C::GROUPS, THREADS = C::THREADS;
   constexpr uint32_t IDESC1 = tc::idesc_f16(128, N1, BF16 ? 1 : 0, 1, 1);
   constexpr uint32_t IDESC2 = tc::idesc_f16(128, N2, 0, 1, 1);
@@ -197,8 +211,11 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
   uint64_t* d1full = pfull + 1;      // [G]  MMA commit -> epilogue group
   uint64_t* a2full = d1full + G;     // [G]  epilogue group (4 warps) -> MMA
   uint64_t* d2full = a2full + G;     // [G]  MMA commit -> epilogue group
+  uint64_t* tready = d2full + G;     // [G]  stage-1 MMA thread: tile index of the group's next tile
   __shared__ float red[MAX_GROUPS * 8];                        // [groups][2 parities][4 warps]
   __shared__ uint32_t tmem_slot[1];
+  __shared__ int tile_id[8];                                   // [S] tile of each X stage (-1: end)
+  __shared__ int seq_tile[32];                                 // [k % 32] tile of sequence index k
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -209,17 +226,28 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
   const int my_tiles = num_tiles > int(blockIdx.x) ? (num_tiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
 
   // X tiles stream into the ring as early as possible (before the TMEM allocation completes)
-  auto issue_x = [&](int k) {
-    const int s = k % S;
+  int kq = 0;                                            // producer's sequence index
+  auto issue_tile = [&](int tile) {
+    const int k = kq++, s = k % S;
     tc::mbar_wait(&xempty[s], ((k / S) & 1) ^ 1);
+    tile_id[s] = tile;                                   // published by the arrive (release) below
     tc::mbar_expect_tx(&xfull[s], C::X_BYTES);
-    const int t0 = (int(blockIdx.x) + k * int(gridDim.x)) * TOK;
     uint8_t* dst = sX + size_t(s) * C::X_BYTES;
 #pragma unroll
-    for (int b = 0; b < C::JB; ++b) tc::tma_load_3d(dst + b * TOK * N1 * 128, &tmX, &xfull[s], b * 64, 0, t0);
+    for (int b = 0; b < C::JB; ++b) tc::tma_load_3d(dst + b * TOK * N1 * 128, &tmX, &xfull[s], b * 64, 0, tile * TOK);
     if (k < 16) trace(8 + k);
   };
-  const int prefill = my_tiles < S ? my_tiles : S;
+  auto issue_end = [&] {
+    const int k = kq, s = k % S;
+    tc::mbar_wait(&xempty[s], ((k / S) & 1) ^ 1);
+    tile_id[s] = -1;
+    tc::mbar_arrive(&xfull[s]);
+  };
+  // DYN: static first chunk [CH b, CH b + CH); strided: tiles b, b + grid, ...
+  const int first_n = DYN ? (CH < num_tiles - CH * int(blockIdx.x) ? CH : num_tiles - CH * int(blockIdx.x)) : my_tiles;
+  auto static_tile = [&](int k) { return DYN ? CH * int(blockIdx.x) + k : int(blockIdx.x) + k * int(gridDim.x); };
+  const int prefill = first_n < S ? first_n : S;
+  unsigned nxt = 0;                                      // DYN: the claim in flight (producer thread)
   if (threadIdx.x == 0) {
     tc::tma_prefetch_desc(&tmX);
     tc::tma_prefetch_desc(&tmP1);
@@ -233,8 +261,10 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
       tc::mbar_init(&d1full[b], 1);
       tc::mbar_init(&a2full[b], 4);
       tc::mbar_init(&d2full[b], 1);
+      tc::mbar_init(&tready[b], 1);
     }
     tc::fence_barrier_init();
+    if constexpr (DYN) nxt = atomicAdd(tsync, 1u);      // first claim: its latency hides behind the loads
     // PDL (fq_internal.h): P1, P2 and X stream in while the preceding kernel finishes unless it
     // writes them (host-side hazard check, fq_abi.cu)
     auto load_p = [&] {
@@ -248,7 +278,7 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     if ((pdl & (PDL_P | PDL_X)) != (PDL_P | PDL_X)) tc::griddep_wait();
     if (!(pdl & PDL_P)) load_p();
     trace(4);
-    for (int k = 0; k < prefill; ++k) issue_x(k);
+    for (int k = 0; k < prefill; ++k) issue_tile(static_tile(k));
     trace(1);
   }
   if (warp == 2) tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -279,8 +309,22 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
 
   if (warp == 0) {
     // ================================ TMA producer ================================
-    if (lane == 0)
-      for (int k = prefill; k < my_tiles; ++k) issue_x(k);
+    if (lane == 0) {
+      for (int k = prefill; k < first_n; ++k) issue_tile(static_tile(k));
+      if constexpr (DYN) {
+        for (;;) {                                       // claim chunks until the tiles run out
+          const int base = CH * (int(gridDim.x) + int(nxt));
+          if (base >= num_tiles) break;
+          nxt = atomicAdd(tsync, 1u);                    // the next claim travels while this chunk loads
+          for (int i = 0; i < CH && base + i < num_tiles; ++i) issue_tile(base + i);
+        }
+        if (atomicAdd(tsync + 1, 1u) == gridDim.x - 1) {   // last CTA out: every claim is made, reset
+          atomicExch(tsync, 0u);
+          atomicExch(tsync + 1, 0u);
+        }
+      }
+      issue_end();
+    }
     __syncwarp();
   } else if (warp == 1 || warp == 3) {
     // ================================ MMA issuers ================================
@@ -290,8 +334,6 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
       const uint32_t p1a = smem_u32(sP1), p2a = smem_u32(sP2);
       auto mma1 = [&](int k) {
         const int s = k % S, par = k % G;
-        tc::mbar_wait(&xfull[s], (k / S) & 1);
-        tc::fence_after();
         if (k < 16) trace(24 + k);
         const uint32_t xs = smem_u32(sX + size_t(s) * C::X_BYTES);
 #pragma unroll
@@ -310,8 +352,6 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
       };
       auto mma2 = [&](int k) {
         const int par = k % G;
-        tc::mbar_wait(&a2full[par], (k / G) & 1);
-        tc::fence_after();
         if (k < 16) trace(40 + k);
         const uint32_t a0 = smem_u32(sA2 + par * C::A2_BYTES);
         const uint32_t d = tmem + uint32_t(G * C::D1C + par * N2);
@@ -323,12 +363,32 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
       };
       if (warp == 1) {
         // D1 slot k % G is free once the group finished the stage-1 epilogue of tile k - G
-        for (int k = 0; k < my_tiles; ++k) {
+        for (int k = 0;; ++k) {
+          const int s = k % S;
+          tc::mbar_wait(&xfull[s], (k / S) & 1);
+          tc::fence_after();
+          const int tile = *static_cast<volatile int*>(&tile_id[s]);
+          if (tile < 0) {                                // end: tell each group (and warp 3) in turn
+            for (int g = 0; g < G; ++g) {
+              const int kk = k + g;
+              if (kk >= G) tc::mbar_wait(&a2full[kk % G], ((kk - G) / G) & 1);
+              seq_tile[kk % 32] = -1;
+              tc::mbar_arrive(&tready[kk % G]);
+            }
+            break;
+          }
           if (k >= G) tc::mbar_wait(&a2full[k % G], ((k - G) / G) & 1);
+          seq_tile[k % 32] = tile;
+          tc::mbar_arrive(&tready[k % G]);
           mma1(k);
         }
       } else if constexpr (!IDENT2) {
-        for (int k = 0; k < my_tiles; ++k) mma2(k);
+        for (int k = 0;; ++k) {
+          tc::mbar_wait(&a2full[k % G], (k / G) & 1);    // the group's stage-1 epilogue (or its end)
+          tc::fence_after();
+          if (*static_cast<volatile int*>(&seq_tile[k % 32]) < 0) break;
+          mma2(k);
+        }
         trace(122);
       }
     }
@@ -353,10 +413,17 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     constexpr int QROW = N2 / 2;                         // packed bytes per row i of a token
     constexpr int QTOK = N1 * N2 / 2;                    // packed bytes per token
     bool waited = (pdl & PDL_OUT) != 0;                  // outputs written before the wait only if allowed
-    for (int k = grp; k < my_tiles; k += G) {
+    for (int k = grp;; k += G) {
       const int par = grp;                               // == k % G
       const uint32_t ph = (k / G) & 1;
-      const int64_t t0 = int64_t(int(blockIdx.x) + k * int(gridDim.x)) * TOK;
+      tc::mbar_wait(&tready[par], ph);
+      const int tile = *static_cast<volatile int*>(&seq_tile[k % 32]);
+      if (tile < 0) {                                    // end: release warp 3 (it reads the -1 too)
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&a2full[par]);
+        break;
+      }
+      const int64_t t0 = int64_t(tile) * TOK;
       if constexpr (IDENT2) {
         // ---- P2 = I: D1 lane j, column i holds Y_t[i][j] (fp32, the whole token in 128 lanes) ----
         tc::mbar_wait(&d1full[par], ph);
@@ -642,6 +709,19 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
 }
 
 // ------------------------------------------------------------------------------ host side
+static unsigned* tq_sync_slot() {
+  static unsigned* base[64] = {nullptr};
+  static std::atomic<uint32_t> next[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!base[dev]) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_tq_sync) != cudaSuccess) return nullptr;
+    base[dev] = static_cast<unsigned*>(p);
+  }
+  return base[dev] + 2 * (next[dev].fetch_add(1, std::memory_order_relaxed) % TQ_SLOTS);
+}
+
 static int multi_tpc() {                           // FQ_TQ_MULTI=<tiles per CTA>: experiment (MULTI)
   static const int v = [] {
     const char* e = std::getenv("FQ_TQ_MULTI");
@@ -686,9 +766,18 @@ static cudaError_t launch(const TQArgs& a) {
     if (!tmap_encode(&m2, a.p2, 2, 2, dims, strides, box, TMAP_SW128)) return cudaErrorInvalidValue;
   }
   const int64_t tiles = (a.T + C::TOK - 1) / C::TOK;
-  const int grid = SMALL == 2 ? int((tiles + multi_tpc() - 1) / multi_tpc()) : int(std::min<int64_t>(tiles, num_sms()));
+  constexpr bool DYN = !SMALL && !IDENT2;
+  unsigned* tsync = nullptr;
+  int grid;
+  if (DYN) {                                      // static first chunk of 2 tiles per CTA, then claims
+    grid = int(std::min<int64_t>((tiles + 1) / 2, num_sms()));
+    tsync = tq_sync_slot();
+    if (!tsync) return cudaErrorInvalidValue;
+  } else {
+    grid = SMALL == 2 ? int((tiles + multi_tpc() - 1) / multi_tpc()) : int(std::min<int64_t>(tiles, num_sms()));
+  }
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(C::THREADS), C::SMEM, a.stream, 1, mx, m1, m2, a.T, a.alpha,
-                             a.q, a.scale, a.y, a.zero, a.pdl);
+                             a.q, a.scale, a.y, a.zero, a.pdl, tsync);
   count_launch();
   return e;
 }
