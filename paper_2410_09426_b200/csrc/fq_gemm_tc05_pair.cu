@@ -164,7 +164,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmY32,
                  const float* __restrict__ sa, int T, int K, const float* __restrict__ sw, int N,
-                 void* __restrict__ yv, const int8_t* __restrict__ za, const int32_t* __restrict__ colsum) {
+                 void* __restrict__ yv, const int8_t* __restrict__ za, const int32_t* __restrict__ colsum,
+                 int pdl) {
   using GE = Geo<BN>;
   constexpr int BN_CTA = GE::BN_CTA, B_BYTES = GE::B_BYTES, P_BYTES = GE::P_BYTES, TMEM_A0 = GE::TMEM_A0;
   constexpr int B_ATOM = GE::B_ATOM, B_TASKS = GE::B_TASKS;
@@ -225,8 +226,11 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   tc::cluster_sync();            // peer barriers initialised before any remote arrive
   tc::fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  tc::griddep_wait();                            // qa / sa written by the previous kernel are visible
-  if (threadIdx.x == 0) tc::griddep_launch();   // dependents launch only after the wait (fq_internal.h)
+  // PDL (round 2c): only the TMA thread waits for the preceding kernel -- after it has requested
+  // the weight (B) halves of its first ring stages, when the host found the weights are not
+  // written by that kernel (PDL_P).  Everything else in this kernel is ordered after the wait
+  // through the ring: the converters, the MMAs, and the epilogue (which reads sa and writes y)
+  // all consume activation data the TMA thread requested after its wait.
 
   // Every converter warp signals the leader's `full` barrier on its own (CTA-scope arrive in the
   // leader, release.cluster remote arrive from the peer), so the A and B paths and the warps of
@@ -249,13 +253,29 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     if (lane == 0) {
       Cursor ld;
       ld.init(sc);
+      int pre = 0;                                   // ring stages whose B half left before the wait
+#ifndef FQ_PAIR_PREB
+#define FQ_PAIR_PREB 1                                 // (experiment builds: 0 = no early weights)
+#endif
+      if (FQ_PAIR_PREB && (pdl & PDL_P)) {
+        Cursor pb = ld;
+        for (; pre < PSTAGES && pb.valid; ++pre, pb.next(sc)) {
+          tc::mbar_expect_tx(&pfull[pre], P_BYTES);
+          tc::tma_load_2d(sP + size_t(pre) * P_BYTES + AP_BYTES, &tmB, &pfull[pre], pb.kb * (BK / 2),
+                          pb.nb * BN + int(rank) * BN_CTA);
+        }
+      }
+      tc::griddep_wait();                        // qa / sa written by the previous kernel are visible
+      tc::griddep_launch();                      // dependents launch only after the wait (fq_internal.h)
       for (int j = 0; ld.valid; ++j, ld.next(sc)) {
         const int sp = j % PSTAGES;
-        tc::mbar_wait(&pempty[sp], ((j / PSTAGES) & 1) ^ 1);
-        tc::mbar_expect_tx(&pfull[sp], P_BYTES);
         uint8_t* dst = sP + size_t(sp) * P_BYTES;
+        if (j >= pre) {
+          tc::mbar_wait(&pempty[sp], ((j / PSTAGES) & 1) ^ 1);
+          tc::mbar_expect_tx(&pfull[sp], P_BYTES);
+          tc::tma_load_2d(dst + AP_BYTES, &tmB, &pfull[sp], ld.kb * (BK / 2), ld.nb * BN + int(rank) * BN_CTA);
+        }
         tc::tma_load_2d(dst, &tmA, &pfull[sp], ld.kb * (BK / 2), ld.mb * BM + int(rank) * BM_CTA);
-        tc::tma_load_2d(dst + AP_BYTES, &tmB, &pfull[sp], ld.kb * (BK / 2), ld.nb * BN + int(rank) * BN_CTA);
       }
     }
     __syncwarp();
@@ -467,8 +487,9 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         // float(256 acc) * (s_a / 256) is exactly float(acc) * s_a (power-of-two scaling).
         // Asymmetric: acc_true = acc - (z - 8) colsum_w is formed after the exact >> 8, in int32
         // (|acc_true| <= 120 K), so it cannot wrap for any supported K.
-        const float s_a = row_ok ? sa[row] * (ASYM ? 1.0f : 1.0f / 256.0f) : 0.f;
-        const int zc = (ASYM && row_ok) ? int(za[row]) : 0;
+        // (L2 loads: this thread did not execute the PDL wait itself, see the TMA producer)
+        const float s_a = row_ok ? __ldcg(sa + row) * (ASYM ? 1.0f : 1.0f / 256.0f) : 0.f;
+        const int zc = (ASYM && row_ok) ? int(__ldcg(za + row)) : 0;
         // one chunk of NC (64 or 32) columns: TMEM -> dequant -> swizzled staging -> TMA store
         auto emit = [&](auto nc_tag, int c0off) {
           constexpr int NC = decltype(nc_tag)::value;
@@ -634,7 +655,7 @@ static cudaError_t launch_bn(const GemmArgs& a) {
   const int num_tiles = int((a.T + BM - 1) / BM) * ((a.N + BN - 1) / BN);
   const int clusters = std::max(1, std::min(num_tiles, num_sms() / 2));
   cudaError_t e = launch_pdl(kern, dim3(unsigned(2 * clusters)), dim3(THREADS), GE::SMEM_BYTES, a.stream, 2, ma, mb,
-                             my, my32, a.sa, int(a.T), a.K, a.sw, a.N, a.y, a.za, a.colsum);
+                             my, my32, a.sa, int(a.T), a.K, a.sw, a.N, a.y, a.za, a.colsum, a.pdl);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

@@ -38,7 +38,7 @@ namespace tqw {
 constexpr int N1 = 128;
 constexpr int SMEM_LIMIT = 232448;
 constexpr int SMEM_OVERHEAD = 1024 + 512;
-constexpr int THREADS = 8 * 32;
+constexpr int THREADS = 12 * 32;                 // round 2c: two epilogue groups (stage 1 / stage 2)
 constexpr int R2 = 256;                          // TMEM column of region R2 (D2)
 constexpr float MAGIC = 12582912.0f;             // 1.5 * 2^23: fma(y, c, MAGIC) rounds half-to-even
 
@@ -117,7 +117,9 @@ tq_wide_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
   uint64_t* a2full = d1full + 1;     // epilogue (4 warps) -> stage-2 MMA
   uint64_t* d2full = a2full + 1;     // stage-2 commit -> epilogue
   uint64_t* d2empty = d2full + 1;    // epilogue (4 warps) -> next stage-2 MMA
-  __shared__ float red[8];           // [2 parities][4 warps]
+  uint64_t* peready = d2empty + 1;   // [2] stage-1 group -> stage-2 group: token's prescale exponent
+  __shared__ float red[16];          // [group][2 parities][4 warps]
+  __shared__ int pe_buf[2];          // prescale exponent of token k, slot k % 2
   __shared__ uint32_t tmem_slot[1];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -145,6 +147,8 @@ tq_wide_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     tc::mbar_init(a2full, 4);
     tc::mbar_init(d2full, 1);
     tc::mbar_init(d2empty, 4);
+    tc::mbar_init(&peready[0], 4);
+    tc::mbar_init(&peready[1], 4);
     tc::fence_barrier_init();
     auto load_p = [&] {                // PDL (fq_internal.h): before the wait unless the predecessor writes them
       tc::mbar_expect_tx(pfull, C::P1_BYTES + C::P2_BYTES);
@@ -213,15 +217,20 @@ tq_wide_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     }
     __syncwarp();
   } else if (warp >= 4) {
-    // ================================ epilogue ================================
+    // ================================ epilogues ================================
+    // Round 2c: warps 4-7 run the stage-1 epilogue of every token, warps 8-11 the stage-2
+    // epilogue, so the stage-1 epilogue of token k+1 overlaps the stage-2 epilogue of token k
+    // (one group doing both serialised them: ~4.4 us per token and SM at 128 x 224).
+    const int grp = (warp - 4) >> 2;                     // 0: stage 1, 1: stage 2
     const int qd = warp & 3, i = qd * 32 + lane;        // TMEM lane == row i of the token
     const uint32_t lane_base = tmem + (uint32_t(qd * 32) << 16);
+    float* redg = red + grp * 8;
     int rp = 0;
     auto exchange = [&](float m) {                       // max over the token's 128 rows (m >= 0)
       m = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(m)));
-      if (lane == 0) red[rp * 4 + qd] = m;
-      named_bar_sync(1, 128);
-      const float r = fmaxf(fmaxf(red[rp * 4 + 0], red[rp * 4 + 1]), fmaxf(red[rp * 4 + 2], red[rp * 4 + 3]));
+      if (lane == 0) redg[rp * 4 + qd] = m;
+      named_bar_sync(1 + grp, 128);
+      const float r = fmaxf(fmaxf(redg[rp * 4 + 0], redg[rp * 4 + 1]), fmaxf(redg[rp * 4 + 2], redg[rp * 4 + 3]));
       rp ^= 1;
       return r;
     };
@@ -230,37 +239,45 @@ tq_wide_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     for (int k = 0; k < my_tiles; ++k) {
       const int64_t t = int64_t(blockIdx.x) + int64_t(k) * gridDim.x;
       const uint32_t ph = k & 1;
-      // -------- stage-1 epilogue: D1 (fp32) -> prescaled fp16 A operand, in place --------
-      tc::mbar_wait(d1full, ph);
-      tc::fence_after();
-      float m1 = 0.f;
+      if (grp == 0) {
+        // -------- stage-1 epilogue: D1 (fp32) -> prescaled fp16 A operand, in place --------
+        tc::mbar_wait(d1full, ph);
+        tc::fence_after();
+        float m1 = 0.f;
 #pragma unroll 1
-      for (int c = 0; c < N2; c += 32) {
-        uint32_t v[32];
-        tmem_ld32c(lane_base + uint32_t(c), v);
+        for (int c = 0; c < N2; c += 32) {
+          uint32_t v[32];
+          tmem_ld32c(lane_base + uint32_t(c), v);
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) m1 = max3f(m1, fabsf(__uint_as_float(v[e])), fabsf(__uint_as_float(v[e + 1])));
-      }
-      const int pe = prescale_exp(exchange(m1));
-      const float pre = exp2i(pe);
-      // chunk c (columns [c, c+32)) becomes A columns [c/2, c/2 + 16): only columns already read
+          for (int e = 0; e < 32; e += 2) m1 = max3f(m1, fabsf(__uint_as_float(v[e])), fabsf(__uint_as_float(v[e + 1])));
+        }
+        const int pe = prescale_exp(exchange(m1));
+        const float pre = exp2i(pe);
+        // chunk c (columns [c, c+32)) becomes A columns [c/2, c/2 + 16): only columns already read
 #pragma unroll 1
-      for (int c = 0; c < N2; c += 32) {
-        uint32_t v[32], h[16];
-        tmem_ld32c(lane_base + uint32_t(c), v);
+        for (int c = 0; c < N2; c += 32) {
+          uint32_t v[32], h[16];
+          tmem_ld32c(lane_base + uint32_t(c), v);
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-          h[e] = pack_half2(__uint_as_float(v[2 * e]) * pre, __uint_as_float(v[2 * e + 1]) * pre);
-        tmem_st16(lane_base + uint32_t(c / 2), h);
+          for (int e = 0; e < 16; ++e)
+            h[e] = pack_half2(__uint_as_float(v[2 * e]) * pre, __uint_as_float(v[2 * e + 1]) * pre);
+          tmem_st16(lane_base + uint32_t(c / 2), h);
+        }
+        tc::tmem_st_wait();
+        tc::fence_before();
+        if (i == 0) pe_buf[k & 1] = pe;                  // for the stage-2 group (peready below)
+        __syncwarp();
+        if (lane == 0) {
+          tc::mbar_arrive(a2full);
+          tc::mbar_arrive(&peready[k & 1]);              // two slots: this group is < 2 tokens ahead
+        }
+        continue;
       }
-      tc::tmem_st_wait();
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(a2full);
-
       // -------- stage-2 epilogue: absmax, clip, quantize, pack, store --------
       tc::mbar_wait(d2full, ph);
+      tc::mbar_wait(&peready[k & 1], (k >> 1) & 1);
       tc::fence_after();
+      const int pe = *static_cast<volatile int*>(&pe_buf[k & 1]);
       const uint32_t d2 = lane_base + uint32_t(R2);
       float m2 = 0.f, hi2 = 0.f, lo2 = 0.f;
 #pragma unroll 1
