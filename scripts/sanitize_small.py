@@ -1,5 +1,6 @@
 """One small launch of every product kernel (transform: tcgen05 64x64, 112x128, wide 128x224, asym,
-P2 = I; GEMM: pair kernel sym/asym, decode kernel; KV quant) for compute-sanitizer runs."""
+P2 = I, SMALL decode config; GEMM: pair kernel sym/asym, decode kernel; the fused decode linear;
+KV quant) for compute-sanitizer runs."""
 import os
 import sys
 
@@ -34,6 +35,17 @@ for T, N, K in [(300, 520, 4096), (40, 776, 2048)]:
     fq.w4a4_linear(qa, sa, qw, sw)
     za = torch.zeros((T,), dtype=torch.int8, device=dev)
     fq.w4a4_linear(qa, sa, qw, sw, za=za, colsum_w=fq.weight_colsum(qw))
+# fused decode linear (transform inside the decode GEMM launch) and the SMALL decode transform
+for T, N in [(40, 1024), (7, 512)]:
+    x = t(synth.activations(T, 4096, seed=5))
+    p1 = t(synth.well_conditioned(64, seed=5, tag="p1"))
+    p2 = t(synth.well_conditioned(64, seed=5, tag="p2"))
+    qw = t(O.pack_int4(synth.random_codes(N, 4096, seed=6)))
+    sw = t(synth.random_scales(N, seed=6))
+    fq.flatquant_linear(x, 64, 64, p1, p2, 0.9, qw, sw)
+x = t(synth.activations(20, 112 * 128, seed=7))
+fq.transform_quant(x, 112, 128, t(synth.well_conditioned(112, seed=7, tag="p1")), t(synth.well_conditioned(128, seed=7, tag="p2")), 0.9)
+torch.cuda.synchronize()
 kv = t(synth.activations(256, 128, seed=4, pivot_channels=0))
 fq.kv_quant(kv, t(synth.well_conditioned(128, seed=4, tag="ph")), 0.95)
 torch.cuda.synchronize()
