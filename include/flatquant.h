@@ -43,8 +43,12 @@
  *    transform when n1 % 16 == 0 and n2 % 16 == 0) need x, q, qa, qw, y and sw 16-byte
  *    aligned and row strides that are multiples of 16 bytes (FQ_ESHAPE otherwise).
  *  - Re-entrant.  Per-device kernel attributes are set once per (kernel, device), thread-safely;
- *    the only state is the per-stream record of the last launch's buffers (see Stream order),
- *    guarded by a mutex.
+ *    the host state is the per-stream record of the last launch's buffers (see Stream order),
+ *    guarded by a mutex.  Device state: the transform kernel's dynamic tile schedule and the
+ *    fused decode linear count through per-launch counter pairs taken round-robin from rings of
+ *    1024 slots per device in the library's own (module) device memory; each launch's last CTA
+ *    resets its slot, so CUDA-graph replays are safe.  At most 1024 such launches of each kind
+ *    may be in flight on one device at a time.
  *  - Non-finite inputs give unspecified codes (the oracle's precondition is finite x).
  */
 #ifndef FLATQUANT_H_
