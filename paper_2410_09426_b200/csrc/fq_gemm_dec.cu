@@ -412,7 +412,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         const long long t_start = clock64();
         // relaxed polling (an acquire load per poll invalidates L1 each time), one acquire fence
         while (ld_relaxed_gpu(fd.sync) < need) {
-          if (clock64() - t_start > (1ll << 32)) __trap();    // never hang the GPU: ~2 s without progress
+          if (clock64() - t_start > (1ll << 36)) __trap();    // never hang the GPU: ~35 s without progress
         }
         fence_acq_rel_gpu();
         fence_proxy_async_global();
