@@ -169,3 +169,19 @@ def test_fused_decode_not_taken_outside_its_shapes():
     fq.fq_flatquant_linear(x2, N1, N2, p1, p2, 0.9, qw, sw, y2, q2, s2)
     assert fq.fq_launch_count() - n0 == 2
     torch.cuda.synchronize()
+
+
+def test_fused_decode_concurrent_streams():
+    """fused launches on three streams at once (each takes its own counter slot; the ticket CTAs
+    are the lowest block indices of their grid, so they are resident whenever a spinning CTA is)"""
+    T, N = 64, 6144
+    x, p1, p2, qw, sw = _inputs(T, N, seed=31)
+    ref, _, _ = _two_kernels(x, p1, p2, 0.9, qw, sw)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    outs = [_bufs(T, N) for _ in range(9)]
+    for i, o in enumerate(outs):
+        _fused(x, p1, p2, 0.9, qw, sw, stream=streams[i % 3], bufs=o)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o[0], ref)
