@@ -4,7 +4,7 @@
 One step = the whole hot path over one batch of synthetic tokens:
 for every linear of the configuration, fq_transform_quant (Kronecker transform + clip + INT4
 quantize/pack) followed by fq_w4a4_linear (tcgen05 W4A4 GEMM + dequant epilogue) -- or, at decode
-sizes (T <= 64, 64 x 64 decomposition), fq_flatquant_linear, which runs both in ONE fused launch
+sizes (T <= 64, 64 x 64 or 112 x 128 decomposition), fq_flatquant_linear, which runs both in ONE fused launch
 (NEXT-4(i); --no-fused keeps the two calls).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
@@ -206,7 +206,7 @@ def fused_linear(T, lin):
     """The library runs fq_flatquant_linear as ONE fused launch (transform + quantize inside the
     decode GEMM, NEXT-4(i)) for T <= 64 with the 64 x 64 decomposition and fp16 activations
     (fq_gemm_dec.cu FUSED); the bench checks this against its launch count."""
-    return T <= 64 and lin.n1 == 64 and lin.n2 == 64
+    return T <= 64 and (lin.n1, lin.n2) in ((64, 64), (112, 128))
 
 
 def fused_bytes(T, lin):

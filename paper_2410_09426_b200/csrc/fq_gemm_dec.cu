@@ -139,7 +139,7 @@ static_assert(RED_BYTES <= STAGES * W_BYTES, "the partial tile reuses the widene
 #ifndef FQ_DEC_P1
 #define FQ_DEC_P1 (FQ_DEC_KP1 == 2 ? 7 : 14)
 #endif
-template <int CFG, bool FUSED = false>
+template <int CFG, int FUSED = 0>
 struct DecCfg {
   // FUSED: the transform tile of phase A borrows the widened-operand stages (48 KB), so the
   // one-CTA-per-SM configuration keeps at least 6 of them
@@ -155,7 +155,10 @@ struct DecCfg {
   static constexpr int TMEM_COLS = !TMEMW ? 64 : (W_COL0 + STAGES * WT_COLS <= 256 ? 256 : 512);
   static constexpr size_t SMEM = size_t(STAGES) * W_BYTES + size_t(PSTAGES) * PB + 1024 + (FUSED ? 512 : 256);
   static_assert(RED_BYTES <= STAGES * W_BYTES, "partial tile in the operand stages");
-  static_assert(!FUSED || STAGES * W_BYTES >= 48 * 1024, "phase-A transform tile in the operand stages");
+  // phase A (the transform tile, fd_geo below): 64 x 64 in the widened-operand stages, 112 x 128 in
+  // those stages plus the first packed ring stages (whose weights the ticket CTAs load afterwards)
+  static_assert(FUSED != 1 || STAGES * W_BYTES >= 48 * 1024, "64 x 64 phase A in the operand stages");
+  static_assert(FUSED != 2 || STAGES * W_BYTES + PSTAGES * PB >= 88 * 1024, "112 x 128 phase A");
   static_assert(!TMEMW || W_COL0 + STAGES * WT_COLS <= TMEM_COLS, "TMEM budget");
   static_assert(MINB == 1 || TMEM_COLS <= 256, "two CTAs per SM share the 512 TMEM columns");
   static_assert(SMEM * MINB <= 232448, "shared memory per SM");
@@ -212,16 +215,36 @@ constexpr int FD_SLOTS = 1024;
 __device__ unsigned g_fd_sync[2 * FD_SLOTS];
 
 struct alignas(64) FdParams {
-  CUtensorMap tmX, tmP1, tmP2;   // x [T][64][64] (box 64 x 64 x 2 tokens), P1, P2 [64][64] (SWIZZLE_128B)
+  CUtensorMap tmX, tmP1, tmP2;   // x [T][n1][n2] (box 64 x n1 x TOK tokens), P1, P2 (SWIZZLE_128B)
   float alpha;
-  uint8_t* q;                    // [T, 2048] packed codes (the caller's q_ws)
+  uint8_t* q;                    // [T, n/2] packed codes (the caller's q_ws)
   float* s;                      // [T] scales (s_ws)
   unsigned* sync;                // {arrivals, departures} of this launch's slot
-  int ntiles;                    // ticket CTAs = ceil(T / 2)
+  int ntiles;                    // ticket CTAs = ceil(T / TOK)
 };
-constexpr int FD_N = 64;                                  // n1 = n2 = 64
-constexpr int FD_X_BYTES = 2 * FD_N * 128, FD_P_BYTES = FD_N * 128, FD_A2_BYTES = 2 * FD_N * 128;
-constexpr uint32_t FD_IDESC = tc::idesc_f16(128, FD_N, 0, 1, 1);   // fp16 x fp16 -> fp32, both MN-major
+// Phase-A geometry (the same tiles as fq_tq_tc05.cu): F = 1 -> n1 = n2 = 64, two tokens per tile;
+// F = 2 -> 112 x 128 (LLaMA-3-8B down_proj), one token.  Layout in shared memory from offset 0:
+// F = 1: X | P1 | P2 | A2 (48 KB, the widened-operand stages); F = 2: P2 | P1 | X with the stage-2
+// operand A2 written over P1 + X once the stage-1 MMA has read them (88 KB).
+template <int F>
+struct FdGeo {
+  static constexpr int N1 = F == 2 ? 112 : 64, N2 = F == 2 ? 128 : 64;
+  static constexpr int TOK = N1 == 64 ? 2 : 1;
+  static constexpr int JB = N2 / 64, P1_ATOMS = (N1 + 63) / 64;
+  static constexpr int X_BYTES = TOK * JB * N1 * 128, P1_BYTES = P1_ATOMS * N1 * 128, P2_BYTES = JB * N2 * 128;
+  static constexpr int A2_BYTES = 2 * N2 * 128;
+  static constexpr bool ALIAS = F == 2;
+  static constexpr int OFF_P2 = ALIAS ? 0 : X_BYTES + P1_BYTES;
+  static constexpr int OFF_P1 = ALIAS ? P2_BYTES : X_BYTES;
+  static constexpr int OFF_X = ALIAS ? P2_BYTES + P1_BYTES : 0;
+  static constexpr int OFF_A2 = ALIAS ? OFF_P1 : X_BYTES + P1_BYTES + P2_BYTES;
+  static constexpr int BYTES = ALIAS ? P2_BYTES + P1_BYTES + X_BYTES : OFF_A2 + A2_BYTES;
+  static constexpr int LOAD_BYTES = X_BYTES + P1_BYTES + P2_BYTES;
+  static constexpr uint32_t IDESC1 = tc::idesc_f16(128, N1, 0, 1, 1);   // fp16 x fp16 -> fp32, MN-major
+  static constexpr uint32_t IDESC2 = tc::idesc_f16(128, N2, 0, 1, 1);
+  static_assert(TOK * N2 == 128, "one M = 128 stage-1 group per tile");
+  static_assert(!ALIAS || A2_BYTES <= P1_BYTES + X_BYTES, "A2 over P1 + X");
+};
 
 FQ_DEVICE unsigned ld_acquire_gpu(const unsigned* p) {
   unsigned v;
@@ -239,7 +262,7 @@ FQ_DEVICE void red_release_gpu_add(unsigned* p, unsigned v) {
 }
 FQ_DEVICE void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
 
-template <int CFG, bool OUT_I32, bool BF16, bool ASYM, bool FUSED = false>
+template <int CFG, bool OUT_I32, bool BF16, bool ASYM, int FUSED = 0>
 __global__ void __launch_bounds__(THREADS, DecCfg<CFG, FUSED>::MINB)
 gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA,
                 const __grid_constant__ CUtensorMap tmWpf, const uint8_t* __restrict__ qwp,
@@ -264,12 +287,14 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   uint64_t* fda2 = fd1 + 1;                //        stage-1 epilogue (4 warps) -> stage-2 MMA
   uint64_t* fd2 = fda2 + 1;                //        stage-2 MMA commit -> epilogue warps
   uint64_t* actready = fd2 + 1;            //        all tickets counted: codes and scales visible
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1 + (FUSED ? 5 : 0));
-  // FUSED phase A borrows the widened-operand stages: X tile | P1 | P2 | stage-2 A operand
-  uint8_t* fsX = sW;
-  uint8_t* fsP1 = sW + FD_X_BYTES;
-  uint8_t* fsP2 = fsP1 + FD_P_BYTES;
-  uint8_t* fsA2 = fsP2 + FD_P_BYTES;
+  uint64_t* fdone = actready + 1;          //        F = 2: phase-A buffers free (ring stages usable)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1 + (FUSED ? 6 : 0));
+  using FG = FdGeo<FUSED == 2 ? 2 : 1>;
+  // FUSED phase A borrows the widened-operand stages (and, F = 2, the first packed ring stages)
+  uint8_t* fsX = smem + FG::OFF_X;
+  uint8_t* fsP1 = smem + FG::OFF_P1;
+  uint8_t* fsP2 = smem + FG::OFF_P2;
+  uint8_t* fsA2 = smem + FG::OFF_A2;
   __shared__ float fd_red[8];                                // [2 parities][4 warps] token maxima
   const bool ticket = FUSED && int(blockIdx.x) < fd.ntiles;
   __shared__ float s_sa[TN_MAX];                             // sa[t] / 256 (0 past T)
@@ -313,6 +338,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       tc::mbar_init(fda2, 4);
       tc::mbar_init(fd2, 1);
       tc::mbar_init(actready, 1);
+      tc::mbar_init(fdone, 4);
     }
     tc::fence_barrier_init();
     tc::tma_prefetch_desc(&tmW);
@@ -326,15 +352,20 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   // FUSED, ticket CTAs: the phase-A loads leave first, before the setup barrier, when x, P1 and P2
   // may be read before the PDL wait (otherwise after the weights, in the producer loop below)
   const bool early_x = ticket && (pdl & (PDL_P | PDL_X)) == (PDL_P | PDL_X);
+  auto fd_load = [&] {                       // this CTA's tile of x, P1 and P2 (fq_tq_tc05.cu boxes)
+    tc::mbar_expect_tx(fdx, uint32_t(FG::LOAD_BYTES));
+#pragma unroll
+    for (int b = 0; b < FG::JB; ++b)
+      tc::tma_load_3d(fsX + b * FG::TOK * FG::N1 * 128, &fd.tmX, fdx, b * 64, 0, FG::TOK * int(blockIdx.x));
+#pragma unroll
+    for (int a = 0; a < FG::P1_ATOMS; ++a) tc::tma_load_2d(fsP1 + a * FG::N1 * 128, &fd.tmP1, fdx, a * 64, 0);
+#pragma unroll
+    for (int b = 0; b < FG::JB; ++b) tc::tma_load_2d(fsP2 + b * FG::N2 * 128, &fd.tmP2, fdx, b * 64, 0);
+  };
   if (FUSED && ticket && warp == TMA_WARP && lane == 0) {
     tc::mbar_init(fdx, 1);
     tc::fence_barrier_init();
-    if (early_x) {
-      tc::mbar_expect_tx(fdx, uint32_t(FD_X_BYTES + 2 * FD_P_BYTES));
-      tc::tma_load_3d(fsX, &fd.tmX, fdx, 0, 0, 2 * int(blockIdx.x));
-      tc::tma_load_2d(fsP1, &fd.tmP1, fdx, 0, 0);
-      tc::tma_load_2d(fsP2, &fd.tmP2, fdx, 0, 0);
-    }
+    if (early_x) fd_load();
   }
   if (warp == ALLOC_WARP) tc::tmem_alloc(tmem_slot, DecCfg<CFG, FUSED>::TMEM_COLS);
   tc::fence_before();
@@ -384,6 +415,15 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   if (warp == TMA_WARP) {
     // ======================= TMA producer =======================
     if (lane == 0) {
+      if (FUSED == 2 && ticket) {
+        // the 112 x 128 phase-A tile occupies the first packed ring stages: this CTA's weights
+        // stream only once its transform tile is done (the other CTAs' from kernel start)
+        if (!early_x) {
+          tc::griddep_wait();
+          fd_load();
+        }
+        tc::mbar_wait(fdone, 0);
+      }
       // the weights are parameters: unless the preceding kernel of the stream writes them
       // (host-side hazard check, fq_abi.cu), start streaming them before the wait
       if (!(pdl & PDL_P)) tc::griddep_wait();
@@ -398,12 +438,9 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         tc::mbar_expect_tx(&pfull[j], uint32_t(WPB + KP * ap_bytes));
         tc::tma_load_2d(sP + size_t(j) * PB, &tmW, &pfull[j], kb_of(j) * PROW, fb * BM);
       }
-      if (FUSED && ticket && !early_x) {          // phase-A loads that had to wait for the predecessor
+      if (FUSED == 1 && ticket && !early_x) {     // phase-A loads that had to wait for the predecessor
         tc::griddep_wait();
-        tc::mbar_expect_tx(fdx, uint32_t(FD_X_BYTES + 2 * FD_P_BYTES));
-        tc::tma_load_3d(fsX, &fd.tmX, fdx, 0, 0, 2 * int(blockIdx.x));
-        tc::tma_load_2d(fsP1, &fd.tmP1, fdx, 0, 0);
-        tc::tma_load_2d(fsP2, &fd.tmP2, fdx, 0, 0);
+        fd_load();
       }
       if constexpr (FUSED) {
         // every ticket CTA has stored its codes and scales (release/acquire at GPU scope); the
@@ -555,26 +592,28 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     // ======================= MMA issuer =======================
     if (lane == 0) {
       if (ticket) {
-        // phase A (fq_tq_tc05.cu, n1 = n2 = 64, two tokens = M 128): D = X^T P1 into the accumulator
-        // columns [0, 64) (unused until the first GEMM MMA, which comes after every ticket's
-        // epilogue has read them), then D = W P2 into the same columns once the stage-1 epilogue
-        // has read D and written W (fp16) to shared memory
+        // phase A (fq_tq_tc05.cu's MMAs, M = 128: two tokens at 64 x 64, one at 112 x 128): D =
+        // (X^T P1) into TMEM columns [0, n1) -- the accumulator columns, unused until the first GEMM
+        // MMA (which follows every ticket's epilogue); at 112 x 128 also the first two weight
+        // stages, which this CTA fills only after phase A (fdone) -- then D = W P2 into columns
+        // [0, n2) once the stage-1 epilogue has read D and written W (fp16) to shared memory
         tc::mbar_wait(fdx, 0);
         tc::fence_after();
         dtrace(tslot, 116);
         const uint32_t xs = smem_u32(fsX), p1a = smem_u32(fsP1), p2a = smem_u32(fsP2), a2 = smem_u32(fsA2);
+        constexpr uint32_t XLBO = FG::N2 == 64 ? FG::N1 * 128 : FG::TOK * FG::N1 * 128;
 #pragma unroll
-        for (int kk = 0; kk < FD_N / 16; ++kk)
-          tc::mma_ss<false>(tmem_base, tc::sdesc_sw128(xs + kk * 2048, FD_N * 128, 1024),
-                            tc::sdesc_sw128(p1a + kk * 2048, FD_N * 128, 1024), FD_IDESC, kk > 0);
+        for (int kk = 0; kk < FG::N1 / 16; ++kk)
+          tc::mma_ss<false>(tmem_base, tc::sdesc_sw128(xs + kk * 2048, XLBO, 1024),
+                            tc::sdesc_sw128(p1a + kk * 2048, FG::N1 * 128, 1024), FG::IDESC1, kk > 0);
         tc::mma_commit(fd1);
         tc::mbar_wait(fda2, 0);
         tc::fence_after();
         dtrace(tslot, 119);
 #pragma unroll
-        for (int kk = 0; kk < FD_N / 16; ++kk)
-          tc::mma_ss<false>(tmem_base, tc::sdesc_sw128(a2 + kk * 2048, FD_N * 128, 1024),
-                            tc::sdesc_sw128(p2a + kk * 2048, FD_N * 128, 1024), FD_IDESC, kk > 0);
+        for (int kk = 0; kk < FG::N2 / 16; ++kk)
+          tc::mma_ss<false>(tmem_base, tc::sdesc_sw128(a2 + kk * 2048, FG::N2 * 128, 1024),
+                            tc::sdesc_sw128(p2a + kk * 2048, FG::N2 * 128, 1024), FG::IDESC2, kk > 0);
         tc::mma_commit(fd2);
       }
       for (int j = 0; j < nk; ++j) {
@@ -624,12 +663,13 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
           tc::tmem_ld16(lb + uint32_t(c), v);
           tc::tmem_ld_wait();
         };
-        // stage 1: D lane (t, j), column i = W_t[i][j]; token t = L / 64
+        constexpr int N1 = FG::N1, N2 = FG::N2, TOK = FG::TOK;
+        // stage 1: D lane (t, j), column i = W_t[i][j] (64 x 64: token t = L / 64)
         tc::mbar_wait(fd1, 0);
         tc::fence_after();
         float m1 = 0.f;
 #pragma unroll
-        for (int c = 0; c < FD_N; c += 16) {
+        for (int c = 0; c < N1; c += 16) {
           uint32_t v[16];
           ld16(c, v);
 #pragma unroll
@@ -637,20 +677,22 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
             m1 = qz::max3f(m1, fabsf(__uint_as_float(v[e])), fabsf(__uint_as_float(v[e + 1])));
         }
         const float4 r1 = exchange(m1);
-        const int pe0 = qz::prescale_exp(fmaxf(r1.x, r1.y)), pe1 = qz::prescale_exp(fmaxf(r1.z, r1.w));
-        const int tt = L >> 6;
+        const int pe0 = qz::prescale_exp(TOK == 2 ? fmaxf(r1.x, r1.y) : fmaxf(fmaxf(r1.x, r1.y), fmaxf(r1.z, r1.w)));
+        const int pe1 = TOK == 2 ? qz::prescale_exp(fmaxf(r1.z, r1.w)) : pe0;
+        const int tt = TOK == 2 ? (L >> 6) : 0;
         const float pre = qz::exp2i(tt ? pe1 : pe0);
         {
-          const int j = L & 63;                            // K row j' of the stage-2 A operand
-          const uint32_t row = smem_u32(fsA2) + uint32_t(tt * (FD_N * 128) + j * 128);
+          const int j = N2 == 64 ? (L & 63) : L;           // K row j' of the stage-2 A operand
+          const uint32_t row = smem_u32(fsA2) + uint32_t(j * 128);
 #pragma unroll
-          for (int c = 0; c < FD_N; c += 16) {
+          for (int c = 0; c < N1; c += 16) {
             uint32_t v[16];
             ld16(c, v);
 #pragma unroll
             for (int e = 0; e < 16; e += 8) {
-              const int ch = ((c + e) >> 3) & 7;
-              tc::sts128(row + uint32_t((ch ^ (j & 7)) << 4),
+              const int c8 = (c + e) >> 3, ch = c8 & 7;
+              const int atom = N1 == 64 ? tt : (c8 >> 3);    // 64-element M atoms of A2
+              tc::sts128(row + uint32_t(atom * (N2 * 128) + ((ch ^ (j & 7)) << 4)),
                          pack_half2(__uint_as_float(v[e + 0]) * pre, __uint_as_float(v[e + 1]) * pre),
                          pack_half2(__uint_as_float(v[e + 2]) * pre, __uint_as_float(v[e + 3]) * pre),
                          pack_half2(__uint_as_float(v[e + 4]) * pre, __uint_as_float(v[e + 5]) * pre),
@@ -662,29 +704,32 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(fda2);
-        // stage 2: D lane (t, i), column j = Y_t[i][j] (prescaled by 2^pe)
+        // stage 2: D lane (t, i), column j = Y_t[i][j] (prescaled by 2^pe); 112 x 128: lanes >= 112
+        // hold no row (their A2 rows were never written) and are left out of the statistics
         tc::mbar_wait(fd2, 0);
         tc::fence_after();
         if (L == 0) dtrace(tslot, 120);
+        const bool valid = N1 == 64 || L < N1;
         float m2 = 0.f;
 #pragma unroll
-        for (int c = 0; c < FD_N; c += 16) {
+        for (int c = 0; c < N2; c += 16) {
           uint32_t v[16];
           ld16(c, v);
 #pragma unroll
           for (int e = 0; e < 16; e += 2)
             m2 = qz::max3f(m2, fabsf(__uint_as_float(v[e])), fabsf(__uint_as_float(v[e + 1])));
         }
-        const float4 r2 = exchange(m2);
-        const float mp = tt == 0 ? fmaxf(r2.x, r2.y) : fmaxf(r2.z, r2.w);
-        const int t = 2 * int(blockIdx.x) + tt, i = L & 63;
-        const bool store = t < T;
+        const float4 r2 = exchange(valid ? m2 : 0.f);
+        const float mp = TOK == 2 ? (tt == 0 ? fmaxf(r2.x, r2.y) : fmaxf(r2.z, r2.w))
+                                  : fmaxf(fmaxf(r2.x, r2.y), fmaxf(r2.z, r2.w));
+        const int t = TOK * int(blockIdx.x) + tt, i = N1 == 64 ? (L & 63) : L;
+        const bool store = valid && t < T;
         const float inv_pre = qz::exp2i(-(tt ? pe1 : pe0));
         const float c15 = qz::sym_c15(fd.alpha, mp);
         if (!(pdl & PDL_OUT)) tc::griddep_wait();          // the predecessor no longer reads q_ws / s_ws
-        uint8_t* qrow = fd.q + (store ? size_t(t) * (FD_N * FD_N / 2) + size_t(i) * (FD_N / 2) : 0);
+        uint8_t* qrow = fd.q + (store ? size_t(t) * (N1 * N2 / 2) + size_t(i) * (N2 / 2) : 0);
 #pragma unroll
-        for (int c = 0; c < FD_N; c += 32) {
+        for (int c = 0; c < N2; c += 32) {
           uint32_t v[32];
           tc::tmem_ld16(lb + uint32_t(c), *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
           tc::tmem_ld16(lb + uint32_t(c + 16), *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
@@ -700,6 +745,11 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
           if (store) *reinterpret_cast<uint4*>(qrow + c / 2) = make_uint4(w[0], w[1], w[2], w[3]);
         }
         if (store && i == 0) fd.s[t] = mp > 0.f ? fd.alpha * (mp * inv_pre) / 7.0f : 1.0f;
+        if constexpr (FUSED == 2) {                        // TMEM and the phase-A buffers are free
+          tc::fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(fdone);
+        }
         if (L == 0) dtrace(tslot, 121);
         fence_proxy_async_global();                        // (the consumers read the codes through TMA)
         tc::fence_before();
@@ -853,7 +903,7 @@ static int dec_policy() {                         // FQ_DEC_POLICY: testing aid 
 
 // How many clusters of S CTAs the hardware keeps resident at once (cluster placement is bounded
 // by the GPC structure, not only by the per-SM limits); cached per (configuration, S).
-template <int CFG, bool FUSED>
+template <int CFG, int FUSED>
 static int dec_max_clusters(const void* kern, int S) {
   static int cache[gd::MAX_SPLIT + 1] = {0};
   if (S <= 1) return gd::DecCfg<CFG, FUSED>::MINB * num_sms();
@@ -887,7 +937,7 @@ static int dec_max_clusters(const void* kern, int S) {
 
 // Split: the largest S <= 8 (and <= the number of K-blocks) for which every cluster of the grid
 // is resident at once; shapes with more feature blocks than that run unsplit.
-template <int CFG, bool FUSED>
+template <int CFG, int FUSED>
 static int dec_pick_split(const void* kern, int N, int K) {
   const int fbs = (N + gd::BM - 1) / gd::BM;
   const int nkb = (K + gd::BK * gd::DecCfg<CFG, FUSED>::KP - 1) / (gd::BK * gd::DecCfg<CFG, FUSED>::KP);
@@ -920,7 +970,7 @@ static unsigned* fd_sync_slot() {
   return base[dev] + 2 * (next[dev].fetch_add(1, std::memory_order_relaxed) % gd::FD_SLOTS);
 }
 
-template <int CFG, bool FUSED>
+template <int CFG, int FUSED>
 static cudaError_t dec_launch_cfg(const GemmArgs& a, int split, const FdArgs* f) {
   using namespace gd;
   using DC = DecCfg<CFG, FUSED>;
@@ -960,19 +1010,27 @@ static cudaError_t dec_launch_cfg(const GemmArgs& a, int split, const FdArgs* f)
   S = std::max(1, std::min({S, MAX_SPLIT, nkb}));
   const int fbs = (a.N + BM - 1) / BM;
   FdParams fd{};
-  if constexpr (FUSED) {
-    // ticket CTAs: one per two-token tile, all within the (resident) grid
-    fd.ntiles = int((a.T + 1) / 2);
+  if constexpr (FUSED != 0) {
+    using FG = FdGeo<FUSED>;
+    // ticket CTAs: one per tile (TOK tokens), all within the (resident) grid
+    fd.ntiles = int((a.T + FG::TOK - 1) / FG::TOK);
     if (fbs * S < fd.ntiles) return cudaErrorNotSupported;      // caller falls back (nothing launched)
-    const uint64_t xd[3] = {uint64_t(FD_N), uint64_t(FD_N), uint64_t(a.T)};
-    const uint64_t xs[2] = {uint64_t(FD_N) * 2, uint64_t(f->ldx) * 2};
-    const uint32_t xb[3] = {64, uint32_t(FD_N), 2};
+    const uint64_t xd[3] = {uint64_t(FG::N2), uint64_t(FG::N1), uint64_t(a.T)};
+    const uint64_t xs[2] = {uint64_t(FG::N2) * 2, uint64_t(f->ldx) * 2};
+    const uint32_t xb[3] = {64, uint32_t(FG::N1), uint32_t(FG::TOK)};
     if (!tmap_encode(&fd.tmX, f->x, 2, 3, xd, xs, xb, TMAP_SW128)) return cudaErrorInvalidValue;
-    const uint64_t pd[2] = {uint64_t(FD_N), uint64_t(FD_N)};
-    const uint64_t ps[1] = {uint64_t(FD_N) * 2};
-    const uint32_t pb[2] = {64, uint32_t(FD_N)};
-    if (!tmap_encode(&fd.tmP1, f->p1, 2, 2, pd, ps, pb, TMAP_SW128)) return cudaErrorInvalidValue;
-    if (!tmap_encode(&fd.tmP2, f->p2, 2, 2, pd, ps, pb, TMAP_SW128)) return cudaErrorInvalidValue;
+    {
+      const uint64_t pd[2] = {uint64_t(FG::N1), uint64_t(FG::N1)};
+      const uint64_t ps[1] = {uint64_t(FG::N1) * 2};
+      const uint32_t pb[2] = {64, uint32_t(FG::N1)};
+      if (!tmap_encode(&fd.tmP1, f->p1, 2, 2, pd, ps, pb, TMAP_SW128)) return cudaErrorInvalidValue;
+    }
+    {
+      const uint64_t pd[2] = {uint64_t(FG::N2), uint64_t(FG::N2)};
+      const uint64_t ps[1] = {uint64_t(FG::N2) * 2};
+      const uint32_t pb[2] = {64, uint32_t(FG::N2)};
+      if (!tmap_encode(&fd.tmP2, f->p2, 2, 2, pd, ps, pb, TMAP_SW128)) return cudaErrorInvalidValue;
+    }
     fd.alpha = f->alpha;
     fd.q = const_cast<uint8_t*>(a.qa);
     fd.s = const_cast<float*>(a.sa);
@@ -1013,17 +1071,19 @@ static bool dec_deep(const GemmArgs& a) {         // FQ_DEC_CFG: testing aid (fo
 
 cudaError_t gemm_dec_launch(const GemmArgs& a, int split) {
   if (split <= 0) split = dec_env_split();
-  return dec_deep(a) ? dec_launch_cfg<1, false>(a, split, nullptr) : dec_launch_cfg<0, false>(a, split, nullptr);
+  return dec_deep(a) ? dec_launch_cfg<1, 0>(a, split, nullptr) : dec_launch_cfg<0, 0>(a, split, nullptr);
 }
 
 bool fused_dec_supported(const GemmArgs& a, int n1, int n2, bool x_bf16, const void* p2) {
-  return n1 == gd::FD_N && n2 == gd::FD_N && !x_bf16 && p2 != nullptr && a.za == nullptr && !a.out_i32 &&
-         gemm_dec_supported(a) && a.K == gd::FD_N * gd::FD_N;
+  const bool shape = (n1 == 64 && n2 == 64) || (n1 == 112 && n2 == 128);
+  return shape && !x_bf16 && p2 != nullptr && a.za == nullptr && !a.out_i32 && gemm_dec_supported(a) &&
+         a.K == n1 * n2;
 }
 
 cudaError_t fused_dec_launch(const GemmArgs& a, const FdArgs& f) {
   const int split = dec_env_split();
-  return dec_deep(a) ? dec_launch_cfg<1, true>(a, split, &f) : dec_launch_cfg<0, true>(a, split, &f);
+  if (f.n1 == 112) return dec_deep(a) ? dec_launch_cfg<1, 2>(a, split, &f) : dec_launch_cfg<0, 2>(a, split, &f);
+  return dec_deep(a) ? dec_launch_cfg<1, 1>(a, split, &f) : dec_launch_cfg<0, 1>(a, split, &f);
 }
 
 }  // namespace fq

@@ -164,13 +164,14 @@ int gemm_pair_pick_bn(int64_t T, int N, int K, int clusters);
 cudaError_t gemm_dec_launch(const GemmArgs& a, int split = 0);  // decode (T <= 64): swapped operands,
 bool gemm_dec_supported(const GemmArgs& a);                     // cluster split-K; split 0 = per shape
 bool gemm_pair_supported(const GemmArgs& a);
-// fused decode linear (T <= 64, n1 = n2 = 64, fp16 x, P2 given, symmetric): the transform +
+// fused decode linear (T <= 64, (n1, n2) = (64, 64) or (112, 128), fp16 x, P2 given, symmetric): the transform +
 // quantize of x (into the codes/scales buffers named by the GemmArgs) runs inside the decode GEMM
 // launch (fq_gemm_dec.cu, FUSED); cudaErrorNotSupported (nothing launched) when the grid for the
 // shape has fewer CTAs than two-token tiles
 struct FdArgs {
   const void* x;
   int64_t ldx;
+  int n1, n2;                // (64, 64) or (112, 128)
   const void* p1;
   const void* p2;
   float alpha;

@@ -185,3 +185,55 @@ def test_fused_decode_concurrent_streams():
     torch.cuda.synchronize()
     for o in outs:
         assert torch.equal(o[0], ref)
+
+
+def _inputs_g(T, N, n1, n2, seed):
+    x = torch.from_numpy(synth.activations(T, n1 * n2, seed=seed, dtype=np.float32)).half().to(DEV)
+    p1 = torch.from_numpy(synth.well_conditioned(n1, seed=seed, tag="p1", dtype=np.float32)).half().to(DEV)
+    p2 = torch.from_numpy(synth.well_conditioned(n2, seed=seed, tag="p2", dtype=np.float32)).half().to(DEV)
+    qw = torch.from_numpy(O.pack_int4(synth.random_codes(N, n1 * n2, seed=seed, tag="qw"))).to(DEV)
+    sw = torch.from_numpy(synth.random_scales(N, seed=seed, tag="sw")).to(DEV)
+    return x, p1, p2, qw, sw
+
+
+@pytest.mark.parametrize("T", [1, 2, 5, 17, 32, 63, 64])
+@pytest.mark.parametrize("N", [4096, 5120])
+def test_fused_decode_112x128_bit_identical(T, N):
+    """LLaMA-3-8B down_proj (14336 = 112 x 128): one token per ticket tile, the phase-A tile over
+    the first packed ring stages (the ticket CTAs load their weights after it)"""
+    n1, n2 = 112, 128
+    x, p1, p2, qw, sw = _inputs_g(T, N, n1, n2, seed=200 + T)
+    y = torch.empty((T, N), dtype=torch.float16, device=DEV)
+    q = torch.full((T, n1 * n2 // 2), 0xAB, dtype=torch.uint8, device=DEV)
+    s = torch.full((T,), -1.0, dtype=torch.float32, device=DEV)
+    n0 = fq.fq_launch_count()
+    fq.fq_flatquant_linear(x, n1, n2, p1, p2, 0.9, qw, sw, y, q, s)
+    assert fq.fq_launch_count() - n0 == 1
+    q2, s2 = fq.transform_quant(x, n1, n2, p1, p2, 0.9)
+    y2 = fq.w4a4_linear(q2, s2, qw, sw)
+    torch.cuda.synchronize()
+    assert torch.equal(q, q2) and torch.equal(s, s2) and torch.equal(y, y2)
+
+
+def test_fused_decode_112x128_chain_with_64x64():
+    """a decode layer's linears back to back (64 x 64 and 112 x 128 fused launches, PDL overlap,
+    shared workspace) equal the synchronised two-kernel results"""
+    T = 64
+    shapes = [(64, 64, 6144), (64, 64, 4096), (64, 64, 28672), (112, 128, 4096)]
+    ins = [_inputs_g(T, N, n1, n2, seed=300 + i) for i, (n1, n2, N) in enumerate(shapes)]
+    kmax = max(n1 * n2 for n1, n2, _ in shapes)
+    qws = torch.empty((T, kmax // 2), dtype=torch.uint8, device=DEV)
+    sws = torch.empty((T,), dtype=torch.float32, device=DEV)
+    ys = []
+    for (n1, n2, N), (x, p1, p2, qw, sw) in zip(shapes, ins):
+        y = torch.empty((T, N), dtype=torch.float16, device=DEV)
+        qv = qws.view(-1)[: T * n1 * n2 // 2].view(T, n1 * n2 // 2)     # one workspace for all linears
+        fq.fq_flatquant_linear(x, n1, n2, p1, p2, 0.9, qw, sw, y, qv, sws)
+        ys.append(y)
+    torch.cuda.synchronize()
+    for (n1, n2, N), (x, p1, p2, qw, sw), y in zip(shapes, ins, ys):
+        q2, s2 = fq.transform_quant(x, n1, n2, p1, p2, 0.9)
+        torch.cuda.synchronize()
+        y2 = fq.w4a4_linear(q2, s2, qw, sw)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y2)
