@@ -4,7 +4,9 @@ statistics of that linear on sampled tokens (the oracle recomputes exactly those
 gpurun_out/results.jsonl (the record is a by-product; the test asserts the north_star bars).
 
 Timing: L2 write-flushed then read-flushed before every timed launch, CUDA events on the
-launching stream, mean of the launches (event ticks are coarse on this part)."""
+launching stream, mean of the launches (event ticks are coarse on this part).  t_tq / t_gemm time
+the two kernels separately (serialised); t_linear times fq_flatquant_linear, the whole linear as a
+user calls it (two kernels overlapped through PDL, or one fused launch at decode sizes)."""
 import json
 import os
 import time
@@ -83,6 +85,12 @@ def test_result_records():
             y = torch.empty((T, N), dtype=torch.float16, device=DEV)
             t_tq = _timed(lambda: fq.fq_transform_quant(xd, n1, n2, p1d, p2d, alpha, q, s), flush)
             t_gemm = _timed(lambda: fq.fq_w4a4_linear(q, s, qwd, swd, y), flush)
+            # the whole-linear entry point: both kernels back to back (PDL), or ONE fused launch at
+            # decode sizes (K10); its launch count is recorded with it
+            n0 = fq.fq_launch_count()
+            fq.fq_flatquant_linear(xd, n1, n2, p1d, p2d, alpha, qwd, swd, y, q, s)
+            lin_launches = fq.fq_launch_count() - n0
+            t_lin = _timed(lambda: fq.fq_flatquant_linear(xd, n1, n2, p1d, p2d, alpha, qwd, swd, y, q, s), flush)
             w16 = torch.randn((N, K), device=DEV, dtype=torch.float16)
             t_fp16 = _timed(lambda: torch.matmul(xd, w16.t()), flush)
             del w16
@@ -122,6 +130,9 @@ def test_result_records():
                 "tokens_per_s": round(T / ((t_tq + t_gemm) * 1e-6), 1),
                 "fp16_tokens_per_s": round(T / (t_fp16 * 1e-6), 1),
                 "speedup_vs_fp16": round(t_fp16 / (t_tq + t_gemm), 3),
+                "t_linear_us": round(t_lin, 2), "linear_launches": int(lin_launches),
+                "linear_tokens_per_s": round(T / (t_lin * 1e-6), 1),
+                "linear_speedup_vs_fp16": round(t_fp16 / t_lin, 3),
                 "parity_rows": int(len(rows)),
                 "code_mismatch_pct": round(100.0 * st["mismatch_frac"], 5),
                 "max_tok_rel_y": st.get("y_rel_max"), "y_rel_fro": ost["out_rel_fro"],
