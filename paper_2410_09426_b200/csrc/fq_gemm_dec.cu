@@ -246,11 +246,6 @@ struct FdGeo {
   static_assert(!ALIAS || A2_BYTES <= P1_BYTES + X_BYTES, "A2 over P1 + X");
 };
 
-FQ_DEVICE unsigned ld_acquire_gpu(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 FQ_DEVICE unsigned ld_relaxed_gpu(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
