@@ -274,9 +274,12 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + size_t(PSTAGES) * PB);
   uint64_t* full = bars;                   // [STAGES]  converters -> MMA
   uint64_t* empty = bars + STAGES;         // [STAGES]  MMA commit -> converters
-  uint64_t* pfull = bars + 2 * STAGES;     // [PSTAGES] TMA -> converters
+  uint64_t* pfull = bars + 2 * STAGES;     // [PSTAGES] TMA (weights) -> converters
   uint64_t* pempty = pfull + PSTAGES;      // [PSTAGES] converter warps -> TMA
-  uint64_t* tfull = pempty + PSTAGES;      // [1]       last MMA commit -> partial-tile warps
+  uint64_t* afull = pempty + PSTAGES;      // [PSTAGES] TMA (activation codes) -> converters: the weights
+                                           //           of a stage are widened as soon as they land,
+                                           //           whether or not the codes exist yet (FUSED)
+  uint64_t* tfull = afull + PSTAGES;       // [1]       last MMA commit -> partial-tile warps
   uint64_t* fdx = tfull + 1;               // FUSED: X tile + P1 + P2 landed (ticket CTAs)
   uint64_t* fd1 = fdx + 1;                 //        stage-1 MMA commit -> epilogue warps
   uint64_t* fda2 = fd1 + 1;                //        stage-1 epilogue (4 warps) -> stage-2 MMA
@@ -325,6 +328,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     }
     for (int s = 0; s < PSTAGES; ++s) {
       tc::mbar_init(&pfull[s], 1);
+      tc::mbar_init(&afull[s], 1);
       tc::mbar_init(&pempty[s], NUM_ARRIVE);
     }
     tc::mbar_init(tfull, 1);
@@ -383,7 +387,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         if (b < nb) {
           const int j = j0 + b, u = j / KP, h = j % KP, sp = u % PSTAGES, st = j % STAGES;
           tc::mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1);
-          tc::mbar_wait(&pfull[sp], (u / PSTAGES) & 1);
+          tc::mbar_wait(&afull[sp], (u / PSTAGES) & 1);
           const uint32_t src = smem_u32(sP + size_t(sp) * PB + WPB);
           const uint32_t dst = smem_u32(sW + size_t(st) * W_BYTES);
 #ifndef FQ_EXP_DEC_SKIPA          // (experiment build: activation conversion removed)
@@ -430,7 +434,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
 #endif
       for (int j = 0; j < pre; ++j) {
         if (j < 36) dtrace(tslot, 4 + j);
-        tc::mbar_expect_tx(&pfull[j], uint32_t(WPB + KP * ap_bytes));
+        tc::mbar_expect_tx(&pfull[j], uint32_t(WPB));
         tc::tma_load_2d(sP + size_t(j) * PB, &tmW, &pfull[j], kb_of(j) * PROW, fb * BM);
       }
       if (FUSED == 1 && ticket && !early_x) {     // phase-A loads that had to wait for the predecessor
@@ -458,16 +462,19 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       } else if (!(pdl & PDL_X)) {
         tc::griddep_wait();                      // qa written by the transform kernel is visible
       }
-      for (int j = 0; j < pre; ++j)
-        if (ap_bytes) tc::tma_load_2d(sP + size_t(j) * PB + WPB, &tmA, &pfull[j], kb_of(j) * PROW, 0);
+      for (int j = 0; j < pre; ++j) {
+        tc::mbar_expect_tx(&afull[j], uint32_t(KP * ap_bytes));
+        if (ap_bytes) tc::tma_load_2d(sP + size_t(j) * PB + WPB, &tmA, &afull[j], kb_of(j) * PROW, 0);
+      }
       for (int j = pre; j < nsb; ++j) {
         const int sp = j % PSTAGES;
         tc::mbar_wait(&pempty[sp], ((j / PSTAGES) & 1) ^ 1);
         if (j < 36) dtrace(tslot, 4 + j);
-        tc::mbar_expect_tx(&pfull[sp], uint32_t(WPB + KP * ap_bytes));
         uint8_t* dst = sP + size_t(sp) * PB;
+        tc::mbar_expect_tx(&pfull[sp], uint32_t(WPB));
         tc::tma_load_2d(dst, &tmW, &pfull[sp], kb_of(j) * PROW, fb * BM);
-        if (ap_bytes) tc::tma_load_2d(dst + WPB, &tmA, &pfull[sp], kb_of(j) * PROW, 0);
+        tc::mbar_expect_tx(&afull[sp], uint32_t(KP * ap_bytes));
+        if (ap_bytes) tc::tma_load_2d(dst + WPB, &tmA, &afull[sp], kb_of(j) * PROW, 0);
       }
     }
     __syncwarp();
@@ -531,6 +538,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       const int sp = j % PSTAGES, st = j % STAGES;
       tc::mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1);
       tc::mbar_wait(&pfull[sp], (j / PSTAGES) & 1);
+      tc::mbar_wait(&afull[sp], (j / PSTAGES) & 1);
       const uint32_t src = smem_u32(sP + size_t(sp) * PB);
       const uint32_t dst = smem_u32(sW + size_t(st) * W_BYTES);
       for (int task = ct; task < ntask; task += CONV_THREADS) {
