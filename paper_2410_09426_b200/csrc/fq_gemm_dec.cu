@@ -157,7 +157,9 @@ struct DecCfg {
   static_assert(RED_BYTES <= STAGES * W_BYTES, "partial tile in the operand stages");
   // phase A (the transform tile, fd_geo below): 64 x 64 in the widened-operand stages, 112 x 128 in
   // those stages plus the first packed ring stages (whose weights the ticket CTAs load afterwards)
+#ifndef FQ_EXP_DEC_NOFUSED            // experiment builds that only time the plain decode GEMM
   static_assert(FUSED != 1 || STAGES * W_BYTES >= 48 * 1024, "64 x 64 phase A in the operand stages");
+#endif
   static_assert(FUSED != 2 || STAGES * W_BYTES + PSTAGES * PB >= 88 * 1024, "112 x 128 phase A");
   static_assert(!TMEMW || W_COL0 + STAGES * WT_COLS <= TMEM_COLS, "TMEM budget");
   static_assert(MINB == 1 || TMEM_COLS <= 256, "two CTAs per SM share the 512 TMEM columns");
