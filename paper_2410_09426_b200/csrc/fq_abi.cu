@@ -323,7 +323,7 @@ static fq_status run_fused(const void* x, int32_t x_dtype, int64_t T, int32_t n1
   a.y_bf16 = y_bf16;
   a.stream = static_cast<cudaStream_t>(stream);
   if (!fused_dec_supported(a, n1, n2, x_dtype == FQ_BF16, p2)) return FQ_ENOTSUP;
-  FdArgs f{x, n, n1, n2, p1, p2, alpha};
+  FdArgs f{x, n, n1, n2, p1, p2, alpha, x_dtype == FQ_BF16};
   const Span sqw = span(qw, size_t(N) * size_t(n / 2)), ssw = span(sw, size_t(N) * 4);
   const Span sp1 = span(p1, size_t(n1) * n1 * 2), sp2 = span(p2, size_t(n2) * n2 * 2);
   const Span sx = span(x, size_t(T) * size_t(n) * 2);

@@ -151,4 +151,37 @@ FQ_DEVICE int bf16_to_f16_pow2(uint8_t* p, int elems, uint32_t* red) {
   return e;
 }
 
+// bf16_to_f16_pow2 for one group of `nthreads` threads (this thread is `tid`) that synchronises
+// through named barrier `bar` instead of the whole block (the fused decode linear's epilogue warps):
+// the same maximum, exponent and conversion, so the result is bit-identical.
+FQ_DEVICE int bf16_to_f16_pow2_group(uint8_t* p, int elems, uint32_t* red, int tid, int nthreads, int bar) {
+  uint4* v4 = reinterpret_cast<uint4*>(p);
+  const int n4 = elems / 8;
+  if (tid == 0) *red = 0u;
+  named_bar_sync(bar, nthreads);
+  uint32_t m = 0;
+  for (int i = tid; i < n4; i += nthreads) {
+    const uint4 v = v4[i];
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) m = max(m, max((w[h] << 16) & 0x7FFFFFFFu, w[h] & 0x7FFF0000u));
+  }
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((tid & 31) == 0) atomicMax(red, m);
+  named_bar_sync(bar, nthreads);
+  const int e = p2_scale_exp(*red);
+  const float sc = __int_as_float((127 + e) << 23);
+  for (int i = tid; i < n4; i += nthreads) {
+    uint4 v = v4[i];
+    uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+    for (int h = 0; h < 4; ++h)
+      w[h] = pack_half2(__uint_as_float(w[h] << 16) * sc, __uint_as_float(w[h] & 0xFFFF0000u) * sc);
+    v4[i] = v;
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  named_bar_sync(bar, nthreads);
+  return e;
+}
+
 }  // namespace fq

@@ -223,6 +223,7 @@ struct alignas(64) FdParams {
   float* s;                      // [T] scales (s_ws)
   unsigned* sync;                // {arrivals, departures} of this launch's slot
   int ntiles;                    // ticket CTAs = ceil(T / TOK)
+  int bf16x;                     // x, P1, P2 are bf16 (stage 2 runs in fp16 with P2 scaled, as K1)
 };
 // Phase-A geometry (the same tiles as fq_tq_tc05.cu): F = 1 -> n1 = n2 = 64, two tokens per tile;
 // F = 2 -> 112 x 128 (LLaMA-3-8B down_proj), one token.  Layout in shared memory from offset 0:
@@ -243,6 +244,7 @@ struct FdGeo {
   static constexpr int BYTES = ALIAS ? P2_BYTES + P1_BYTES + X_BYTES : OFF_A2 + A2_BYTES;
   static constexpr int LOAD_BYTES = X_BYTES + P1_BYTES + P2_BYTES;
   static constexpr uint32_t IDESC1 = tc::idesc_f16(128, N1, 0, 1, 1);   // fp16 x fp16 -> fp32, MN-major
+  static constexpr uint32_t IDESC1_BF16 = tc::idesc_f16(128, N1, 1, 1, 1);
   static constexpr uint32_t IDESC2 = tc::idesc_f16(128, N2, 0, 1, 1);
   static_assert(TOK * N2 == 128, "one M = 128 stage-1 group per tile");
   static_assert(!ALIAS || A2_BYTES <= P1_BYTES + X_BYTES, "A2 over P1 + X");
@@ -610,7 +612,8 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
 #pragma unroll
         for (int kk = 0; kk < FG::N1 / 16; ++kk)
           tc::mma_ss<false>(tmem_base, tc::sdesc_sw128(xs + kk * 2048, XLBO, 1024),
-                            tc::sdesc_sw128(p1a + kk * 2048, FG::N1 * 128, 1024), FG::IDESC1, kk > 0);
+                            tc::sdesc_sw128(p1a + kk * 2048, FG::N1 * 128, 1024),
+                            fd.bf16x ? FG::IDESC1_BF16 : FG::IDESC1, kk > 0);
         tc::mma_commit(fd1);
         tc::mbar_wait(fda2, 0);
         tc::fence_after();
@@ -669,6 +672,15 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
           tc::tmem_ld_wait();
         };
         constexpr int N1 = FG::N1, N2 = FG::N2, TOK = FG::TOK;
+        // bf16 x / P: stage 2 runs in fp16 (R9), so P2 becomes fp16 P2 2^e2 in place
+        // (K1's power-of-two scaling into fp16 range) while the stage-1 MMA runs; 2^-e2 is
+        // divided out of the statistics exactly.  The stage-2 MMA reads P2 only after fda2 below.
+        float inv_p2 = 1.0f;
+        if (fd.bf16x) {
+          __shared__ uint32_t fd_p2max;
+          tc::mbar_wait(fdx, 0);
+          inv_p2 = qz::exp2i(-bf16_to_f16_pow2_group(fsP2, FG::P2_BYTES / 2, &fd_p2max, L, 128, 1));
+        }
         // stage 1: D lane (t, j), column i = W_t[i][j] (64 x 64: token t = L / 64)
         tc::mbar_wait(fd1, 0);
         tc::fence_after();
@@ -749,7 +761,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
           }
           if (store) *reinterpret_cast<uint4*>(qrow + c / 2) = make_uint4(w[0], w[1], w[2], w[3]);
         }
-        if (store && i == 0) fd.s[t] = mp > 0.f ? fd.alpha * (mp * inv_pre) / 7.0f : 1.0f;
+        if (store && i == 0) fd.s[t] = mp > 0.f ? fd.alpha * (mp * inv_pre * inv_p2) / 7.0f : 1.0f;
         if constexpr (FUSED == 2) {                        // TMEM and the phase-A buffers are free
           tc::fence_before();
           __syncwarp();
@@ -1037,6 +1049,7 @@ static cudaError_t dec_launch_cfg(const GemmArgs& a, int split, const FdArgs* f)
       if (!tmap_encode(&fd.tmP2, f->p2, 2, 2, pd, ps, pb, TMAP_SW128)) return cudaErrorInvalidValue;
     }
     fd.alpha = f->alpha;
+    fd.bf16x = f->bf16 ? 1 : 0;
     fd.q = const_cast<uint8_t*>(a.qa);
     fd.s = const_cast<float*>(a.sa);
     fd.sync = fd_sync_slot();
@@ -1080,8 +1093,9 @@ cudaError_t gemm_dec_launch(const GemmArgs& a, int split) {
 }
 
 bool fused_dec_supported(const GemmArgs& a, int n1, int n2, bool x_bf16, const void* p2) {
+  (void)x_bf16;                                    // fp16 and bf16 activations (bf16: P2 scaled, K1)
   const bool shape = (n1 == 64 && n2 == 64) || (n1 == 112 && n2 == 128);
-  return shape && !x_bf16 && p2 != nullptr && a.za == nullptr && !a.out_i32 && gemm_dec_supported(a) &&
+  return shape && p2 != nullptr && a.za == nullptr && !a.out_i32 && gemm_dec_supported(a) &&
          a.K == n1 * n2;
 }
 

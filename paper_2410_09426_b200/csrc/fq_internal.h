@@ -164,7 +164,7 @@ int gemm_pair_pick_bn(int64_t T, int N, int K, int clusters);
 cudaError_t gemm_dec_launch(const GemmArgs& a, int split = 0);  // decode (T <= 64): swapped operands,
 bool gemm_dec_supported(const GemmArgs& a);                     // cluster split-K; split 0 = per shape
 bool gemm_pair_supported(const GemmArgs& a);
-// fused decode linear (T <= 64, (n1, n2) = (64, 64) or (112, 128), fp16 x, P2 given, symmetric): the transform +
+// fused decode linear (T <= 64, (n1, n2) = (64, 64) or (112, 128), fp16 or bf16 x, P2 given, symmetric): the transform +
 // quantize of x (into the codes/scales buffers named by the GemmArgs) runs inside the decode GEMM
 // launch (fq_gemm_dec.cu, FUSED); cudaErrorNotSupported (nothing launched) when the grid for the
 // shape has fewer CTAs than two-token tiles
@@ -175,6 +175,7 @@ struct FdArgs {
   const void* p1;
   const void* p2;
   float alpha;
+  bool bf16;                 // x, p1, p2 bf16 (else fp16)
 };
 bool fused_dec_supported(const GemmArgs& a, int n1, int n2, bool x_bf16, const void* p2);
 cudaError_t fused_dec_launch(const GemmArgs& a, const FdArgs& f);

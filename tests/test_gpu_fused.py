@@ -155,13 +155,9 @@ def test_fused_decode_slot_reuse_and_graph_replay():
 
 
 def test_fused_decode_not_taken_outside_its_shapes():
-    """bf16 activations, other decompositions and T > 64 keep the two-kernel path (2 launches)"""
+    """T > 64 keeps the two-kernel path (2 launches)"""
     T, N = 64, 512
     x, p1, p2, qw, sw = _inputs(T, N, seed=2)
-    y, q, s = _bufs(T, N)
-    n0 = fq.fq_launch_count()
-    fq.fq_flatquant_linear(x.bfloat16(), N1, N2, p1.bfloat16(), p2.bfloat16(), 0.9, qw, sw, y, q, s)
-    assert fq.fq_launch_count() - n0 == 2
     T2 = 65
     x2, _, _, _, _ = _inputs(T2, N, seed=2)
     y2, q2, s2 = _bufs(T2, N)
@@ -237,3 +233,24 @@ def test_fused_decode_112x128_chain_with_64x64():
         y2 = fq.w4a4_linear(q2, s2, qw, sw)
         torch.cuda.synchronize()
         assert torch.equal(y, y2)
+
+
+@pytest.mark.parametrize("n1,n2,N", [(64, 64, 4096), (112, 128, 4096)])
+@pytest.mark.parametrize("T", [1, 9, 64])
+@pytest.mark.parametrize("p2_scale", [1.0, 1e5])
+def test_fused_decode_bf16_bit_identical(n1, n2, N, T, p2_scale):
+    """bf16 activations and transforms: P2 is scaled by a power of two into fp16 range inside the
+    fused kernel as in the transform kernel (also for a P2 beyond fp16 range)"""
+    x, p1, p2, qw, sw = _inputs_g(T, N, n1, n2, seed=400 + T)
+    x, p1 = x.bfloat16(), p1.bfloat16()
+    p2 = (p2.float() * p2_scale).bfloat16()
+    y = torch.empty((T, N), dtype=torch.bfloat16, device=DEV)
+    q = torch.full((T, n1 * n2 // 2), 0xAB, dtype=torch.uint8, device=DEV)
+    s = torch.full((T,), -1.0, dtype=torch.float32, device=DEV)
+    n0 = fq.fq_launch_count()
+    fq.fq_flatquant_linear(x, n1, n2, p1, p2, 0.9, qw, sw, y, q, s)
+    assert fq.fq_launch_count() - n0 == 1
+    q2, s2 = fq.transform_quant(x, n1, n2, p1, p2, 0.9)
+    y2 = fq.w4a4_linear(q2, s2, qw, sw, out_dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    assert torch.equal(q, q2) and torch.equal(s, s2) and torch.equal(y, y2)
