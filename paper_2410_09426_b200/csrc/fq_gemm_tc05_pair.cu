@@ -91,7 +91,7 @@ constexpr int B_CHUNKS = BK / 32;                          // 16-byte packed chu
 // fill the last wave (fewer, narrower waves when N / 192 tiles would leave most clusters idle).
 template <int BN>
 struct Geo {
-  static_assert(BN % 32 == 0 && BN >= 64 && BN <= 256, "BN: multiple of 32 in [64, 256]");
+  static_assert(BN % 16 == 0 && BN >= 64 && BN <= 256, "BN: multiple of 16 in [64, 256] (MMA N at M = 256)");
   // up to 192 columns two accumulators fit beside the A stages (epilogue of tile i overlaps the
   // main loop of tile i+1); a 256-wide tile has one, and its epilogue is not overlapped
   static constexpr int NACC = BN <= 192 ? 2 : 1;
@@ -163,6 +163,7 @@ template <int BN, bool OUT_I32, bool BF16, bool ASYM>
 __global__ void __launch_bounds__(THREADS, 1)
 gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmY32,
+                 const __grid_constant__ CUtensorMap tmY16,
                  const float* __restrict__ sa, int T, int K, const float* __restrict__ sw, int N,
                  void* __restrict__ yv, const int8_t* __restrict__ za, const int32_t* __restrict__ colsum,
                  int pdl) {
@@ -464,16 +465,20 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       const uint32_t tacc = tmem_base + (uint32_t(warp * 32) << 16) + uint32_t(TMEM_ACC0 + buf * BN);
       if constexpr (OUT_I32) {
 #pragma unroll 1
-        for (int cc = 0; cc < BN / 32; ++cc) {
+        for (int cc = 0; cc < (BN + 31) / 32; ++cc) {
           uint32_t v[32];
-          tc::tmem_ld32(tacc + uint32_t(cc * 32), v);
+          if (BN % 32 != 0 && cc == BN / 32) {                 // 16-column tail (BN = 240)
+            tc::tmem_ld16(tacc + uint32_t(cc * 32), *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+          } else {
+            tc::tmem_ld32(tacc + uint32_t(cc * 32), v);
+          }
           tc::tmem_ld_wait();
           const int col0 = nb * BN + cc * 32;
           if (row_ok) {
 #pragma unroll
             for (int j = 0; j < 32; j += 8) {
               const int col = col0 + j;
-              if (col >= N) break;
+              if (col >= N || cc * 32 + j >= BN) break;
               int32_t* dst = static_cast<int32_t*>(yv) + size_t(row) * N + col;
               reinterpret_cast<int4*>(dst)[0] =
                   make_int4(int(v[j]) >> 8, int(v[j + 1]) >> 8, int(v[j + 2]) >> 8, int(v[j + 3]) >> 8);
@@ -494,7 +499,11 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         auto emit = [&](auto nc_tag, int c0off) {
           constexpr int NC = decltype(nc_tag)::value;
           uint32_t v[NC];
-          tc::tmem_ld32(tacc + uint32_t(c0off), *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+          if constexpr (NC == 16) {
+            tc::tmem_ld16(tacc + uint32_t(c0off), *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+          } else {
+            tc::tmem_ld32(tacc + uint32_t(c0off), *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+          }
           if constexpr (NC == 64)
             tc::tmem_ld32(tacc + uint32_t(c0off + 32), *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
           if (lane == 0) tc::bulk_wait_read0();          // previous chunk's store has left the buffer
@@ -545,19 +554,23 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             }
             if constexpr (NC == 64)      // 32 rows x 128 B, SWIZZLE_128B: chunk ^= row % 8
               tc::sts128(stg + uint32_t(lane * 128 + ((c8 ^ (lane & 7)) << 4)), o[0], o[1], o[2], o[3]);
-            else                         // 32 rows x 64 B, SWIZZLE_64B: chunk ^= (row / 2) % 4
+            else if constexpr (NC == 32) // 32 rows x 64 B, SWIZZLE_64B: chunk ^= (row / 2) % 4
               tc::sts128(stg + uint32_t(lane * 64 + ((c8 ^ ((lane >> 1) & 3)) << 4)), o[0], o[1], o[2], o[3]);
+            else                         // 32 rows x 32 B, no swizzle (the 16-column tail of BN = 240)
+              tc::sts128(stg + uint32_t(lane * 32 + (c8 << 4)), o[0], o[1], o[2], o[3]);
           }
           tc::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tc::tma_store_2d(NC == 64 ? &tmY : &tmY32, stg, col0, mb * BM + int(rank) * BM_CTA + warp * 32);
+            tc::tma_store_2d(NC == 64 ? &tmY : (NC == 32 ? &tmY32 : &tmY16), stg, col0,
+                             mb * BM + int(rank) * BM_CTA + warp * 32);
             tc::bulk_commit();
           }
         };
 #pragma unroll 1
         for (int q = 0; q < BN / 64; ++q) emit(std::integral_constant<int, 64>{}, q * 64);
-        if constexpr (BN % 64 != 0) emit(std::integral_constant<int, 32>{}, (BN / 64) * 64);
+        if constexpr (BN % 64 >= 32) emit(std::integral_constant<int, 32>{}, (BN / 64) * 64);
+        if constexpr (BN % 32 != 0) emit(std::integral_constant<int, 16>{}, (BN / 32) * 32);
       }
       tc::fence_before();
       named_bar_sync(2, NUM_EPI_WARPS * 32);
@@ -630,7 +643,7 @@ static cudaError_t launch_bn(const GemmArgs& a) {
   static std::atomic<uint64_t> attr_done[5];   // per kernel variant: devices configured
   const int which = a.out_i32 ? 0 : (a.y_bf16 ? 1 : 2) + (asym ? 2 : 0);
   if (cudaError_t e = ensure_smem_attr(kern, int(GE::SMEM_BYTES), attr_done[which]); e != cudaSuccess) return e;
-  CUtensorMap ma{}, mb{}, my{}, my32{};
+  CUtensorMap ma{}, mb{}, my{}, my32{}, my16{};
   {
     const uint64_t dims[2] = {uint64_t(a.K / 2), uint64_t(a.T)};
     const uint64_t strides[1] = {uint64_t(a.K / 2)};
@@ -651,11 +664,13 @@ static cudaError_t launch_bn(const GemmArgs& a) {
     if (!tmap_encode(&my, a.y, 2, 2, dims, strides, box, TMAP_SW128)) return cudaErrorInvalidValue;
     const uint32_t box32[2] = {32, 32};
     if (BN % 64 != 0 && !tmap_encode(&my32, a.y, 2, 2, dims, strides, box32, TMAP_SW64)) return cudaErrorInvalidValue;
+    const uint32_t box16[2] = {16, 32};
+    if (BN % 32 != 0 && !tmap_encode(&my16, a.y, 2, 2, dims, strides, box16, TMAP_SW_NONE)) return cudaErrorInvalidValue;
   }
   const int num_tiles = int((a.T + BM - 1) / BM) * ((a.N + BN - 1) / BN);
   const int clusters = std::max(1, std::min(num_tiles, num_sms() / 2));
   cudaError_t e = launch_pdl(kern, dim3(unsigned(2 * clusters)), dim3(THREADS), GE::SMEM_BYTES, a.stream, 2, ma, mb,
-                             my, my32, a.sa, int(a.T), a.K, a.sw, a.N, a.y, a.za, a.colsum, a.pdl);
+                             my, my32, my16, a.sa, int(a.T), a.K, a.sw, a.N, a.y, a.za, a.colsum, a.pdl);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
@@ -670,6 +685,7 @@ cudaError_t gemm_pair_launch(const GemmArgs& a, int bn) {
   if (bn == 0) bn = gemm_pair_pick_bn(a.T, a.N, a.K, std::max(1, num_sms() / 2));
   switch (bn) {
     case 256: return launch_bn<256>(a);
+    case 240: return launch_bn<240>(a);
     case 160: return launch_bn<160>(a);
     case 128: return launch_bn<128>(a);
     case 96: return launch_bn<96>(a);
