@@ -103,13 +103,29 @@ struct Cfg {
   static constexpr int D1C = G1 * N1;                  // TMEM columns of one stage-1 result
   // epilogue groups = tiles in flight (each owns a D1, D2 and A2 slot), as many as TMEM allows
   static constexpr int D2C = IDENT2 ? 0 : N2;         // TMEM columns of one stage-2 result
-  static constexpr int GROUPS_FIT = (512 / (D1C + D2C)) > MAX_GROUPS ? MAX_GROUPS : (512 / (D1C + D2C));
+  // ALIAS_D (round 2c, n2 = 128): a group's stage-2 result is written over its stage-1 result (the
+  // stage-2 MMA runs after the stage-1 epilogue has read D1; the next stage-1 MMA of the group waits
+  // until the stage-2 epilogue has read D2), so a group needs max(D1, D2) columns, not their sum:
+  // three epilogue groups instead of two at 64 x 128 and 112 x 128
+  static constexpr bool ALIAS_D = SMALL == 0 && !IDENT2 && N2 == 128;
+  static constexpr int GW = ALIAS_D ? (D1C > N2 ? D1C : N2) : D1C + D2C;   // TMEM columns per group
+  static constexpr int GROUPS_TMEM = (512 / GW) > MAX_GROUPS ? MAX_GROUPS : (512 / GW);
+  static constexpr bool ALIAS_A2 = SMALL == 1 && !IDENT2;     // A2 over P1 + X (one tile per CTA)
+  // and as many as leave shared memory for two X stages
+  static constexpr int fixed_of(int g) { return P1_BYTES + (IDENT2 ? 0 : P2_BYTES) + (ALIAS_A2 ? 0 : g * A2_BYTES); }
+  static constexpr int GROUPS_FIT =
+      (GROUPS_TMEM > 1 && (SMEM_LIMIT - SMEM_OVERHEAD - fixed_of(GROUPS_TMEM)) / X_BYTES < 2)
+          ? ((GROUPS_TMEM > 2 && (SMEM_LIMIT - SMEM_OVERHEAD - fixed_of(GROUPS_TMEM - 1)) / X_BYTES < 2)
+                 ? GROUPS_TMEM - 2 : GROUPS_TMEM - 1)
+          : GROUPS_TMEM;
   static constexpr int GROUPS = SMALL ? 1 : GROUPS_FIT;
   static constexpr int THREADS = (4 + 4 * GROUPS) * 32;
-  static constexpr int TMEM_USED = GROUPS * (D1C + D2C);
+  static constexpr int TMEM_USED = GROUPS * GW;
   static constexpr int TMEM_COLS = TMEM_USED <= 128 ? 128 : (TMEM_USED <= 256 ? 256 : 512);
-  static constexpr bool ALIAS_A2 = SMALL == 1 && !IDENT2;     // A2 over P1 + X (one tile per CTA)
-  static constexpr int FIXED = P1_BYTES + (IDENT2 ? 0 : P2_BYTES) + (ALIAS_A2 ? 0 : GROUPS * A2_BYTES);
+  static constexpr int D1_STRIDE = ALIAS_D ? GW : D1C;        // D1 of group par: par * D1_STRIDE
+  static constexpr int D2_COL0 = ALIAS_D ? 0 : GROUPS * D1C;   // D2 of group par: D2_COL0 + par * D2_STRIDE
+  static constexpr int D2_STRIDE = ALIAS_D ? GW : N2;
+  static constexpr int FIXED = fixed_of(GROUPS);
   static constexpr int STAGES_FIT = (SMEM_LIMIT - SMEM_OVERHEAD - FIXED) / X_BYTES;
   static constexpr int STAGES = SMALL == 1 ? 1 : SMALL == 2 ? 2 : (STAGES_FIT > 8 ? 8 : STAGES_FIT);
   static constexpr size_t SMEM = size_t(FIXED) + size_t(STAGES) * X_BYTES + SMEM_OVERHEAD;
@@ -212,6 +228,7 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
   uint64_t* a2full = d1full + G;     // [G]  epilogue group (4 warps) -> MMA
   uint64_t* d2full = a2full + G;     // [G]  MMA commit -> epilogue group
   uint64_t* tready = d2full + G;     // [G]  stage-1 MMA thread: tile index of the group's next tile
+  uint64_t* d2free = tready + G;     // [G]  ALIAS_D: stage-2 epilogue read D2 -> next stage-1 MMA
   __shared__ float red[MAX_GROUPS * 8];                        // [groups][2 parities][4 warps]
   __shared__ uint32_t tmem_slot[1];
   __shared__ int tile_id[8];                                   // [S] tile of each X stage (-1: end)
@@ -262,6 +279,7 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
       tc::mbar_init(&a2full[b], 4);
       tc::mbar_init(&d2full[b], 1);
       tc::mbar_init(&tready[b], 1);
+      tc::mbar_init(&d2free[b], 4);
     }
     tc::fence_barrier_init();
     if constexpr (DYN) nxt = atomicAdd(tsync, 1u);      // first claim: its latency hides behind the loads
@@ -341,7 +359,7 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
           // M = 128 rows (t, j): n2 = 64 -> the TOK tokens' j-block 0; n2 = 128 -> token g's 2 j-blocks
           const uint32_t a0 = xs + uint32_t(N2 == 64 ? 0 : g * N1 * 128);
           const uint32_t lbo = uint32_t(N2 == 64 ? N1 * 128 : TOK * N1 * 128);
-          const uint32_t d = tmem + uint32_t(par * C::D1C + g * N1);
+          const uint32_t d = tmem + uint32_t(par * C::D1_STRIDE + g * N1);
 #pragma unroll
           for (int kk = 0; kk < N1 / 16; ++kk)
             tc::mma_ss<false>(d, tc::sdesc_sw128(a0 + kk * 2048, lbo, 1024),
@@ -354,7 +372,7 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
         const int par = k % G;
         if (k < 16) trace(40 + k);
         const uint32_t a0 = smem_u32(sA2 + par * C::A2_BYTES);
-        const uint32_t d = tmem + uint32_t(G * C::D1C + par * N2);
+        const uint32_t d = tmem + uint32_t(C::D2_COL0 + par * C::D2_STRIDE);
 #pragma unroll
         for (int kk = 0; kk < N2 / 16; ++kk)
           tc::mma_ss<false>(d, tc::sdesc_sw128(a0 + kk * 2048, N2 * 128, 1024),
@@ -377,7 +395,10 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
             }
             break;
           }
-          if (k >= G) tc::mbar_wait(&a2full[k % G], ((k - G) / G) & 1);
+          if (k >= G) {                                  // the group's TMEM slot is free
+            if constexpr (C::ALIAS_D) tc::mbar_wait(&d2free[k % G], ((k - G) / G) & 1);
+            else tc::mbar_wait(&a2full[k % G], ((k - G) / G) & 1);
+          }
           seq_tile[k % 32] = tile;
           tc::mbar_arrive(&tready[k % G]);
           mma1(k);
@@ -431,7 +452,7 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
         uint8_t* stg = sA2 + par * C::A2_BYTES;          // [N1][N2/2] packed bytes of one token
 #pragma unroll 1
         for (int g = 0; g < C::G1; ++g) {
-          const uint32_t d1 = lane_base + uint32_t(par * C::D1C + g * N1);
+          const uint32_t d1 = lane_base + uint32_t(par * C::D1_STRIDE + g * N1);
           const int64_t t = t0 + g;
           float m1 = 0.f, hi1 = 0.f, lo1 = 0.f;
           tmem_chunks<N1>(d1, [&](const uint32_t* v, int n, int) {
@@ -545,7 +566,7 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
       constexpr bool SINGLE2 = (N2 == 64);
 #pragma unroll
       for (int g = 0; g < C::G1; ++g) {
-        const uint32_t d1 = lane_base + uint32_t(par * C::D1C + g * N1);
+        const uint32_t d1 = lane_base + uint32_t(par * C::D1_STRIDE + g * N1);
         uint32_t rv1[SINGLE1 ? N1 : 1];
         if constexpr (SINGLE1) tmem_ld_row<N1>(d1, rv1);
         // pass 1: max |W| over this lane's row (rows > 64 columns: two passes over TMEM keep
@@ -600,7 +621,7 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
       tc::fence_after();
       if (L == 0 && k < 16) trace(88 + k);
       FQ_SUB(8);
-      const uint32_t d2 = lane_base + uint32_t(G * C::D1C + par * N2);
+      const uint32_t d2 = lane_base + uint32_t(C::D2_COL0 + par * C::D2_STRIDE);
       const int tt = (N1 == 64) ? (L >> 6) : 0;
       const int i = (N1 == 64) ? (L & 63) : L;
       const bool valid = (N1 == 64) || (L < N1);
@@ -682,6 +703,10 @@ tq_tc05_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
         }
       });
       tc::fence_before();
+      if constexpr (C::ALIAS_D) {                        // D2 read out: the group's columns are free
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&d2free[par]);
+      }
       if (store && i == 0) {
         if constexpr (ASYM) {
           scale[t] = mp > 0.f ? alpha * (mp * inv_pre * inv_p2) / 15.0f : 1.0f;
