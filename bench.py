@@ -206,7 +206,7 @@ def fused_linear(T, lin):
     """The library runs fq_flatquant_linear as ONE fused launch (transform + quantize inside the
     decode GEMM, NEXT-4(i)) for T <= 64 with the 64 x 64 decomposition and fp16 activations
     (fq_gemm_dec.cu FUSED); the bench checks this against its launch count."""
-    return T <= 64 and (lin.n1, lin.n2) in ((64, 64), (112, 128))
+    return T <= 64 and (lin.n1, lin.n2) in ((64, 64), (64, 128), (112, 128))
 
 
 def fused_bytes(T, lin):

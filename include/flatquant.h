@@ -164,8 +164,9 @@ fq_status fq_w4a4_gemm_i32(const uint8_t* qa, int64_t T, int32_t K, const uint8_
  * and y hold bit-identical results either way.
  * Decode sizes run FUSED in ONE launch (PAPER.md:312-314 fuses the
  * transform and quantization into one kernel, here it is fused into the GEMM as well): for
- * 1 <= T <= 64, (n1, n2) = (64, 64) or (112, 128), fp16 or bf16 x and p2 != NULL, the first CTAs of the
- * decode GEMM transform one tile each (two tokens at 64 x 64, one at 112 x 128) into q_ws/s_ws
+ * 1 <= T <= 64, (n1, n2) = (64, 64), (64, 128) or (112, 128), fp16 or bf16 x and p2 != NULL, the
+ * first CTAs of the decode GEMM transform one tile each (two tokens at 64 x 64 and 64 x 128, one at
+ * 112 x 128) into q_ws/s_ws
  * (L2-resident at these sizes) while the other CTAs already stream their weights, and the GEMM
  * reads the codes once all tiles are published.  Tile
  * publication uses a {arrivals, departures} counter pair from a ring of 1024 slots per device in

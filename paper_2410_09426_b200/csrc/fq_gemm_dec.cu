@@ -161,6 +161,7 @@ struct DecCfg {
   static_assert(FUSED != 1 || STAGES * W_BYTES >= 48 * 1024, "64 x 64 phase A in the operand stages");
 #endif
   static_assert(FUSED != 2 || STAGES * W_BYTES + PSTAGES * PB >= 88 * 1024, "112 x 128 phase A");
+  static_assert(FUSED != 3 || STAGES * W_BYTES + PSTAGES * PB >= 72 * 1024, "64 x 128 phase A");
   static_assert(!TMEMW || W_COL0 + STAGES * WT_COLS <= TMEM_COLS, "TMEM budget");
   static_assert(MINB == 1 || TMEM_COLS <= 256, "two CTAs per SM share the 512 TMEM columns");
   static_assert(SMEM * MINB <= 232448, "shared memory per SM");
@@ -226,17 +227,20 @@ struct alignas(64) FdParams {
   int bf16x;                     // x, P1, P2 are bf16 (stage 2 runs in fp16 with P2 scaled, as K1)
 };
 // Phase-A geometry (the same tiles as fq_tq_tc05.cu): F = 1 -> n1 = n2 = 64, two tokens per tile;
-// F = 2 -> 112 x 128 (LLaMA-3-8B down_proj), one token.  Layout in shared memory from offset 0:
-// F = 1: X | P1 | P2 | A2 (48 KB, the widened-operand stages); F = 2: P2 | P1 | X with the stage-2
-// operand A2 written over P1 + X once the stage-1 MMA has read them (88 KB).
+// F = 2 -> 112 x 128 (LLaMA-3-8B down_proj), one token; F = 3 -> 64 x 128 (n = 8192, e.g. the
+// 70B models' attention and MLP inputs), two tokens as two M = 128 stage-1 groups.  Layout in shared
+// memory from offset 0: F = 1: X | P1 | P2 | A2 (48 KB, the widened-operand stages); F = 2, 3:
+// P2 | P1 | X with the stage-2 operand A2 written over P1 + X once the stage-1 MMA has read them
+// (88 / 72 KB, into the first packed ring stages).
 template <int F>
 struct FdGeo {
-  static constexpr int N1 = F == 2 ? 112 : 64, N2 = F == 2 ? 128 : 64;
+  static constexpr int N1 = F == 2 ? 112 : 64, N2 = F == 1 ? 64 : 128;
   static constexpr int TOK = N1 == 64 ? 2 : 1;
+  static constexpr int G1 = TOK * N2 / 128;                // stage-1 MMA groups (M = 128) per tile
   static constexpr int JB = N2 / 64, P1_ATOMS = (N1 + 63) / 64;
   static constexpr int X_BYTES = TOK * JB * N1 * 128, P1_BYTES = P1_ATOMS * N1 * 128, P2_BYTES = JB * N2 * 128;
   static constexpr int A2_BYTES = 2 * N2 * 128;
-  static constexpr bool ALIAS = F == 2;
+  static constexpr bool ALIAS = F != 1;
   static constexpr int OFF_P2 = ALIAS ? 0 : X_BYTES + P1_BYTES;
   static constexpr int OFF_P1 = ALIAS ? P2_BYTES : X_BYTES;
   static constexpr int OFF_X = ALIAS ? P2_BYTES + P1_BYTES : 0;
@@ -246,7 +250,7 @@ struct FdGeo {
   static constexpr uint32_t IDESC1 = tc::idesc_f16(128, N1, 0, 1, 1);   // fp16 x fp16 -> fp32, MN-major
   static constexpr uint32_t IDESC1_BF16 = tc::idesc_f16(128, N1, 1, 1, 1);
   static constexpr uint32_t IDESC2 = tc::idesc_f16(128, N2, 0, 1, 1);
-  static_assert(TOK * N2 == 128, "one M = 128 stage-1 group per tile");
+  static_assert(G1 == 1 || (N1 == 64 && N2 == 128), "two stage-1 groups only at 64 x 128");
   static_assert(!ALIAS || A2_BYTES <= P1_BYTES + X_BYTES, "A2 over P1 + X");
 };
 
@@ -291,7 +295,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   uint64_t* actready = fd2 + 1;            //        all tickets counted: codes and scales visible
   uint64_t* fdone = actready + 1;          //        F = 2: phase-A buffers free (ring stages usable)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1 + (FUSED ? 6 : 0));
-  using FG = FdGeo<FUSED == 2 ? 2 : 1>;
+  using FG = FdGeo<FUSED == 0 ? 1 : FUSED>;
   // FUSED phase A borrows the widened-operand stages (and, F = 2, the first packed ring stages)
   uint8_t* fsX = smem + FG::OFF_X;
   uint8_t* fsP1 = smem + FG::OFF_P1;
@@ -418,8 +422,8 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   if (warp == TMA_WARP) {
     // ======================= TMA producer =======================
     if (lane == 0) {
-      if (FUSED == 2 && ticket) {
-        // the 112 x 128 phase-A tile occupies the first packed ring stages: this CTA's weights
+      if (FG::ALIAS && ticket) {
+        // the 112 x 128 / 64 x 128 phase-A tile occupies the first packed ring stages: this CTA's weights
         // stream only once its transform tile is done (the other CTAs' from kernel start)
         if (!early_x) {
           tc::griddep_wait();
@@ -610,10 +614,14 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         const uint32_t xs = smem_u32(fsX), p1a = smem_u32(fsP1), p2a = smem_u32(fsP2), a2 = smem_u32(fsA2);
         constexpr uint32_t XLBO = FG::N2 == 64 ? FG::N1 * 128 : FG::TOK * FG::N1 * 128;
 #pragma unroll
-        for (int kk = 0; kk < FG::N1 / 16; ++kk)
-          tc::mma_ss<false>(tmem_base, tc::sdesc_sw128(xs + kk * 2048, XLBO, 1024),
-                            tc::sdesc_sw128(p1a + kk * 2048, FG::N1 * 128, 1024),
-                            fd.bf16x ? FG::IDESC1_BF16 : FG::IDESC1, kk > 0);
+        for (int g = 0; g < FG::G1; ++g) {               // 64 x 128: token g's M = 128 rows (j)
+          const uint32_t a0 = xs + uint32_t(FG::N2 == 64 ? 0 : g * FG::N1 * 128);
+#pragma unroll
+          for (int kk = 0; kk < FG::N1 / 16; ++kk)
+            tc::mma_ss<false>(tmem_base + uint32_t(g * FG::N1), tc::sdesc_sw128(a0 + kk * 2048, XLBO, 1024),
+                              tc::sdesc_sw128(p1a + kk * 2048, FG::N1 * 128, 1024),
+                              fd.bf16x ? FG::IDESC1_BF16 : FG::IDESC1, kk > 0);
+        }
         tc::mma_commit(fd1);
         tc::mbar_wait(fda2, 0);
         tc::fence_after();
@@ -681,34 +689,46 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
           tc::mbar_wait(fdx, 0);
           inv_p2 = qz::exp2i(-bf16_to_f16_pow2_group(fsP2, FG::P2_BYTES / 2, &fd_p2max, L, 128, 1));
         }
-        // stage 1: D lane (t, j), column i = W_t[i][j] (64 x 64: token t = L / 64)
+        // stage 1: D lane (t, j), column i = W_t[i][j] (64 x 64: token t = L / 64; 64 x 128: token g
+        // of stage-1 group g spans all 128 lanes)
         tc::mbar_wait(fd1, 0);
         tc::fence_after();
-        float m1 = 0.f;
+        int pe0 = 0, pe1 = 0;
 #pragma unroll
-        for (int c = 0; c < N1; c += 16) {
-          uint32_t v[16];
-          ld16(c, v);
+        for (int g = 0; g < FG::G1; ++g) {
+          const uint32_t dg = uint32_t(g * N1);
+          float m1 = 0.f;
 #pragma unroll
-          for (int e = 0; e < 16; e += 2)
-            m1 = qz::max3f(m1, fabsf(__uint_as_float(v[e])), fabsf(__uint_as_float(v[e + 1])));
-        }
-        const float4 r1 = exchange(m1);
-        const int pe0 = qz::prescale_exp(TOK == 2 ? fmaxf(r1.x, r1.y) : fmaxf(fmaxf(r1.x, r1.y), fmaxf(r1.z, r1.w)));
-        const int pe1 = TOK == 2 ? qz::prescale_exp(fmaxf(r1.z, r1.w)) : pe0;
-        const int tt = TOK == 2 ? (L >> 6) : 0;
-        const float pre = qz::exp2i(tt ? pe1 : pe0);
-        {
+          for (int c = 0; c < N1; c += 16) {
+            uint32_t v[16];
+            ld16(int(dg) + c, v);
+#pragma unroll
+            for (int e = 0; e < 16; e += 2)
+              m1 = qz::max3f(m1, fabsf(__uint_as_float(v[e])), fabsf(__uint_as_float(v[e + 1])));
+          }
+          const float4 r1 = exchange(m1);
+          const float all = fmaxf(fmaxf(r1.x, r1.y), fmaxf(r1.z, r1.w));
+          if (N2 == 64) {                                  // two tokens in the lane halves
+            pe0 = qz::prescale_exp(fmaxf(r1.x, r1.y));
+            pe1 = qz::prescale_exp(fmaxf(r1.z, r1.w));
+          } else if (g == 0) {
+            pe0 = qz::prescale_exp(all);
+            pe1 = pe0;
+          } else {
+            pe1 = qz::prescale_exp(all);
+          }
+          const int tg = N2 == 64 ? (L >> 6) : g;          // token of this thread's row in group g
+          const float pre = qz::exp2i(tg ? pe1 : pe0);
           const int j = N2 == 64 ? (L & 63) : L;           // K row j' of the stage-2 A operand
           const uint32_t row = smem_u32(fsA2) + uint32_t(j * 128);
 #pragma unroll
           for (int c = 0; c < N1; c += 16) {
             uint32_t v[16];
-            ld16(c, v);
+            ld16(int(dg) + c, v);
 #pragma unroll
             for (int e = 0; e < 16; e += 8) {
               const int c8 = (c + e) >> 3, ch = c8 & 7;
-              const int atom = N1 == 64 ? tt : (c8 >> 3);    // 64-element M atoms of A2
+              const int atom = N1 == 64 ? tg : (c8 >> 3);    // 64-element M atoms of A2
               tc::sts128(row + uint32_t(atom * (N2 * 128) + ((ch ^ (j & 7)) << 4)),
                          pack_half2(__uint_as_float(v[e + 0]) * pre, __uint_as_float(v[e + 1]) * pre),
                          pack_half2(__uint_as_float(v[e + 2]) * pre, __uint_as_float(v[e + 3]) * pre),
@@ -717,6 +737,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
             }
           }
         }
+        const int tt = TOK == 2 ? (L >> 6) : 0;            // stage 2: token of this thread's row
         tc::fence_proxy_async_smem();
         tc::fence_before();
         __syncwarp();
@@ -762,7 +783,7 @@ gemm_dec_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
           if (store) *reinterpret_cast<uint4*>(qrow + c / 2) = make_uint4(w[0], w[1], w[2], w[3]);
         }
         if (store && i == 0) fd.s[t] = mp > 0.f ? fd.alpha * (mp * inv_pre * inv_p2) / 7.0f : 1.0f;
-        if constexpr (FUSED == 2) {                        // TMEM and the phase-A buffers are free
+        if constexpr (FG::ALIAS) {                         // TMEM and the phase-A buffers are free
           tc::fence_before();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(fdone);
@@ -1094,7 +1115,7 @@ cudaError_t gemm_dec_launch(const GemmArgs& a, int split) {
 
 bool fused_dec_supported(const GemmArgs& a, int n1, int n2, bool x_bf16, const void* p2) {
   (void)x_bf16;                                    // fp16 and bf16 activations (bf16: P2 scaled, K1)
-  const bool shape = (n1 == 64 && n2 == 64) || (n1 == 112 && n2 == 128);
+  const bool shape = (n1 == 64 && n2 == 64) || (n1 == 112 && n2 == 128) || (n1 == 64 && n2 == 128);
   return shape && p2 != nullptr && a.za == nullptr && !a.out_i32 && gemm_dec_supported(a) &&
          a.K == n1 * n2;
 }
@@ -1102,6 +1123,7 @@ bool fused_dec_supported(const GemmArgs& a, int n1, int n2, bool x_bf16, const v
 cudaError_t fused_dec_launch(const GemmArgs& a, const FdArgs& f) {
   const int split = dec_env_split();
   if (f.n1 == 112) return dec_deep(a) ? dec_launch_cfg<1, 2>(a, split, &f) : dec_launch_cfg<0, 2>(a, split, &f);
+  if (f.n2 == 128) return dec_deep(a) ? dec_launch_cfg<1, 3>(a, split, &f) : dec_launch_cfg<0, 3>(a, split, &f);
   return dec_deep(a) ? dec_launch_cfg<1, 1>(a, split, &f) : dec_launch_cfg<0, 1>(a, split, &f);
 }
 

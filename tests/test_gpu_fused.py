@@ -193,6 +193,25 @@ def _inputs_g(T, N, n1, n2, seed):
 
 
 @pytest.mark.parametrize("T", [1, 2, 5, 17, 32, 63, 64])
+@pytest.mark.parametrize("N", [8192, 10240])
+def test_fused_decode_64x128_bit_identical(T, N):
+    """n = 8192 = 64 x 128 (the 70B models' hidden size): two tokens per ticket tile as two M = 128
+    stage-1 groups, the phase-A tile over the first packed ring stages"""
+    n1, n2 = 64, 128
+    x, p1, p2, qw, sw = _inputs_g(T, N, n1, n2, seed=500 + T)
+    y = torch.empty((T, N), dtype=torch.float16, device=DEV)
+    q = torch.full((T, n1 * n2 // 2), 0xAB, dtype=torch.uint8, device=DEV)
+    s = torch.full((T,), -1.0, dtype=torch.float32, device=DEV)
+    n0 = fq.fq_launch_count()
+    fq.fq_flatquant_linear(x, n1, n2, p1, p2, 0.9, qw, sw, y, q, s)
+    assert fq.fq_launch_count() - n0 == 1
+    q2, s2 = fq.transform_quant(x, n1, n2, p1, p2, 0.9)
+    y2 = fq.w4a4_linear(q2, s2, qw, sw)
+    torch.cuda.synchronize()
+    assert torch.equal(q, q2) and torch.equal(s, s2) and torch.equal(y, y2)
+
+
+@pytest.mark.parametrize("T", [1, 2, 5, 17, 32, 63, 64])
 @pytest.mark.parametrize("N", [4096, 5120])
 def test_fused_decode_112x128_bit_identical(T, N):
     """LLaMA-3-8B down_proj (14336 = 112 x 128): one token per ticket tile, the phase-A tile over
@@ -235,7 +254,7 @@ def test_fused_decode_112x128_chain_with_64x64():
         assert torch.equal(y, y2)
 
 
-@pytest.mark.parametrize("n1,n2,N", [(64, 64, 4096), (112, 128, 4096)])
+@pytest.mark.parametrize("n1,n2,N", [(64, 64, 4096), (112, 128, 4096), (64, 128, 8192)])
 @pytest.mark.parametrize("T", [1, 9, 64])
 @pytest.mark.parametrize("p2_scale", [1.0, 1e5])
 def test_fused_decode_bf16_bit_identical(n1, n2, N, T, p2_scale):
