@@ -171,8 +171,9 @@ fq_status fq_w4a4_gemm_i32(const uint8_t* qa, int64_t T, int32_t K, const uint8_
  * reads the codes once all tiles are published.  Tile
  * publication uses a {arrivals, departures} counter pair from a ring of 1024 slots per device in
  * the library's own device memory, reset by the last CTA of each launch (so CUDA-graph replay is
- * safe); at most 1024 fused launches may be in flight on one device at a time.  Every other
- * shape, dtype or T runs the two kernels.
+ * safe); at most 1024 fused launches may be in flight on one device at a time.  The fused
+ * launch also needs its whole grid resident at once (N <= 37888: 128 outputs per CTA, two
+ * CTAs per SM) and at least one CTA per tile.  Every other shape, dtype, T or N runs the two kernels.
  * ------------------------------------------------------------------------------------- */
 fq_status fq_flatquant_linear(const void* x, int32_t x_dtype, int64_t T, int32_t n1,
                               int32_t n2, const void* p1, const void* p2, float alpha,

@@ -212,8 +212,9 @@ FQ_DEVICE void convert_chunk(uint32_t src, uint32_t dst_rows, int row, int c, in
 // the start of the kernel and loads the activation codes once the count is complete.  The
 // counter pair (arrivals, departures) lives in a ring of slots in this module's device memory
 // and is reset by the last CTA to leave, so a slot is reusable by a later launch (and by a CUDA
-// graph replay).  Ticket CTAs are the lowest block indices and the grid is sized to be resident
-// at once (dec_pick_split), so the tickets can always run.
+// graph replay).  Ticket CTAs are the lowest block indices; the launcher runs the fused kernel
+// only when the whole grid fits on the device at once (larger grids take the two-kernel path),
+// so the tickets can always run whatever order the blocks are dispatched in.
 constexpr int FD_SLOTS = 1024;
 __device__ unsigned g_fd_sync[2 * FD_SLOTS];
 
@@ -939,6 +940,29 @@ static int dec_policy() {                         // FQ_DEC_POLICY: testing aid 
   return p;
 }
 
+// CTAs of a kernel resident on one SM at once, from its threads, registers, shared memory and
+// TMEM columns.  (cudaOccupancyMaxActiveBlocksPerMultiprocessor reports 1 for every kernel that
+// contains tcgen05.alloc, whatever its resources; scripts/probes/occ_tc05.cu measures 2-4 such
+// CTAs running concurrently on one SM, so the limits are computed here.)
+static int resident_ctas_per_sm(const void* kern, int threads, size_t dyn_smem, int tmem_cols) {
+  cudaFuncAttributes fa{};
+  int dev = 0, thr = 0, regs = 0, smem = 0, rsv = 0;
+  if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess || cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&thr, cudaDevAttrMaxThreadsPerMultiProcessor, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&regs, cudaDevAttrMaxRegistersPerMultiprocessor, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  const int warps = (threads + 31) / 32;
+  const int regs_per_warp = ((fa.numRegs * 32 + 255) / 256) * 256;   // 256-register allocation unit
+  const size_t smem_per_cta = dyn_smem + fa.sharedSizeBytes + size_t(rsv);
+  int n = std::min({thr / threads, regs / std::max(1, regs_per_warp * warps), int(size_t(smem) / smem_per_cta),
+                    512 / std::max(32, tmem_cols)});
+  return std::max(1, n);
+}
+
 // How many clusters of S CTAs the hardware keeps resident at once (cluster placement is bounded
 // by the GPC structure, not only by the per-SM limits); cached per (configuration, S).
 template <int CFG, int FUSED>
@@ -1077,6 +1101,16 @@ static cudaError_t dec_launch_cfg(const GemmArgs& a, int split, const FdArgs* f)
     if (!fd.sync) return cudaErrorInvalidValue;
   }
   if (cudaError_t e = ensure_smem_attr(kern, int(DC::SMEM), attr_done[which]); e != cudaSuccess) return e;
+  if constexpr (FUSED != 0) {
+    // forward progress: the GEMM CTAs wait for the ticket CTAs, so the whole grid must fit on
+    // the device at once (the CUDA model does not promise that blocks are dispatched in index
+    // order); larger grids run the two kernels (nothing launched here)
+    static std::atomic<int> occ[5];               // per kernel variant (0: not computed yet)
+    if (occ[which].load(std::memory_order_relaxed) == 0)
+      occ[which].store(resident_ctas_per_sm(reinterpret_cast<const void*>(kern), THREADS, DC::SMEM, DC::TMEM_COLS),
+                       std::memory_order_relaxed);
+    if (fbs * S > occ[which].load(std::memory_order_relaxed) * num_sms()) return cudaErrorNotSupported;
+  }
   static const bool dbg = std::getenv("FQ_DEC_DEBUG") != nullptr;
   if (dbg)
     std::fprintf(stderr, "[fq] decode GEMM%s N=%d K=%d T=%lld: config %d, split %d, %d CTAs, max resident clusters %d\n",

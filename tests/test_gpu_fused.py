@@ -273,3 +273,19 @@ def test_fused_decode_bf16_bit_identical(n1, n2, N, T, p2_scale):
     y2 = fq.w4a4_linear(q2, s2, qw, sw, out_dtype=torch.bfloat16)
     torch.cuda.synchronize()
     assert torch.equal(q, q2) and torch.equal(s, s2) and torch.equal(y, y2)
+
+
+@pytest.mark.parametrize("T,N,fused", [(64, 128, False), (64, 256, False), (16, 128, True),
+                                       (1, 65536, False), (64, 65536, False), (64, 37888, True)])
+def test_fused_decode_falls_back_outside_its_limits(T, N, fused):
+    """one CTA per tile and the whole grid resident at once (the GEMM CTAs wait for the ticket
+    CTAs): outside that the linear runs the two kernels, with the same bits"""
+    x, p1, p2, qw, sw = _inputs(T, N, seed=900 + T)
+    n0 = fq.fq_launch_count()
+    y, q, s = _fused(x, p1, p2, 0.9, qw, sw)
+    assert fq.fq_launch_count() - n0 == (1 if fused else 2)
+    y2, q2, s2 = _two_kernels(x, p1, p2, 0.9, qw, sw)
+    torch.cuda.synchronize()
+    assert torch.equal(q, q2)
+    assert torch.equal(s, s2)
+    assert torch.equal(y, y2)
