@@ -75,6 +75,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--alpha", type=float, default=0.9)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-streams", type=int, default=2, help="streams the e2e step's linears rotate over")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp16", action="store_true")
     ap.add_argument("--no-kv", action="store_true", help="skip the KV-cache quantization measurement")
@@ -573,7 +574,7 @@ def run_ours(args):
         # overlaps the next one's H2D copy (PCIe is full duplex) and compute; every linear has
         # its own staging buffers.  The step ends when both streams are done.  (Splitting each
         # linear into 4 token chunks was measured slower: 0.47 vs 0.51 M tokens/s on C3.)
-        e2e_streams = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+        e2e_streams = [torch.cuda.Stream(device=dev) for _ in range(max(1, args.e2e_streams))]
 
         def e2e_step():
             start = torch.cuda.Event()
@@ -583,7 +584,7 @@ def run_ours(args):
             for i, (L, x_h, y_h, x_d) in enumerate(zip(layers, hx, hy, dx)):
                 lin = L["lin"]
                 fq.fq_flatquant_linear_host(x_h, x_d, lin.n1, lin.n2, L["p1"], L["p2"], args.alpha, L["qw"], L["sw"],
-                                            y_h, L["y"], L["q"], L["s"], stream=e2e_streams[i % 2], sync=False)
+                                            y_h, L["y"], L["q"], L["s"], stream=e2e_streams[i % len(e2e_streams)], sync=False)
             for st in e2e_streams:
                 done = torch.cuda.Event()
                 done.record(st)

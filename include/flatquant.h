@@ -174,6 +174,9 @@ fq_status fq_w4a4_gemm_i32(const uint8_t* qa, int64_t T, int32_t K, const uint8_
  * safe); at most 1024 fused launches may be in flight on one device at a time.  The fused
  * launch also needs its whole grid resident at once (N <= 37888: 128 outputs per CTA, two
  * CTAs per SM) and at least one CTA per tile.  Every other shape, dtype, T or N runs the two kernels.
+ * Fused launches running concurrently on several streams also rely on each grid's first blocks
+ * (the tickets) being dispatched no later than its others, as the hardware does (tests run three
+ * streams); a CTA that waits more than ~35 s for the tiles traps (a launch error), it does not hang.
  * ------------------------------------------------------------------------------------- */
 fq_status fq_flatquant_linear(const void* x, int32_t x_dtype, int64_t T, int32_t n1,
                               int32_t n2, const void* p1, const void* p2, float alpha,
