@@ -75,7 +75,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--alpha", type=float, default=0.9)
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-streams", type=int, default=2, help="streams the e2e step's linears rotate over")
+    ap.add_argument("--e2e-streams", type=int, default=4, help="streams the e2e step's linears rotate over")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp16", action="store_true")
     ap.add_argument("--no-kv", action="store_true", help="skip the KV-cache quantization measurement")
@@ -570,10 +570,12 @@ def run_ours(args):
         hy = [torch.empty(L["y"].shape, dtype=L["y"].dtype).pin_memory() for L in layers]
         dx = [torch.empty_like(L["x"]) for L in layers]
 
-        # two streams: the linears of a step alternate between them, so one linear's D2H copy
-        # overlaps the next one's H2D copy (PCIe is full duplex) and compute; every linear has
-        # its own staging buffers.  The step ends when both streams are done.  (Splitting each
-        # linear into 4 token chunks was measured slower: 0.47 vs 0.51 M tokens/s on C3.)
+        # one stream per linear (the four linears of a step are independent inputs here): every
+        # H2D copy is queued at once and each linear's D2H overlaps the others' copies and compute
+        # (PCIe is full duplex); every linear has its own staging buffers.  The step ends when all
+        # streams are done.  Measured e2e (same box): C4 1 / 2 / 4 streams 0.190 / 0.215 / 0.240 M
+        # tokens/s, C3 0.369 / 0.520 / 0.540 M.  (Splitting each linear into 4 token chunks was
+        # measured slower: 0.47 vs 0.51 M tokens/s on C3.)
         e2e_streams = [torch.cuda.Stream(device=dev) for _ in range(max(1, args.e2e_streams))]
 
         def e2e_step():
