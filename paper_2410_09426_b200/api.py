@@ -23,13 +23,20 @@ __all__ = [
 
 
 def _ptr(t):
-    return None if t is None else ctypes.c_void_p(t.data_ptr())
+    return None if t is None else t.data_ptr()     # the argtypes are c_void_p (_lib.py)
 
 
-def _stream(stream) -> ctypes.c_void_p:
-    if stream is None:
-        stream = torch.cuda.current_stream()
-    return ctypes.c_void_p(stream.cuda_stream)
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
+def _stream(stream) -> int:
+    """the cudaStream_t handle: `stream`, else the current stream of the current device (read
+    without building a torch.cuda.Stream object: a decode-size call is otherwise host-bound)"""
+    if stream is not None:
+        return stream.cuda_stream
+    if _raw_stream is not None:
+        return _raw_stream(torch.cuda.current_device())
+    return torch.cuda.current_stream().cuda_stream
 
 
 def _fq_dtype(dt: torch.dtype) -> int:
