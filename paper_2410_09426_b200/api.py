@@ -62,15 +62,21 @@ def _buf(t, name, shape, dtype):
     """An output/parameter buffer the C ABI addresses as a dense row-major array of `shape`."""
     if t is None:
         return
-    _need(tuple(t.shape) == tuple(shape), f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
-    _need(t.dtype == dtype, f"{name}: dtype {t.dtype}, expected {dtype}")
-    _need(t.is_contiguous(), f"{name} must be contiguous")
+    # messages are formatted only on failure (this runs for every buffer of every call)
+    if t.shape != shape:
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if t.dtype != dtype:
+        raise ValueError(f"{name}: dtype {t.dtype}, expected {dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
 
 
 def _rows(x, name, min_cols):
     """A [rows, >= min_cols] matrix with unit column stride (the row stride is passed)."""
-    _need(x.dim() == 2 and x.stride(1) == 1, f"{name} must be 2-D with unit column stride")
-    _need(x.shape[1] >= min_cols, f"{name}: {x.shape[1]} columns < {min_cols}")
+    if not (x.dim() == 2 and x.stride(1) == 1):
+        raise ValueError(f"{name} must be 2-D with unit column stride")
+    if x.shape[1] < min_cols:
+        raise ValueError(f"{name}: {x.shape[1]} columns < {min_cols}")
 
 
 # ------------------------------------------------------------------ raw entry points
