@@ -48,7 +48,8 @@
  *    fused decode linear count through per-launch counter pairs taken round-robin from rings of
  *    1024 slots per device in the library's own (module) device memory; each launch's last CTA
  *    resets its slot, so CUDA-graph replays are safe.  At most 1024 such launches of each kind
- *    may be in flight on one device at a time.
+ *    may be in flight on one device at a time; a captured launch keeps the slot it was given at
+ *    capture, so one graph must not be replayed concurrently with itself (on two streams).
  *  - Non-finite inputs give unspecified codes (the oracle's precondition is finite x).
  */
 #ifndef FLATQUANT_H_
