@@ -1,6 +1,6 @@
 """Host-side cost of the Python binding + C-ABI enqueue for one linear at a decode size small
-enough (T = 1, N = 512) that the device never backs the launch queue up: is an eager decode call
-host-bound, and what does the binding add to the raw ctypes call?"""
+(T = 1, N = 512), enqueued behind a device sleep so the host time is the enqueue alone: is an
+eager decode call host-bound, and what does the binding add to the raw ctypes call?"""
 import ctypes
 import os
 import sys
@@ -30,13 +30,14 @@ def timed(label, fn):
     for _ in range(20):
         fn()
     torch.cuda.synchronize()
+    torch.cuda._sleep(200_000_000)      # ~0.1 s: the device holds the queue, so host time is enqueue only
     t0 = time.perf_counter()
     for _ in range(n):
         fn()
     t1 = time.perf_counter()
     torch.cuda.synchronize()
     t2 = time.perf_counter()
-    print(f"{label:58s} host {(t1 - t0) / n * 1e6:6.1f} us/call, drained {(t2 - t0) / n * 1e6:6.1f} us/call")
+    print(f"{label:58s} host (enqueue only) {(t1 - t0) / n * 1e6:6.1f} us/call")
 
 
 timed("fq_flatquant_linear (binding, current stream)",
