@@ -48,7 +48,8 @@ def ncu_traffic(cfg_name, linears, kind):
     """DRAM bytes (read + write) of one step's `kind` launches ("gemm" or "tq") from the committed
     ncu --set full captures (profiles/ncu_traffic.json, scripts/make_profiles.py), or None."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if cfg_name != "C3" or not os.path.exists(path):
+    # the captures are of C3's shapes (gemm_*, tq_*) and of C4's fused decode linears (fused_*)
+    if (cfg_name, kind) not in (("C3", "gemm"), ("C3", "tq"), ("C4", "fused")) or not os.path.exists(path):
         return None
     t = json.load(open(path))
     keys = [f"{kind}_{lin.name}" for lin in linears]
@@ -632,7 +633,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args.config, args.alpha)
 
-    gemm_traffic = ncu_traffic(args.config, [L["lin"] for L in layers], "gemm")
+    gemm_traffic = ncu_traffic(args.config, [L["lin"] for L in layers], "fused" if all(fused) else "gemm")
     tq_traffic = ncu_traffic(args.config, [L["lin"] for L in layers], "tq")
     decode = T <= 64     # decode step (C4): the GEMM streams the weights, HBM-bound (SURVEY 8(a) sizes)
     g_bytes = sum(fused_bytes(T, L["lin"]) if fused[i] else gemm_min_bytes(T, L["lin"]) for i, L in enumerate(layers))
@@ -641,8 +642,10 @@ def run_ours(args):
         kname = "fq_w4a4_linear (decode kernel: tcgen05 kind::i8, cluster split-K)"
         if any(fused):
             kname = ("decode GEMM launches: fq_flatquant_linear fused (transform + tcgen05 kind::i8 GEMM, "
-                     + ", ".join(L["lin"].name for i, L in enumerate(layers) if fused[i]) + "), fq_w4a4_linear ("
-                     + ", ".join(L["lin"].name for i, L in enumerate(layers) if not fused[i]) + ")")
+                     + ", ".join(L["lin"].name for i, L in enumerate(layers) if fused[i]) + ")")
+            if not all(fused):
+                kname += (", fq_w4a4_linear ("
+                          + ", ".join(L["lin"].name for i, L in enumerate(layers) if not fused[i]) + ")")
         roof = {"bound": "hbm", "kernel": kname,
                 "achieved": round(g_gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": round(g_gbs / pk["hbm_gbs"], 4), "traffic": gemm_traffic,
