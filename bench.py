@@ -48,11 +48,13 @@ def ncu_traffic(cfg_name, linears, kind):
     """DRAM bytes (read + write) of one step's `kind` launches ("gemm" or "tq") from the committed
     ncu --set full captures (profiles/ncu_traffic.json, scripts/make_profiles.py), or None."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    # the captures are of C3's shapes (gemm_*, tq_*) and of C4's fused decode linears (fused_*)
-    if (cfg_name, kind) not in (("C3", "gemm"), ("C3", "tq"), ("C4", "fused")) or not os.path.exists(path):
+    # the captures are of C3's shapes (gemm_*, tq_*) and of C4's fused decode linears (fused_*);
+    # C2's one linear (2048 x 4096 -> 4096, 64 x 64) is C3's o_proj shape, so its capture serves
+    if (cfg_name, kind) not in (("C2", "gemm"), ("C2", "tq"), ("C3", "gemm"), ("C3", "tq"), ("C4", "fused")) \
+            or not os.path.exists(path):
         return None
     t = json.load(open(path))
-    keys = [f"{kind}_{lin.name}" for lin in linears]
+    keys = [f"{kind}_P_o" if cfg_name == "C2" else f"{kind}_{lin.name}" for lin in linears]
     if not all(k in t for k in keys):
         return None
     return {"bytes_per_step": int(sum(t[k]["dram_bytes"] for k in keys)),
